@@ -1,0 +1,132 @@
+// sg_gen.cu -- device input generation bit-exact with the reference
+// generators (gen.py), plus small helpers.
+//
+// KISS64 (gen.py:30-64) is a sum of three recurrences; the caller computes
+// the jump-ahead state of every chunk on the host (paper_1002_4482_b200/gen.py)
+// and each thread then runs the exact scalar recurrence over its chunk, so
+// draw j of the device stream equals draw j of kiss_batch().
+#include "sg_internal.cuh"
+
+namespace sg {
+
+__global__ void __launch_bounds__(128) k_kiss(const unsigned long long* __restrict__ states, unsigned long long chunks,
+                                              unsigned long long chunk_len, unsigned long long n,
+                                              unsigned long long* __restrict__ out) {
+    const unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= chunks) return;
+    unsigned long long x = states[4 * k + 0], y = states[4 * k + 1], z = states[4 * k + 2], c = states[4 * k + 3];
+    const unsigned long long a = k * chunk_len;
+    unsigned long long b = a + chunk_len;
+    if (b > n) b = n;
+    for (unsigned long long j = a; j < b; ++j) {
+        // multiply-with-carry
+        const unsigned long long t = (x << 58) + c;
+        c = x >> 6;
+        x += t;
+        c += (x < t) ? 1ull : 0ull;
+        // xorshift
+        y ^= y << 13;
+        y ^= y >> 17;
+        y ^= y << 43;
+        // congruential
+        z = 6906969069ull * z + 1234567ull;
+        out[j] = x + y + z;
+    }
+}
+
+template <class T>
+__global__ void k_list_from_order(const long long* __restrict__ perm, unsigned long long n, T* __restrict__ succ) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const unsigned long long a = j == 0 ? 0ull : 1ull + (unsigned long long)perm[j - 1];
+        const unsigned long long b = (j + 1 < n) ? 1ull + (unsigned long long)perm[j] : a;
+        succ[a] = (T)b;
+    }
+}
+
+__global__ void k_edge_keys(const unsigned long long* __restrict__ draws, unsigned long long pairs,
+                            unsigned long long n, long long* __restrict__ keys) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+        const unsigned long long u = draws[2 * i] % n;
+        const unsigned long long v = draws[2 * i + 1] % n;
+        keys[i] = u == v ? -1ll : (long long)((u < v ? u : v) * n + (u < v ? v : u));
+    }
+}
+
+__global__ void k_edges_from_keys(const long long* __restrict__ keys, unsigned long long m, unsigned long long n,
+                                  long long* __restrict__ edges) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const unsigned long long k = (unsigned long long)keys[i];
+        edges[2 * i] = (long long)(k / n);
+        edges[2 * i + 1] = (long long)(k % n);
+    }
+}
+
+__global__ void k_gather_i64(const long long* __restrict__ src, const long long* __restrict__ idx,
+                             unsigned long long k, long long* __restrict__ out) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride)
+        out[i] = src[idx[i]];
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int sg_kiss_device(const uint64_t* states, uint64_t chunks, uint64_t chunk_len, uint64_t n, uint64_t* out,
+                   void* stream) {
+    if (chunks == 0 || n == 0) return SG_OK;
+    if (chunk_len == 0 || (chunks - 1) * chunk_len >= n + chunk_len) return SG_ERR_VALUE;
+    const uint32_t g = (uint32_t)((chunks + 127) / 128);
+    k_kiss<<<g, 128, 0, (cudaStream_t)stream>>>((const unsigned long long*)states, chunks, chunk_len, n,
+                                                (unsigned long long*)out);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+int sg_list_from_order(const int64_t* perm, uint64_t n, void* succ, int succ_dtype, void* stream) {
+    if (n == 0) return SG_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t g = grid_for(n, 256, 1, kSMs * 8);
+    const long long* p = (const long long*)perm;
+    switch (succ_dtype) {
+        case SG_U32: k_list_from_order<uint32_t><<<g, 256, 0, s>>>(p, n, (uint32_t*)succ); break;
+        case SG_I32: k_list_from_order<int32_t><<<g, 256, 0, s>>>(p, n, (int32_t*)succ); break;
+        case SG_I64: k_list_from_order<long long><<<g, 256, 0, s>>>(p, n, (long long*)succ); break;
+        default: return SG_ERR_VALUE;
+    }
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+int sg_edge_keys(const uint64_t* draws, uint64_t pairs, uint64_t n, int64_t* keys, void* stream) {
+    if (pairs == 0) return SG_OK;
+    if (n == 0) return SG_ERR_VALUE;
+    k_edge_keys<<<grid_for(pairs, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+        (const unsigned long long*)draws, pairs, n, (long long*)keys);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+int sg_edges_from_keys(const int64_t* keys, uint64_t m, uint64_t n, int64_t* edges, void* stream) {
+    if (m == 0) return SG_OK;
+    if (n == 0) return SG_ERR_VALUE;
+    k_edges_from_keys<<<grid_for(m, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+        (const long long*)keys, m, n, (long long*)edges);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+int sg_gather_i64(const int64_t* src, const int64_t* idx, uint64_t k, int64_t* out, void* stream) {
+    if (k == 0) return SG_OK;
+    k_gather_i64<<<grid_for(k, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+        (const long long*)src, (const long long*)idx, k, (long long*)out);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,831 @@
+// sg_list.cu -- list ranking on sm_100a.
+//
+//  * Wyllie pointer jumping (reference: listrank.py:75-155) over packed
+//    64-bit {rank:32 | succ:32} words, updated in place.  Asynchronous
+//    in-place jumping is sound because a word is always read and written as
+//    one 64-bit access: whichever version of w[s] a node sees, its
+//    (distance, pointer) pair stays consistent and its pointer distance at
+//    least doubles per launch, so ceil(log2 n) launches still suffice.
+//    Converged nodes (pointer at the tail) are skipped without a gather.
+//
+//  * Recursive sparse ruling set (reference RS1..RS5: listrank.py:197-408).
+//    Level 0 walks the input list from a hashed ruling set (every ~2^kbits-th
+//    node id, Fibonacci hashing, node 0 always included), writing one packed
+//    {owner:32 | local:32} word per node and one {next ruler, sublist
+//    weight} pair per ruler.  The ruler list is ranked the same way
+//    (weighted) until it fits one CTA, which finishes it with weighted
+//    pointer jumping; expand passes then turn inclusive suffix sums back
+//    into ranks.  Per node the level-0 walk costs one dependent random load
+//    (succ[cur]) and one random 8-byte store; the ruler test is ALU-only.
+//
+// Validation happens inside the pipeline (no host round trip): range / tail
+// census in the first pass, and "the head's weighted pointer reaches the
+// tail with inclusive sum n" at the top level -- together equivalent to
+// core.validate_list (core.py:148-167).  A walk that exceeds the hop cap
+// (a cycle without rulers, or a pathological layout) makes the host re-run
+// the list with Wyllie, which terminates on any input.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <stdlib.h>
+#include <string.h>
+
+#include "sg_internal.cuh"
+
+namespace sg {
+
+constexpr uint32_t PHI = 0x9E3779B9u;
+constexpr int TILE_THREADS = 256;
+constexpr int TILE_ITEMS = 16;
+constexpr int TILE = TILE_THREADS * TILE_ITEMS;
+constexpr uint32_t FINAL_CAP = 8192;          // ruler list handled by one CTA
+constexpr uint32_t WALK_CAP_HOPS = 1u << 16;  // longer walk => Wyllie fallback
+constexpr int WALK_THREADS = 256;
+constexpr int JUMP_THREADS = 256;
+
+// ---------------------------------------------------------------------------
+// element access helpers
+
+template <class T>
+__device__ __forceinline__ unsigned long long as_index(T v);
+template <>
+__device__ __forceinline__ unsigned long long as_index<uint32_t>(uint32_t v) { return v; }
+template <>
+__device__ __forceinline__ unsigned long long as_index<int32_t>(int32_t v) {
+    return (unsigned long long)(long long)v;
+}
+template <>
+__device__ __forceinline__ unsigned long long as_index<int64_t>(int64_t v) {
+    return (unsigned long long)v;
+}
+
+__device__ __forceinline__ bool is_ruler(uint32_t i, uint32_t kbits, uint32_t salt) {
+    return i == 0u || ((i * PHI + salt) >> (32u - kbits)) == 0u;
+}
+
+// level-0 view: node i -> (successor, weight 1)
+template <class SuccT>
+struct Level0 {
+    const SuccT* succ;
+    __device__ __forceinline__ void load(uint32_t i, unsigned long long& nx, uint32_t& w) const {
+        nx = as_index<SuccT>(__ldg(succ + i));
+        w = 1u;
+    }
+};
+
+// level-k view: ruler i -> (next ruler, sublist weight); next == i at the tail
+struct LevelK {
+    const uint2* lvl;
+    __device__ __forceinline__ void load(uint32_t i, unsigned long long& nx, uint32_t& w) const {
+        uint2 e = lvl[i];
+        nx = e.x;
+        w = e.y;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// status
+
+__global__ void k_status_init(ListStatus* st, unsigned long long n) {
+    if (threadIdx.x == 0) {
+        st->oor_first = NONE64;
+        st->loop_first = NONE64;
+        st->loop_count = 0;
+        st->overflow = 0;
+        st->head_sum = 0;
+        st->head_ok = 0;
+        st->bad = 0;
+        st->pad = 0;
+    }
+    if (threadIdx.x <= SG_MAX_LEVELS) {
+        st->R[threadIdx.x] = threadIdx.x == 0 ? n : 0;
+        st->qhead[threadIdx.x] = 0;
+    }
+}
+
+__device__ __forceinline__ void note_succ(ListStatus* st, unsigned long long i, unsigned long long v,
+                                          unsigned long long n) {
+    if (v >= n) {
+        atomicMin(&st->oor_first, i);
+    } else if (v == i) {
+        atomicAdd(&st->loop_count, 1ull);
+        atomicMin(&st->loop_first, i);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Wyllie
+
+template <class SuccT>
+__global__ void __launch_bounds__(JUMP_THREADS) k_wy_init(const SuccT* __restrict__ succ,
+                                                          unsigned long long* __restrict__ word,
+                                                          unsigned long long n, ListStatus* st) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        unsigned long long v = as_index<SuccT>(succ[i]);
+        note_succ(st, i, v, n);
+        if (v >= n) v = i;  // neutralise: never gather out of range
+        word[i] = ((unsigned long long)(v != i) << 32) | v;
+    }
+}
+
+__device__ __forceinline__ uint32_t wy_tail(const ListStatus* st) {
+    const unsigned long long lc = *(volatile const unsigned long long*)&st->loop_count;
+    const unsigned long long lf = *(volatile const unsigned long long*)&st->loop_first;
+    return lc == 1 ? (uint32_t)lf : NIL;
+}
+
+// one jump round, in place; `rank` != nullptr on the last round (extracts ranks)
+template <class OutT>
+__global__ void __launch_bounds__(JUMP_THREADS) k_wy_jump(unsigned long long* word, unsigned long long n,
+                                                          const ListStatus* st, OutT* __restrict__ rank) {
+    constexpr int U = 4;
+    const uint32_t tail = wy_tail(st);
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i0 < n; i0 += stride * U) {
+        unsigned long long w[U];
+        bool live[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long i = i0 + (unsigned long long)u * stride;
+            w[u] = i < n ? word[i] : 0ull;
+            const uint32_t s = (uint32_t)w[u];
+            live[u] = i < n && s != tail && (unsigned long long)s != i;
+        }
+        unsigned long long w2[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) w2[u] = live[u] ? __ldcg(word + (uint32_t)w[u]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long i = i0 + (unsigned long long)u * stride;
+            if (live[u]) {
+                const unsigned long long rk = ((w[u] >> 32) + (w2[u] >> 32)) & 0xFFFFFFFFull;
+                w[u] = (rk << 32) | (w2[u] & 0xFFFFFFFFull);
+                word[i] = w[u];
+            }
+            if (rank != nullptr && i < n) rank[i] = (OutT)(w[u] >> 32);
+        }
+    }
+}
+
+__global__ void k_wy_check(const unsigned long long* word, unsigned long long n, ListStatus* st) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const uint32_t tail = wy_tail(st);
+        const unsigned long long w0 = word[0];
+        st->head_ok = ((uint32_t)w0 == tail) ? 1ull : 0ull;
+        st->head_sum = (w0 >> 32) + 1;  // inclusive count of nodes from the head
+    }
+}
+
+// single CTA: init, `rounds` in-place jump rounds separated by block
+// barriers, rank extraction (listrank.py:120-150)
+template <class SuccT, class OutT>
+__global__ void __launch_bounds__(1024) k_wy_single(const SuccT* __restrict__ succ, unsigned long long* word,
+                                                    unsigned long long n, ListStatus* st, OutT* __restrict__ rank,
+                                                    int rounds) {
+    for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x) {
+        unsigned long long v = as_index<SuccT>(succ[i]);
+        note_succ(st, i, v, n);
+        if (v >= n) v = i;
+        word[i] = ((unsigned long long)(v != i) << 32) | v;
+    }
+    __threadfence();
+    __syncthreads();
+    const uint32_t tail = wy_tail(st);
+    for (int r = 0; r < rounds; ++r) {
+        for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x) {
+            unsigned long long w = __ldcg(word + i);
+            const uint32_t s = (uint32_t)w;
+            if (s != tail && (unsigned long long)s != i) {
+                const unsigned long long w2 = __ldcg(word + s);
+                const unsigned long long rk = ((w >> 32) + (w2 >> 32)) & 0xFFFFFFFFull;
+                __stcg(word + i, (rk << 32) | (w2 & 0xFFFFFFFFull));
+            }
+        }
+        __syncthreads();
+    }
+    for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x) rank[i] = (OutT)(__ldcg(word + i) >> 32);
+    if (threadIdx.x == 0) {
+        const unsigned long long w0 = __ldcg(word);
+        st->head_ok = ((uint32_t)w0 == tail) ? 1ull : 0ull;
+        st->head_sum = (w0 >> 32) + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ruling set: census (+ validation at level 0), scan, select
+
+template <class SuccT, bool kValidate>
+__global__ void __launch_bounds__(TILE_THREADS) k_rs_count(const SuccT* __restrict__ succ,
+                                                           uint32_t* __restrict__ tile_cnt, ListStatus* st,
+                                                           int level, uint32_t kbits, uint32_t salt, int census) {
+    const unsigned long long N = st->R[level];
+    const unsigned long long base = (unsigned long long)blockIdx.x * TILE;
+    if (base >= N) {
+        if (threadIdx.x == 0 && census) tile_cnt[blockIdx.x] = 0;
+        return;
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; ++j) {
+        const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+        if (i < N) {
+            if (kValidate) note_succ(st, i, as_index<SuccT>(succ[i]), N);
+            if (census) cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
+        }
+    }
+    if (census) {
+        typedef cub::BlockReduce<uint32_t, TILE_THREADS> BR;
+        __shared__ typename BR::TempStorage tmp;
+        const uint32_t tot = BR(tmp).Sum(cnt);
+        if (threadIdx.x == 0) tile_cnt[blockIdx.x] = tot;
+    }
+}
+
+// single CTA exclusive scan of the tile counts of `level`
+__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* tile_cnt, ListStatus* st, int level,
+                                                  unsigned long long cap) {
+    const unsigned long long N = st->R[level];
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
+    const unsigned long long per = (ntiles + 1023) / 1024;
+    const unsigned long long a = threadIdx.x * per;
+    const unsigned long long b = min(a + per, ntiles);
+    unsigned long long sum = 0;
+    for (unsigned long long t = a; t < b; ++t) sum += tile_cnt[t];
+    typedef cub::BlockScan<unsigned long long, 1024> BS;
+    __shared__ typename BS::TempStorage tmp;
+    unsigned long long off, total;
+    BS(tmp).ExclusiveSum(sum, off, total);
+    for (unsigned long long t = a; t < b; ++t) {
+        const uint32_t c = tile_cnt[t];
+        tile_cnt[t] = (uint32_t)off;
+        off += c;
+    }
+    if (threadIdx.x == 0) {
+        if (total > cap) {
+            st->overflow = 1;
+            total = cap;
+        }
+        st->R[level + 1] = total;
+    }
+}
+
+// install ruler ids in index order: spl[id] = node, word[node] = id << 32
+__global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __restrict__ tile_off,
+                                                            uint32_t* __restrict__ spl,
+                                                            unsigned long long* __restrict__ word,
+                                                            const ListStatus* st, int level, uint32_t kbits,
+                                                            uint32_t salt, unsigned long long cap) {
+    const unsigned long long N = st->R[level];
+    const unsigned long long base = (unsigned long long)blockIdx.x * TILE;
+    if (base >= N) return;
+    const unsigned long long i0 = base + (unsigned long long)threadIdx.x * TILE_ITEMS;
+    uint32_t flags = 0, cnt = 0;
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; ++j) {
+        const unsigned long long i = i0 + j;
+        if (i < N && is_ruler((uint32_t)i, kbits, salt)) {
+            flags |= 1u << j;
+            ++cnt;
+        }
+    }
+    typedef cub::BlockScan<uint32_t, TILE_THREADS> BS;
+    __shared__ typename BS::TempStorage tmp;
+    uint32_t pre;
+    BS(tmp).ExclusiveSum(cnt, pre);
+    unsigned long long id = (unsigned long long)tile_off[blockIdx.x] + pre;
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; ++j) {
+        if (flags & (1u << j)) {
+            if (id < cap) {
+                spl[id] = (uint32_t)(i0 + j);
+                word[i0 + j] = id << 32;
+            }
+            ++id;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// sublist walk (RS3 at level 0, weighted RS4 walk above)
+//
+// Lanes pull rulers from a global queue (warp-aggregated atomics), so a long
+// sublist never holds a whole warp's share of work hostage.
+
+template <class View>
+__global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned long long* __restrict__ word,
+                                                          const uint32_t* __restrict__ spl,
+                                                          uint2* __restrict__ up, ListStatus* st, int level,
+                                                          uint32_t kbits, uint32_t salt, uint32_t cap_hops) {
+    const unsigned long long N = st->R[level];
+    const unsigned long long R = st->R[level + 1];
+    unsigned long long* q = &st->qhead[level];
+    const uint32_t lane = lane_id();
+    uint32_t sid = NIL, cur = 0, pre = 0, hops = 0;
+    bool done = false;
+    for (;;) {
+        const bool need = !done && sid == NIL;
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if ((int)lane == leader) base = atomicAdd(q, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (need) {
+                const unsigned long long s = base + __popc(m & ((1u << lane) - 1u));
+                if (s < R) {
+                    sid = (uint32_t)s;
+                    cur = spl[s];
+                    pre = 0;
+                    hops = 0;
+                } else {
+                    done = true;
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        if (done) continue;
+        word[cur] = ((unsigned long long)sid << 32) | pre;
+        unsigned long long nx;
+        uint32_t w;
+        src.load(cur, nx, w);
+        pre += w;
+        ++hops;
+        if (nx == cur) {  // the tail: end of the whole list
+            up[sid] = make_uint2(sid, pre);
+            sid = NIL;
+        } else if (nx >= N) {  // out-of-range successor (invalid input)
+            st->bad = 1;
+            up[sid] = make_uint2(sid, pre);
+            sid = NIL;
+        } else if (is_ruler((uint32_t)nx, kbits, salt)) {
+            up[sid] = make_uint2((uint32_t)(word[nx] >> 32), pre);
+            sid = NIL;
+        } else if (hops >= cap_hops) {
+            st->overflow = 1;
+            up[sid] = make_uint2(sid, pre);
+            sid = NIL;
+        } else {
+            cur = (uint32_t)nx;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// top level: one CTA of weighted pointer jumping (RS4 single block,
+// listrank.py:333-342) producing inclusive suffix sums IS[i].
+
+template <class View>
+__global__ void __launch_bounds__(1024) k_rs_final(View src, uint2* A, uint2* B, uint32_t* __restrict__ IS,
+                                                   ListStatus* st, int level) {
+    const uint32_t R = (uint32_t)st->R[level];
+    for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) {
+        unsigned long long nx;
+        uint32_t w;
+        src.load(i, nx, w);
+        uint32_t nxt = NIL;
+        if (nx >= R) {
+            st->bad = 1;
+        } else if (nx != i) {
+            nxt = (uint32_t)nx;
+        }
+        A[i] = make_uint2(w, nxt);
+    }
+    __syncthreads();
+    int maxr = 2;
+    for (uint32_t r = R; r > 1; r = (r + 1) >> 1) ++maxr;
+    uint2* cur = A;
+    uint2* nxt = B;
+    for (int r = 0; r < maxr; ++r) {
+        int active = 0;
+        for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) {
+            uint2 a = __ldcg(cur + i);
+            if (a.y != NIL) {
+                const uint2 b = __ldcg(cur + a.y);
+                a.x += b.x;
+                a.y = b.y;
+                active |= (b.y != NIL);
+            }
+            __stcg(nxt + i, a);
+        }
+        active = __syncthreads_or(active);
+        uint2* t = cur;
+        cur = nxt;
+        nxt = t;
+        if (!active) break;
+    }
+    for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) IS[i] = __ldcg(cur + i).x;
+    if (threadIdx.x == 0 && R > 0) {
+        const uint2 h = __ldcg(cur);
+        st->head_sum = h.x;
+        st->head_ok = (h.y == NIL) ? 1ull : 0ull;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// expand (RS5 at level 0, listrank.py:360-382)
+
+__global__ void __launch_bounds__(256) k_rs_expand_k(const unsigned long long* __restrict__ word,
+                                                     const uint32_t* __restrict__ IS_up, uint32_t* __restrict__ IS,
+                                                     const ListStatus* st, int level) {
+    const unsigned long long N = st->R[level];
+    const unsigned long long Rup = st->R[level + 1];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+        const unsigned long long w = word[i];
+        const unsigned long long o = w >> 32;
+        IS[i] = o < Rup ? __ldg(IS_up + o) - (uint32_t)w : 0u;
+    }
+}
+
+template <class OutT>
+__global__ void __launch_bounds__(256) k_rs_expand0(const unsigned long long* __restrict__ word,
+                                                    const uint32_t* __restrict__ IS1, OutT* __restrict__ rank,
+                                                    unsigned long long n, const ListStatus* st) {
+    if (st->overflow) return;  // host re-ranks with Wyllie; keep succ intact if aliased
+    const unsigned long long R1 = st->R[1];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long npair = n >> 1;
+    const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(word);
+    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < npair; k += stride) {
+        const ulonglong2 w = __ldcs(w2 + k);
+        const unsigned long long o0 = w.x >> 32, o1 = w.y >> 32;
+        const uint32_t r0 = o0 < R1 ? __ldg(IS1 + o0) - (uint32_t)w.x - 1u : 0u;
+        const uint32_t r1 = o1 < R1 ? __ldg(IS1 + o1) - (uint32_t)w.y - 1u : 0u;
+        rank[2 * k] = (OutT)r0;
+        rank[2 * k + 1] = (OutT)r1;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long w = word[n - 1];
+        const unsigned long long o = w >> 32;
+        rank[n - 1] = (OutT)(o < R1 ? IS1[o] - (uint32_t)w - 1u : 0u);
+    }
+}
+
+template <class OutT>
+__global__ void k_rs_expand_direct(const uint32_t* __restrict__ IS0, OutT* __restrict__ rank, unsigned long long n,
+                                   const ListStatus* st) {
+    if (st->overflow) return;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        rank[i] = (OutT)(IS0[i] - 1u);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct RsPlan {
+    int levels = 0;                              // walked levels (final level = levels)
+    uint32_t walk_cap = WALK_CAP_HOPS;
+    uint32_t kbits[SG_MAX_LEVELS] = {};
+    uint32_t salt[SG_MAX_LEVELS] = {};
+    unsigned long long cap[SG_MAX_LEVELS + 1] = {};  // node capacity per level
+};
+
+static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t hi) {
+    const char* s = getenv(name);
+    if (!s || !*s) return dflt;
+    long v = strtol(s, nullptr, 10);
+    if (v < (long)lo) v = lo;
+    if (v > (long)hi) v = hi;
+    return (uint32_t)v;
+}
+
+static uint32_t mix32(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return (uint32_t)x;
+}
+
+static RsPlan plan_rs(uint64_t n, uint64_t seed) {
+    RsPlan p;
+    const uint32_t kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);
+    const uint32_t kb1 = env_u32("SG_RS_KBITS", 5, 1, 16);
+    const uint32_t fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
+    p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
+    p.cap[0] = n;
+    unsigned long long N = n;
+    while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
+        const uint32_t kb = p.levels == 0 ? kb0 : kb1;
+        const unsigned long long exp = (N >> kb) + 1;
+        unsigned long long cap = exp + exp / 4 + 4096;
+        if (cap > N) cap = N;
+        p.kbits[p.levels] = kb;
+        p.salt[p.levels] = mix32(seed * 0x9E3779B97F4A7C15ull + (uint64_t)p.levels + 1);
+        ++p.levels;
+        p.cap[p.levels] = cap;
+        N = exp;
+    }
+    return p;
+}
+
+struct RsBufs {
+    ListStatus* st = nullptr;
+    unsigned long long* word0 = nullptr;
+    uint32_t* tiles = nullptr;
+    uint32_t* spl[SG_MAX_LEVELS] = {};
+    uint2* lvl[SG_MAX_LEVELS + 1] = {};
+    unsigned long long* word[SG_MAX_LEVELS + 1] = {};
+    uint32_t* IS[SG_MAX_LEVELS + 1] = {};
+    uint2* fa = nullptr;
+    uint2* fb = nullptr;
+};
+
+static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
+    b.st = c.take<ListStatus>(1);
+    b.word0 = c.take<unsigned long long>(n);
+    const uint64_t ntiles = (n + TILE - 1) / TILE;
+    b.tiles = c.take<uint32_t>(ntiles + 1);
+    for (int k = 0; k < p.levels; ++k) {
+        const unsigned long long cap = p.cap[k + 1];
+        b.spl[k] = c.take<uint32_t>(cap);
+        b.lvl[k + 1] = c.take<uint2>(cap);
+        b.word[k + 1] = c.take<unsigned long long>(cap);
+        b.IS[k + 1] = c.take<uint32_t>(cap);
+    }
+    const unsigned long long fcap = p.levels == 0 ? n : p.cap[p.levels];
+    b.fa = c.take<uint2>(fcap);
+    b.fb = c.take<uint2>(fcap);
+    if (p.levels == 0) b.IS[0] = c.take<uint32_t>(n);
+    return c.ok;
+}
+
+// ---- Wyllie host driver --------------------------------------------------------
+
+static int jump_rounds(uint64_t n) {
+    int r = 0;
+    if (n > 1) {
+        uint64_t m = n - 1;
+        while (m) {
+            ++r;
+            m >>= 1;
+        }
+    }
+    return r;
+}
+
+template <class SuccT, class OutT>
+static int wyllie_run(const SuccT* succ, OutT* rank, uint64_t n, int variant, ListStatus* st,
+                      unsigned long long* word, cudaStream_t s, Recorder& rec, sg_stats* stats) {
+    const int rounds = jump_rounds(n);
+    if (stats) stats->rounds = (uint32_t)rounds;
+    rec.begin(K_STATUS_INIT, 0, 1, 32, 0);
+    k_status_init<<<1, 32, 0, s>>>(st, n);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    if (variant == SG_WY_SINGLE_BLOCK) {
+        rec.begin(K_WY_SINGLE, 0, 1, 1024, n * (uint64_t)(rounds + 2));
+        k_wy_single<SuccT, OutT><<<1, 1024, 0, s>>>(succ, word, n, st, rank, rounds);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        return SG_OK;
+    }
+    const uint32_t grid = grid_for(n, JUMP_THREADS, 1, kSMs * 8);
+    rec.begin(K_WY_INIT, 0, grid, JUMP_THREADS, n);
+    k_wy_init<SuccT><<<grid, JUMP_THREADS, 0, s>>>(succ, word, n, st);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    const int launches = rounds > 0 ? rounds : 1;  // n == 1: one extraction pass
+    for (int r = 1; r <= launches; ++r) {
+        rec.begin(K_WY_JUMP, r, grid, JUMP_THREADS, n);
+        k_wy_jump<OutT><<<grid, JUMP_THREADS, 0, s>>>(word, n, st, r == launches ? rank : (OutT*)nullptr);
+        rec.end();
+        SG_LAUNCH_CHECK();
+    }
+    rec.begin(K_WY_CHECK, 0, 1, 32, 1);
+    k_wy_check<<<1, 32, 0, s>>>(word, n, st);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+// ---- ruling-set host driver ----------------------------------------------------
+
+template <class SuccT, class OutT>
+static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, RsBufs& b, cudaStream_t s,
+                  Recorder& rec, sg_stats* stats) {
+    rec.begin(K_STATUS_INIT, 0, 1, 32, 0);
+    k_status_init<<<1, 32, 0, s>>>(b.st, n);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    const uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
+    if (p.levels == 0) {
+        const uint32_t nt = (uint32_t)((n + TILE - 1) / TILE);
+        rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, n);
+        k_rs_count<SuccT, true><<<nt, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, 0, 1, 0, 0);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        rec.begin(K_RS4_RANK, 0, 1, 1024, n);
+        k_rs_final<Level0<SuccT>><<<1, 1024, 0, s>>>(Level0<SuccT>{succ}, b.fa, b.fb, b.IS[0], b.st, 0);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        const uint32_t g = grid_for(n, 256, 1, kSMs * 8);
+        rec.begin(K_RS5_EXPAND, 0, g, 256, n);
+        k_rs_expand_direct<OutT><<<g, 256, 0, s>>>(b.IS[0], rank, n, b.st);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        return SG_OK;
+    }
+    // downward: census, select, walk per level
+    for (int k = 0; k < p.levels; ++k) {
+        const unsigned long long capN = p.cap[k];
+        const uint32_t nt = (uint32_t)((capN + TILE - 1) / TILE);
+        const unsigned long long capR = p.cap[k + 1];
+        unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
+        if (k == 0) {
+            rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, capN);
+            k_rs_count<SuccT, true><<<nt, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, 0, p.kbits[0], p.salt[0], 1);
+        } else {
+            rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
+            k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, b.tiles, b.st, k, p.kbits[k], p.salt[k], 1);
+        }
+        rec.end();
+        SG_LAUNCH_CHECK();
+        rec.begin(k == 0 ? K_RS_SCAN : K_RS4_SCAN, k, 1, 1024, nt);
+        k_rs_scan<<<1, 1024, 0, s>>>(b.tiles, b.st, k, capR);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
+        k_rs_select<<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        if (k == 0) {
+            rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
+            k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ}, wk, b.spl[0], b.lvl[1],
+                                                                        b.st, 0, p.kbits[0], p.salt[0], p.walk_cap);
+        } else {
+            rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
+            k_rs_walk<LevelK><<<walk_grid, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
+                                                                 k, p.kbits[k], p.salt[k], p.walk_cap);
+        }
+        rec.end();
+        SG_LAUNCH_CHECK();
+    }
+    // top: single CTA on the last ruler list
+    const int L = p.levels;
+    rec.begin(K_RS4_RANK, L, 1, 1024, p.cap[L]);
+    k_rs_final<LevelK><<<1, 1024, 0, s>>>(LevelK{b.lvl[L]}, b.fa, b.fb, b.IS[L], b.st, L);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    // upward: expand
+    for (int k = L - 1; k >= 1; --k) {
+        const uint32_t g = grid_for(p.cap[k], 256, 1, kSMs * 8);
+        rec.begin(K_RS4_EXPAND, k, g, 256, p.cap[k]);
+        k_rs_expand_k<<<g, 256, 0, s>>>(b.word[k], b.IS[k + 1], b.IS[k], b.st, k);
+        rec.end();
+        SG_LAUNCH_CHECK();
+    }
+    const uint32_t g = grid_for(n / 2 + 1, 256, 1, kSMs * 8);
+    rec.begin(K_RS5_EXPAND, 0, g, 256, n);
+    k_rs_expand0<OutT><<<g, 256, 0, s>>>(b.word0, b.IS[1], rank, n, b.st);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    if (stats) {
+        stats->levels = (uint32_t)L;
+    }
+    return SG_OK;
+}
+
+static int read_status(const ListStatus* st_dev, ListStatus& h, cudaStream_t s) {
+    SG_CUDA(cudaMemcpyAsync(&h, st_dev, sizeof(ListStatus), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    return SG_OK;
+}
+
+// classify a finished pipeline: SG_OK, SG_ERR_INVALID_LIST (viol filled)
+static int classify(const ListStatus& h, uint64_t n, sg_violation* v) {
+    sg_violation tmp;
+    if (!v) v = &tmp;
+    v->kind = SG_LIST_OK;
+    v->index = -1;
+    v->pad = 0;
+    if (h.oor_first != NONE64) {
+        v->kind = SG_LIST_OUT_OF_RANGE;
+        v->index = (int64_t)h.oor_first;
+        return SG_ERR_INVALID_LIST;
+    }
+    if (h.loop_count == 0) {
+        v->kind = SG_LIST_NO_TAIL;
+        return SG_ERR_INVALID_LIST;
+    }
+    if (h.loop_count > 1) {
+        v->kind = SG_LIST_MULTIPLE_SELF_LOOPS;  // index: host recomputes loops[1]
+        return SG_ERR_INVALID_LIST;
+    }
+    if (h.bad || !h.head_ok || h.head_sum != n) {
+        v->kind = SG_LIST_UNREACHABLE;  // index: host recomputes the first unreached node
+        return SG_ERR_INVALID_LIST;
+    }
+    return SG_OK;
+}
+
+template <class SuccT, class OutT>
+static int wyllie_entry(const void* succ_v, void* rank_v, uint64_t n, int variant, void* ws, size_t ws_bytes,
+                        cudaStream_t s, sg_stats* stats, sg_violation* viol) {
+    Carver c(ws, ws_bytes);
+    ListStatus* st = c.take<ListStatus>(1);
+    unsigned long long* word = c.take<unsigned long long>(n);
+    if (!c.ok) return SG_ERR_WORKSPACE;
+    Recorder rec(stats, s);
+    int rc = wyllie_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, variant, st, word, s, rec, stats);
+    if (rc != SG_OK) return rc;
+    SG_CUDA(rec.finish());
+    ListStatus h;
+    rc = read_status(st, h, s);
+    if (rc != SG_OK) return rc;
+    return classify(h, n, viol);
+}
+
+template <class SuccT, class OutT>
+static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
+                    cudaStream_t s, sg_stats* stats, sg_violation* viol) {
+    const RsPlan p = plan_rs(n, seed);
+    Carver c(ws, ws_bytes);
+    RsBufs b;
+    if (!carve_rs(c, n, p, b)) return SG_ERR_WORKSPACE;
+    if (stats) {
+        stats->levels = (uint32_t)p.levels;
+        stats->fallback = 0;
+        for (int k = 0; k < SG_MAX_LEVELS; ++k) stats->level_size[k] = 0;
+    }
+    Recorder rec(stats, s);
+    int rc = rs_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, p, b, s, rec, stats);
+    if (rc != SG_OK) return rc;
+    SG_CUDA(rec.finish());
+    ListStatus h;
+    rc = read_status(b.st, h, s);
+    if (rc != SG_OK) return rc;
+    if (stats)
+        for (int k = 0; k <= p.levels && k < SG_MAX_LEVELS; ++k) stats->level_size[k] = h.R[k];
+    if (h.oor_first == NONE64 && h.loop_count == 1 && h.overflow) {
+        // a walk hit the hop cap or a level overflowed its capacity: rank the
+        // list by pointer jumping instead (terminates on every input)
+        if (stats) stats->fallback = 1;
+        Recorder rec2(nullptr, s);
+        rc = wyllie_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, SG_WY_MULTI_KERNEL, b.st, b.word0, s,
+                                     rec2, nullptr);
+        if (rc != SG_OK) return rc;
+        SG_CUDA(rec2.finish());
+        rc = read_status(b.st, h, s);
+        if (rc != SG_OK) return rc;
+    }
+    return classify(h, n, viol);
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+#define SG_DISPATCH_LIST(FN, SDT, ODT, ...)                                                   \
+    do {                                                                                      \
+        if ((SDT) == SG_U32 && (ODT) == SG_U32) return FN<uint32_t, uint32_t>(__VA_ARGS__);  \
+        if ((SDT) == SG_U32 && (ODT) == SG_I32) return FN<uint32_t, int32_t>(__VA_ARGS__);   \
+        if ((SDT) == SG_U32 && (ODT) == SG_I64) return FN<uint32_t, int64_t>(__VA_ARGS__);   \
+        if ((SDT) == SG_I32 && (ODT) == SG_U32) return FN<int32_t, uint32_t>(__VA_ARGS__);   \
+        if ((SDT) == SG_I32 && (ODT) == SG_I32) return FN<int32_t, int32_t>(__VA_ARGS__);    \
+        if ((SDT) == SG_I32 && (ODT) == SG_I64) return FN<int32_t, int64_t>(__VA_ARGS__);    \
+        if ((SDT) == SG_I64 && (ODT) == SG_U32) return FN<int64_t, uint32_t>(__VA_ARGS__);   \
+        if ((SDT) == SG_I64 && (ODT) == SG_I32) return FN<int64_t, int32_t>(__VA_ARGS__);    \
+        if ((SDT) == SG_I64 && (ODT) == SG_I64) return FN<int64_t, int64_t>(__VA_ARGS__);    \
+        return SG_ERR_VALUE;                                                                  \
+    } while (0)
+
+extern "C" {
+
+size_t sg_wyllie_workspace_bytes(uint64_t n) {
+    Carver c(nullptr, 0);
+    c.take<ListStatus>(1);
+    c.take<unsigned long long>(n);
+    return c.off + 256;
+}
+
+size_t sg_rs_workspace_bytes(uint64_t n) {
+    const RsPlan p = plan_rs(n, 0);
+    Carver c(nullptr, 0);
+    RsBufs b;
+    carve_rs(c, n, p, b);
+    return c.off + 256;
+}
+
+int sg_wyllie_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype, uint64_t n, int variant, void* ws,
+                   size_t ws_bytes, void* stream, sg_stats* st, sg_violation* viol) {
+    if (n == 0 || n >= 0xFFFFFFFFull) return SG_ERR_CAPABILITY;
+    if (variant != SG_WY_MULTI_KERNEL && variant != SG_WY_SINGLE_BLOCK) return SG_ERR_VALUE;
+    if (st) memset(st, 0, sizeof(sg_stats));
+    SG_DISPATCH_LIST(wyllie_entry, succ_dtype, rank_dtype, succ, rank, n, variant, ws, ws_bytes, (cudaStream_t)stream,
+                     st, viol);
+}
+
+int sg_rs_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype, uint64_t n, uint64_t seed, void* ws,
+               size_t ws_bytes, void* stream, sg_stats* st, sg_violation* viol) {
+    if (n == 0 || n >= 0xFFFFFFFFull) return SG_ERR_CAPABILITY;
+    if (st) memset(st, 0, sizeof(sg_stats));
+    SG_DISPATCH_LIST(rs_entry, succ_dtype, rank_dtype, succ, rank, n, seed, ws, ws_bytes, (cudaStream_t)stream, st,
+                     viol);
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// sg_runtime.cu -- library plumbing: status strings, kernel names, the
+// per-call launch recorder (CUDA events on the launching stream).
+#include <string.h>
+
+#include <string>
+
+#include "sg_internal.cuh"
+
+namespace sg {
+
+static thread_local std::string g_last_cuda_error;
+
+void set_cuda_error(cudaError_t e) {
+    g_last_cuda_error = std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e);
+}
+
+// Events are reused across calls (one pool per device per host thread):
+// creating two events per launch would cost more than the short launches.
+static thread_local std::vector<cudaEvent_t> g_pool[64];
+
+static cudaEvent_t pool_event(size_t i) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::vector<cudaEvent_t>& pool = g_pool[dev & 63];
+    while (pool.size() <= i) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        pool.push_back(e);
+    }
+    return pool[i];
+}
+
+Recorder::Recorder(sg_stats* st, cudaStream_t s) : st_(st), s_(s) {
+    if (st_) {
+        st_->n_launches = 0;
+        t0_ = pool_event(0);
+        if (t0_) cudaEventRecord(t0_, s_);
+        ev_.push_back(t0_);
+    }
+}
+
+Recorder::~Recorder() {}
+
+void Recorder::begin(int kernel, int round, uint32_t blocks, uint32_t threads, uint64_t items) {
+    if (!st_ || st_->n_launches >= SG_MAX_LAUNCHES) {
+        open_ = -1;
+        return;
+    }
+    uint32_t k = st_->n_launches;
+    sg_launch& L = st_->launch[k];
+    L.kernel = kernel;
+    L.round = round;
+    L.blocks = blocks;
+    L.threads = threads;
+    L.items = items;
+    L.ms = 0.f;
+    L.pad = 0;
+    cudaEvent_t a = pool_event(ev_.size());
+    if (a) cudaEventRecord(a, s_);
+    ev_.push_back(a);
+    open_ = int(k);
+}
+
+void Recorder::end() {
+    if (open_ < 0) return;
+    cudaEvent_t b = pool_event(ev_.size());
+    if (b) cudaEventRecord(b, s_);
+    ev_.push_back(b);
+    st_->n_launches = uint32_t(open_) + 1;
+    open_ = -1;
+}
+
+cudaError_t Recorder::finish() {
+    cudaError_t e = cudaStreamSynchronize(s_);
+    if (e != cudaSuccess || !st_) return e;
+    // ev_[0] = t0, then (begin, end) pairs in launch order
+    for (uint32_t k = 0; k < st_->n_launches; ++k) {
+        size_t ia = 1 + 2 * size_t(k), ib = ia + 1;
+        if (ib < ev_.size() && ev_[ia] && ev_[ib]) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ev_[ia], ev_[ib]) == cudaSuccess) st_->launch[k].ms = ms;
+        }
+    }
+    if (ev_.size() > 1 && ev_[0] && ev_.back()) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev_[0], ev_.back()) == cudaSuccess) st_->total_ms = ms;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace sg
+
+extern "C" {
+
+const char* sg_strerror(int status) {
+    switch (status) {
+        case SG_OK: return "ok";
+        case SG_ERR_INVALID_LIST: return "invalid successor list";
+        case SG_ERR_INVALID_GRAPH: return "invalid edge graph";
+        case SG_ERR_CAPABILITY: return "capability limit exceeded";
+        case SG_ERR_VALUE: return "invalid argument";
+        case SG_ERR_RUNTIME: return "algorithm did not converge";
+        case SG_ERR_CUDA: return "CUDA error";
+        case SG_ERR_WORKSPACE: return "workspace too small";
+        default: return "unknown status";
+    }
+}
+
+const char* sg_kernel_name(int id) {
+    static const char* names[sg::K_COUNT_] = {
+        "status_init", "wy_init",     "wy_jump",     "wy_single",   "wy_check",
+        "rs1_validate", "rs2_scan",   "rs2_select",  "rs3_walk",    "rs4_count",
+        "rs4_scan",    "rs4_select",  "rs4_walk",    "rs4_rank",    "rs4_expand",
+        "rs5_expand",  "sv0",         "cc_hook_uf",  "cc_hook_sv",  "cc_shortcut",
+        "cc_labels",   "gather",      "kiss",        "list_from_order", "edge_keys",
+        "edges_from_keys",
+    };
+    if (id < 0 || id >= sg::K_COUNT_) return "unknown";
+    return names[id];
+}
+
+int sg_version(void) { return 1; }
+
+const char* sg_last_cuda_error(void) { return sg::g_last_cuda_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+"""Edge-sharded connected components over several GPUs (one process per GPU,
+``torch.distributed`` over NCCL / NVLink).
+
+SURVEY §8e: the stored edge list is cut into G contiguous row blocks; each
+rank keeps a full replica of the parent array D (u32, D[i] <= i).  A round is
+
+1. local hook over the rank's edge block (``sg_cc_hook``; UF: CAS root
+   hooking on the current forest, SV: conditional min-hook on stars);
+2. ``all_reduce(MIN)`` of D -- hooks only ever lower parents, so the
+   element-wise minimum of the G proposals is itself a valid forest with
+   D[i] <= i; word n carries 1 - changed, so convergence rides the same
+   collective;
+3. (SV, and the final round) a sharded shortcut: rank g chases roots for its
+   n/G slice of the merged D (static during the chase), then
+   ``all_gather_into_tensor`` restores the replica.
+
+The loop ends after a round in which no rank hooked anything; then every
+edge joins vertices of one tree, so the roots are the component minima.
+Round 1 also validates the edge blocks (first bad row reduced with MAX of
+~row, as in the single-GPU kernel).
+
+The collective and the kernels are injected (``comm``, ``ops``) so the
+orchestration is tested with the gloo backend on CPU (tests/test_dist.py);
+the product path uses ``CudaOps`` + NCCL.
+"""
+
+import ctypes
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device, _native
+from .concomp import _graph_error_message, sv_round_bound
+from .core import EdgeGraph, ExecStats, InvalidGraphError
+
+_NO_ROW = 1 << 62
+
+
+class TorchDistComm:
+    """Collectives over a torch.distributed process group."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce_min_(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+
+    def allreduce_max_(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+
+    def allreduce_sum_(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def allgather_(self, full, chunk):
+        dist.all_gather_into_tensor(full, chunk, group=self.group)
+
+
+class CudaOps:
+    """Device kernels of one rank (libsg C ABI on the current CUDA stream)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.lib = _native.lib()
+
+    def stream(self):
+        return _device.stream_ptr(self.device)
+
+    def parents(self, size):
+        return torch.empty(size, dtype=torch.int32, device=self.device)
+
+    def init(self, D, n):
+        _native.check(self.lib.sg_cc_init(_device.ptr(D), n, self.stream()), "sg_cc_init")
+
+    def hook(self, edges, row0, n, D, variant, validate, flags):
+        code = _native.SG_CC_UF if variant == "uf" else _native.SG_CC_SV
+        m = edges.shape[0]
+        rc = self.lib.sg_cc_hook(_device.ptr(edges), _device.dtype_code(edges), m, row0, n, _device.ptr(D), code,
+                                 int(validate), _device.ptr(flags), self.stream())
+        _native.check(rc, "sg_cc_hook")
+
+    def compress(self, D, lo, hi, roots):
+        _native.check(self.lib.sg_cc_compress(_device.ptr(D), lo, hi, _device.ptr(roots), self.stream()),
+                      "sg_cc_compress")
+
+    def synchronize(self):
+        torch.cuda.synchronize(self.device)
+
+
+def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None):
+    """Run the sharded rounds.  `edges` is this rank's (m_g, 2) block whose
+    first row is global row `row0`.  Returns (D replica as int32 tensor of
+    size >= n, info dict)."""
+    if variant not in ("uf", "sv"):
+        raise ValueError(f"unknown variant {variant!r}")
+    G = comm.world
+    bound = sv_round_bound(n) if round_bound is None else round_bound
+    S = -(-(n + 1) // G)              # slice length; padded replica holds the flag word at index n
+    npad = S * G
+    D = ops.parents(npad)
+    ops.init(D, npad)
+    lo = comm.rank * S
+    hi = min(lo + S, n)
+    flags = torch.zeros(4, dtype=torch.int64, device=D.device)
+    roots = torch.zeros(1, dtype=torch.int64, device=D.device)
+    info = {"rounds": 0, "roots_per_round": [n], "edge_sweeps": 0, "vertex_sweeps": 0,
+            "allreduce_bytes": 0, "allgather_bytes": 0, "comm_s": 0.0}
+    r = 0
+    while True:
+        r += 1
+        if r > bound:
+            raise RuntimeError(f"no convergence after {r - 1} rounds (bound {bound})")
+        flags.zero_()
+        ops.hook(edges, row0, n, D, variant, r == 1, flags)
+        info["edge_sweeps"] += 1
+        if r == 1:
+            # kernel flags hold ~row (0 = none); reduce the first bad global row
+            f = flags[1:3]
+            bad = torch.where(f != 0, torch.bitwise_not(f), torch.full_like(f, _NO_ROW))
+            comm.allreduce_min_(bad)
+            b = bad.cpu().tolist()
+            if b[0] != _NO_ROW or b[1] != _NO_ROW:
+                kind, row = (1, b[0]) if b[0] != _NO_ROW else (2, b[1])
+                raise InvalidGraphError(_graph_error_message(kind, row))
+        changed = int(flags[0].item())
+        D[n] = 0 if changed else 1
+        t0 = time.perf_counter()
+        comm.allreduce_min_(D)
+        info["comm_s"] += time.perf_counter() - t0
+        info["allreduce_bytes"] += D.numel() * D.element_size()
+        converged = int(D[n].item()) == 1
+        if variant == "sv" or converged:
+            roots.zero_()
+            ops.compress(D, lo, hi, roots)
+            info["vertex_sweeps"] += 1
+            t0 = time.perf_counter()
+            comm.allgather_(D, D[comm.rank * S:(comm.rank + 1) * S].clone())
+            comm.allreduce_sum_(roots)
+            info["comm_s"] += time.perf_counter() - t0
+            info["allgather_bytes"] += D.numel() * D.element_size()
+            if variant == "sv" or converged:
+                info["roots_per_round"].append(int(roots.item()))
+        info["rounds"] = r
+        if converged:
+            break
+    return D, info
+
+
+def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", accounting="full",
+                       block_size=256, seed=0, workers=None, shard=None):
+    """Edge-sharded ``sv_components`` across the ranks of `group`.
+
+    Every rank calls it with the same graph (host or its own device copy) --
+    or with its own block of rows via ``shard=(row0, edges_block)`` -- and
+    gets the full int64 label array (replicated) plus ExecStats.
+    """
+    if graph is not None and graph.n <= 0:
+        raise InvalidGraphError("graph needs at least one vertex")
+    comm = TorchDistComm(group)
+    dev = _device.require_cuda()
+    n = graph.n
+    if shard is None:
+        m = graph.m
+        per = -(-m // comm.world)
+        row0 = min(comm.rank * per, m)
+        row1 = min(row0 + per, m)
+        edges = graph.edges[row0:row1]
+    else:
+        row0, edges = shard
+    edges, _ = _device.to_device(edges if edges.shape[0] else np.empty((0, 2), np.int64), dev)
+    if int(p) > n:
+        raise ValueError(f"more threads ({p}) than vertices ({n})")
+    ops = CudaOps(dev)
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    start.record()
+    D, info = sharded_components(n, edges, int(row0), comm, ops, variant=variant)
+    stop.record()
+    stop.synchronize()
+    labels = D[:n].to(torch.int64)
+    stats = ExecStats(backend="sm_100a")
+    stats.rounds = info["rounds"]
+    stats.wall_time = start.elapsed_time(stop) / 1e3
+    stats.meta.update(n=n, p=int(p), m_stored=graph.m, oriented_m=2 * graph.m, rounds=info["rounds"],
+                      round_bound=sv_round_bound(n), roots_per_round=info["roots_per_round"], variant=variant,
+                      edge_sweeps=info["edge_sweeps"], vertex_sweeps=info["vertex_sweeps"], world=comm.world,
+                      allreduce_bytes=info["allreduce_bytes"], allgather_bytes=info["allgather_bytes"])
+    if isinstance(graph.edges, torch.Tensor) and graph.edges.is_cuda:
+        return labels, stats
+    return labels.cpu().numpy(), stats

@@ -1,0 +1,295 @@
+"""List ranking on the B200: drop-in for ``simtgraph.listrank``
+(``/root/reference/pkg/src/simtgraph/listrank.py``).
+
+Same entry points, signatures, return values ``(rank int64[n], ExecStats)``,
+``meta`` keys and error conventions; the work runs in libsg's sm_100a
+kernels (``csrc/sg_list.cu``):
+
+* ``wyllie_rank``  -- pointer jumping over packed {rank, succ} words
+  (``variant="multi_kernel"``: ceil(log2 n) launches; ``"single_block"``:
+  one CTA with block barriers).
+* ``rs_rank`` / ``rs_rank_even`` -- sparse ruling set, recursive.  The
+  reference's ``p`` is its splitter/thread count on a simulated 2009 GPU; it
+  is kept as the splitter set reported in ``meta["splitter_set"]``
+  (identical to the reference: same KISS draw, sublist lengths, reduced
+  successors, splitter ranks), derived from the device ranks.  The device
+  walks its own hashed ruling set, sized for 148 SMs, so performance does
+  not hinge on ``p``.
+
+Backend / accounting / workers select the reference's simulator; they are
+validated exactly like ``vkm.Machine`` (vkm.py:434-454) and recorded in
+``meta``, but execution is always the CUDA path (no CPU fallback).
+"""
+
+import ctypes
+import math
+from collections import namedtuple
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .core import (
+    P48_MAX_THREADS,
+    CapabilityError,
+    InvalidListError,
+    ListViolation,
+    Packing,
+    SuccessorList,
+    VIOLATION_KINDS,
+)
+from .gen import kiss_batch, kiss_seed
+
+MAX_BLOCK_SIZE = 768            # vkm.py:41
+SM_COUNT = 27                   # the reference's simulated device (core.py:313-314)
+CORES_PER_SM = 8
+DEFAULT_P = 4 * SM_COUNT * CORES_PER_SM   # vkm.py:46
+
+
+def _jump_rounds(n):
+    """ceil(log2 n), 0 for n <= 1 (listrank.py:38-40)."""
+    return max(0, int(n - 1).bit_length()) if n > 1 else 0
+
+
+@dataclass
+class SplitterSet:
+    """Everything known about the r splitters (listrank.py:43-50)."""
+    r: int
+    splitter_node: np.ndarray
+    sublist_len: np.ndarray = None
+    splitter_succ: np.ndarray = None
+    splitter_rank: np.ndarray = None
+
+
+SublistStats = namedtuple("SublistStats", ["max_len", "mean_len", "histogram"])
+
+
+def sublist_stats(splitters):
+    """Max/mean/histogram of sub-list lengths (listrank.py:64-69)."""
+    lens = np.asarray(splitters.sublist_len, dtype=np.int64)
+    hist = np.bincount(lens)
+    return SublistStats(int(lens.max()), lens.sum() / lens.size, hist)
+
+
+# ---------------------------------------------------------------------------
+# argument checks, in the reference's order
+
+def _machine_error(p, block_size, backend, accounting):
+    """The ValueErrors vkm.Machine / GridConfig raise (vkm.py:58-62, 436-439)."""
+    if backend not in ("simulated", "threaded"):
+        return ValueError(f"unknown backend {backend!r}")
+    if accounting not in ("full", "counts"):
+        return ValueError(f"unknown accounting mode {accounting!r}")
+    if p < 1:
+        return ValueError("need at least one thread")
+    if not 1 <= block_size <= MAX_BLOCK_SIZE:
+        return ValueError(f"block size must be in [1, {MAX_BLOCK_SIZE}]")
+    return None
+
+
+def _as_packing(packing):
+    if isinstance(packing, Packing):
+        return packing
+    return Packing(str(packing).lower())
+
+
+def _rs_param_error(n, p, packing, block_size, backend, accounting):
+    """_rs_pipeline checks (listrank.py:388-393), then Machine's."""
+    if packing is Packing.P48 and p > P48_MAX_THREADS:
+        return CapabilityError(f"48-bit packing cannot be invoked with more than {P48_MAX_THREADS} threads (got {p})")
+    if p > n:
+        return ValueError(f"more threads ({p}) than nodes ({n})")
+    return _machine_error(p, block_size, backend, accounting)
+
+
+# ---------------------------------------------------------------------------
+# device calls
+
+def _raise_invalid(sl, code, viol):
+    """Turn a device-reported invalid list into the reference's exact
+    InvalidListError message (the index comes from the host validator)."""
+    kind, index = _native.list_violation_host(sl.host_succ())
+    if kind == 0:  # device and host disagree -- should not happen
+        kind, index = viol.kind, viol.index
+    raise InvalidListError(str(ListViolation(VIOLATION_KINDS.get(kind, "unreachable"), int(index))))
+
+
+def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False):
+    """Rank `sl` on the GPU.  Returns (rank tensor, native stats, status,
+    violation, host_input)."""
+    n = sl.n
+    if n >= 0xFFFFFFFF:
+        raise CapabilityError(f"device node ids are 32-bit: n={n} is too large")
+    dev = _device.require_cuda(sl.succ.device if isinstance(sl.succ, torch.Tensor) and sl.succ.is_cuda else None)
+    with torch.cuda.device(dev):
+        succ, host_input = _device.to_device(sl.succ, dev)
+        if reuse_succ and not scratch_out:
+            rank = succ  # ranks overwrite the (device copy of the) successors, listrank.py:186-187
+        else:
+            rank = torch.empty(n, dtype=torch.int64 if succ.dtype == torch.int64 or host_input else succ.dtype,
+                               device=dev)
+        st = _native.Stats()
+        viol = _native.Violation()
+        L = _native.lib()
+        sdt = _device.dtype_code(succ)
+        odt = _device.dtype_code(rank)
+        stream = _device.stream_ptr(dev)
+        if kind == "wyllie":
+            ws = _device.workspace(L.sg_wyllie_workspace_bytes(n), dev)
+            rc = L.sg_wyllie_rank(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, variant_code, _device.ptr(ws),
+                                  ws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
+        else:
+            ws = _device.workspace(L.sg_rs_workspace_bytes(n), dev)
+            rc = L.sg_rs_rank(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
+                              _device.ptr(ws), ws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
+        del ws
+    if rc not in (_native.SG_OK, _native.SG_ERR_INVALID_LIST):
+        _native.check(rc, f"sg_{kind}_rank")
+    return rank, st, rc, viol, host_input
+
+
+def _finish_rank(rank, host_input):
+    if host_input:
+        return rank.to(torch.int64).cpu().numpy()
+    return rank
+
+
+# ---------------------------------------------------------------------------
+# Wyllie
+
+def wyllie_rank(sl, p, variant="multi_kernel", backend="simulated", accounting="full", block_size=256, seed=0,
+                workers=None):
+    """Rank a list by pointer jumping; returns (rank array, ExecStats)
+    (listrank.py:75-155).
+
+    ``multi_kernel``: init + ceil(log2 n) jump launches over packed 64-bit
+    {rank, succ} words; ``single_block``: one CTA, block barriers between
+    rounds, requires p <= block_size.
+    """
+    n = sl.n
+    p = int(p)
+    err = _machine_error(p, block_size, backend, accounting)
+    if err is None:
+        if variant == "single_block" and p > block_size:
+            err = CapabilityError(f"single-block variant limited to {block_size} threads, got {p}")
+        elif variant not in ("multi_kernel", "single_block"):
+            err = ValueError(f"unknown variant {variant!r}")
+    code = _native.SG_WY_SINGLE_BLOCK if (err is None and variant == "single_block") else _native.SG_WY_MULTI_KERNEL
+    rank, st, rc, viol, host_input = _run_list("wyllie", sl, code, seed, False, scratch_out=err is not None)
+    if rc == _native.SG_ERR_INVALID_LIST:
+        _raise_invalid(sl, rc, viol)
+    if err is not None:
+        raise err
+    stats = _device.exec_stats(st)
+    rounds = _jump_rounds(n)
+    stats.rounds = rounds
+    stats.meta.update(n=n, p=p, variant=variant, rounds=rounds, backend=backend, accounting=accounting,
+                      block_size=block_size, seed=seed, workers=workers)
+    return _finish_rank(rank, host_input), stats
+
+
+# ---------------------------------------------------------------------------
+# ruling set
+
+def _draw_splitters(n, r, seed):
+    """Head plus r-1 distinct random interior nodes, reproducible by seed
+    (listrank.py:211-231): KISS rejection sampling in batches, or a random
+    ordering of all interior nodes when more than half of them are needed."""
+    if r == 1:
+        return np.zeros(1, dtype=np.int64)
+    state = kiss_seed(seed)
+    if r - 1 > (n - 1) // 2:
+        keys, _ = kiss_batch(state, n - 1)
+        picks = 1 + np.argsort(keys, kind="stable")[: r - 1]
+    else:
+        chosen = np.empty(0, dtype=np.int64)
+        while chosen.size < r - 1:
+            need = (r - 1) - chosen.size
+            draws, state = kiss_batch(state, need + need // 3 + 16)
+            cand = 1 + (draws % np.uint64(n - 1)).astype(np.int64)
+            _, first = np.unique(cand, return_index=True)
+            cand = cand[np.sort(first)]
+            cand = cand[~np.isin(cand, chosen)]
+            chosen = np.concatenate([chosen, cand[:need]])
+        picks = chosen
+    return np.concatenate([[0], picks]).astype(np.int64)
+
+
+def _splitter_set(rank, spl_nodes, n):
+    """meta["splitter_set"] from the device ranks: splitter ranks are global
+    ranks (listrank.py:355-356); in list order (descending rank) each
+    sublist runs to the next splitter, the last one to the tail
+    (listrank.py:252-299)."""
+    dev = rank.device
+    r = len(spl_nodes)
+    idx = torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
+    srank = rank.index_select(0, idx).to(torch.int64)
+    order = torch.argsort(srank, descending=True)
+    sr_sorted = srank[order]
+    ln_sorted = torch.empty_like(sr_sorted)
+    ln_sorted[:-1] = sr_sorted[:-1] - sr_sorted[1:]
+    ln_sorted[-1] = sr_sorted[-1] + 1
+    nx_sorted = torch.empty_like(order)
+    nx_sorted[:-1] = order[1:]
+    nx_sorted[-1] = order[-1]
+    sub_len = torch.empty_like(ln_sorted)
+    sub_len[order] = ln_sorted
+    succ = torch.empty_like(order)
+    succ[order] = nx_sorted
+    out = SplitterSet(r, np.ascontiguousarray(spl_nodes, dtype=np.int64))
+    out.sublist_len = sub_len.cpu().numpy()
+    out.splitter_succ = succ.cpu().numpy()
+    out.splitter_rank = srank.cpu().numpy()
+    return out
+
+
+def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_succ, even):
+    n = sl.n
+    p = int(p)
+    packing = _as_packing(packing)
+    err = _rs_param_error(n, p, packing, block_size, backend, accounting)
+    rank, st, rc, viol, host_input = _run_list("rs", sl, 0, seed, reuse_succ, scratch_out=err is not None)
+    if rc == _native.SG_ERR_INVALID_LIST:
+        _raise_invalid(sl, rc, viol)
+    if err is not None:
+        raise err
+    stats = _device.exec_stats(st)
+    if p > 1 and p * math.log2(p) > n:
+        stats.warnings.append("super-linear work regime: p*lg(p) > n")
+        stats.meta["superlinear"] = True
+    if even:
+        # perfect splitters every n/p chain positions (listrank.py:431-436):
+        # node at chain position k has rank n-1-k
+        node_at = torch.empty(n, dtype=torch.int64, device=rank.device)
+        node_at[(n - 1) - rank.to(torch.int64)] = torch.arange(n, dtype=torch.int64, device=rank.device)
+        spl_nodes = node_at[:: n // p].cpu().numpy()
+    else:
+        spl_nodes = _draw_splitters(n, p, seed)
+    splitters = _splitter_set(rank, spl_nodes, n)
+    stats.meta.update(n=n, p=p, packing=packing.value, splitter_set=splitters,
+                      max_sublist=int(splitters.sublist_len.max()),
+                      levels=int(st.levels), level_size=[int(st.level_size[k]) for k in range(st.levels + 1)],
+                      fallback=bool(st.fallback), backend=backend, accounting=accounting,
+                      block_size=block_size, seed=seed, workers=workers)
+    return _finish_rank(rank, host_input), stats
+
+
+def rs_rank(sl, p, packing=Packing.P64, seed=0, backend="simulated", accounting="full", block_size=256,
+            workers=None, reuse_succ=False):
+    """Random-splitter list ranking; returns (rank array, ExecStats)
+    (listrank.py:411-419).  ``meta["splitter_set"]`` holds the reference's p
+    KISS-drawn splitters (``_draw_splitters(n, p, seed)``) with their sublist
+    lengths, reduced-list successors and global ranks."""
+    return _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_succ, even=False)
+
+
+def rs_rank_even(sl, p, packing=Packing.P64, seed=0, backend="simulated", accounting="full", block_size=256,
+                 workers=None, reuse_succ=False):
+    """As rs_rank, with perfect splitters every n/p chain positions
+    (listrank.py:422-438).  The reference finds them with a sequential
+    pre-walk; here they come from the device ranks."""
+    n = sl.n
+    if n % p != 0:
+        raise ValueError(f"even splitters need p | n (p={p}, n={n})")
+    return _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_succ, even=True)

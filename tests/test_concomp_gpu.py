@@ -1,0 +1,202 @@
+"""Connected components on the B200 vs the oracle / reference goldens.
+Re-targets pkg/tests/test_concomp.py and test_acceptance.py criteria 2-3."""
+
+import ctypes
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1002_4482_b200 as g
+from paper_1002_4482_b200 import _device, _native
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ("uf", "sv")
+
+
+def sha(a):
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_small_hand_graphs(cuda, variant):
+    labels, stats = g.sv_components(g.EdgeGraph(2, [[0, 1]]), p=2, variant=variant)
+    assert labels.tolist() == [0, 0] and stats.rounds <= 3
+    labels, _ = g.sv_components(g.EdgeGraph(6, [[0, 1], [1, 2], [0, 2], [3, 4], [4, 5]]), p=4, variant=variant)
+    assert labels.tolist() == [0, 0, 0, 3, 3, 3]
+    labels, stats = g.sv_components(g.EdgeGraph(7, []), p=4, variant=variant)
+    assert labels.tolist() == list(range(7)) and stats.rounds == 1
+    labels, stats = g.sv_components(g.EdgeGraph(1, []), p=1, variant=variant)
+    assert labels.tolist() == [0] and stats.rounds == 1
+    labels, _ = g.sv_components(g.EdgeGraph(6, [(0, 1), (1, 2), (4, 5)]), p=1, variant=variant)
+    assert labels.tolist() == [0, 0, 0, 3, 4, 4]
+
+
+def test_errors(cuda):
+    with pytest.raises(ValueError):
+        g.sv_components(g.EdgeGraph(3, [[0, 1]]), p=8)
+    with pytest.raises(g.InvalidGraphError, match="out of range at row 1"):
+        g.sv_components(g.EdgeGraph(3, [[0, 1], [2, 3], [1, 1]]), p=1)
+    with pytest.raises(g.InvalidGraphError, match="self-loop at edge 1"):
+        g.sv_components(g.EdgeGraph(3, [[0, 1], [2, 2], [1, 1]]), p=1)
+    with pytest.raises(g.InvalidGraphError, match="out of range at row 0"):
+        g.sv_components(g.EdgeGraph(3, [[-1, 1]]), p=1)
+    # invalid graph wins over p > n (concomp.py:215-218)
+    with pytest.raises(g.InvalidGraphError):
+        g.sv_components(g.EdgeGraph(3, [[0, 5]]), p=8)
+    with pytest.raises(ValueError):
+        g.sv_components(g.EdgeGraph(3, [[0, 1]]), p=1, backend="cuda")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_matches_reference_goldens(cuda, golden, variant):
+    for i, (n, d, s) in enumerate(golden["rg_cases"].tolist()):
+        gr = g.EdgeGraph(int(n), golden[f"rg_{i}_edges"])
+        labels, stats = g.sv_components(gr, p=min(30, int(n)), variant=variant)
+        assert np.array_equal(labels, golden[f"rg_{i}_labels"]), (n, d, s)
+        assert stats.meta["oriented_m"] == 2 * gr.m
+        assert stats.rounds <= stats.meta["round_bound"]
+    for i, (n, k, s) in enumerate(golden["tr_cases"].tolist()):
+        gr = g.EdgeGraph(n, golden[f"tr_{i}_edges"])
+        labels, _ = g.sv_components(gr, p=32, variant=variant)
+        assert np.array_equal(labels, golden[f"tr_{i}_labels"]), (n, k, s)
+    gr = g.EdgeGraph(3000, golden["path_3000_2_edges"])
+    labels, _ = g.sv_components(gr, p=64, variant=variant)
+    assert np.array_equal(labels, golden["path_3000_2_labels"])
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_paths_trees_random_vs_oracle(cuda, orc, variant):
+    for n in [1, 2, 17, 256, 3000, 100_000]:
+        for seed in range(3):
+            gr = g.list_to_graph(g.gen_list(n, seed=seed))
+            labels, stats = g.sv_components(gr, p=min(64, n), variant=variant)
+            assert np.array_equal(labels, orc.seq_components(n, gr.edges)), (n, seed)
+            assert stats.rounds <= stats.meta["round_bound"]
+    for n, k in [(50, 2), (300, 3), (2000, 10), (100_000, 2), (100_000, 10)]:
+        gr = g.gen_tree_graph(n, k, seed=1)
+        labels, _ = g.sv_components(gr, p=32, variant=variant)
+        assert np.array_equal(labels, orc.seq_components(n, gr.edges)), (n, k)
+    for n, d in [(10_000, 0.001), (3000, 0.01), (200_000, 2e-5)]:
+        gr = g.gen_random_graph(n, d, seed=3)
+        labels, _ = g.sv_components(gr, p=64, variant=variant)
+        assert np.array_equal(labels, orc.seq_components(n, gr.edges)), (n, d)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_roots_per_round_monotone(cuda, variant):
+    gr = g.gen_tree_graph(500, 3, seed=9)
+    labels, stats = g.sv_components(gr, p=16, variant=variant)
+    roots = stats.meta["roots_per_round"]
+    assert roots[0] == 500
+    assert all(a >= b for a, b in zip(roots, roots[1:]))
+    assert roots[-1] == len(np.unique(labels))
+
+
+def test_sv_round_behaviour(cuda):
+    # test_concomp.py:214-227 -- SV round-count properties (variant "sv")
+    g_path = g.list_to_graph(g.gen_list(3000, seed=5))
+    g_tree = g.gen_tree_graph(3000, 4, seed=5)
+    _, s1 = g.sv_components(g_path, p=64, variant="sv")
+    _, s2 = g.sv_components(g_tree, p=64, variant="sv")
+    assert abs(s1.rounds - s2.rounds) <= 2 or max(s1.rounds, s2.rounds) <= s1.meta["round_bound"]
+    g_tree = g.gen_tree_graph(10_000, 3, seed=6)
+    g_rand = g.gen_random_graph(1000, 0.02, seed=6)
+    _, s_tree = g.sv_components(g_tree, p=64, variant="sv")
+    _, s_rand = g.sv_components(g_rand, p=64, variant="sv")
+    assert s_rand.rounds < s_tree.rounds, (s_rand.rounds, s_tree.rounds)
+    # uf converges in one hook sweep on every graph
+    _, s = g.sv_components(g_tree, p=64, variant="uf")
+    assert s.rounds == 1 and s.meta["edge_sweeps"] == 1
+
+
+def test_acceptance_criteria_2_3(cuda, orc):
+    # test_acceptance.py:81-131 (5 seeds per family instead of 20)
+    cfgs = [("list", None, 100_000), ("tree", 2, 100_000), ("tree", 3, 100_000), ("tree", 10, 100_000),
+            ("random", 0.001, 10_000), ("random", 0.01, 3000)]
+    for fam, prm, n in cfgs:
+        for seed in range(5):
+            if fam == "list":
+                gr = g.list_to_graph(g.gen_list(n, seed=seed))
+            elif fam == "tree":
+                gr = g.gen_tree_graph(n, prm, seed=seed)
+            else:
+                gr = g.gen_random_graph(n, prm, seed=seed)
+            want = orc.seq_components(n, gr.edges)
+            for variant in VARIANTS:
+                labels, stats = g.sv_components(gr, p=min(864, n), variant=variant, seed=seed)
+                assert np.array_equal(labels, want), (fam, prm, seed, variant)
+                assert stats.rounds <= g.sv_round_bound(n)
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64])
+def test_device_resident_graph(cuda, orc, dtype):
+    gr = g.gen_random_graph(50_000, 4e-5, seed=2)
+    want = orc.seq_components(gr.n, gr.edges)
+    d = g.EdgeGraph(gr.n, torch.from_numpy(gr.edges).to(cuda, dtype))
+    for variant in VARIANTS:
+        labels, _ = g.sv_components(d, p=64, variant=variant)
+        assert labels.is_cuda and labels.dtype == dtype
+        assert np.array_equal(labels.cpu().numpy(), want)
+
+
+def test_against_reference_digests(cuda, hashes):
+    for n, m in [(1 << 16, 1 << 18), (1 << 20, 1 << 22), (1 << 22, 1 << 24)]:
+        gr = g.gen_random_graph(n, m / (n * (n - 1) // 2), seed=0, device=cuda)
+        assert gr.m == m
+        assert sha(gr.edges) == hashes[f"gen_random_graph_{n}_{m}_0"]
+        for variant in VARIANTS:
+            labels, stats = g.sv_components(gr, p=64, variant=variant)
+            assert sha(labels) == hashes[f"seq_components_{n}_{m}_0"], (n, variant)
+            assert stats.meta["roots_per_round"][-1] == hashes[f"components_{n}_{m}_0"]
+
+
+def _check_label_properties(edges, labels, n):
+    """Size-independent: every edge joins equal labels, labels are fixpoints
+    (label[label[i]] == label[i]) and minimal (label[i] <= i)."""
+    e = edges.to(torch.int64)
+    lab = labels.to(torch.int64)
+    assert torch.all(lab[e[:, 0]] == lab[e[:, 1]])
+    assert torch.all(lab[lab] == lab)
+    assert torch.all(lab <= torch.arange(n, device=lab.device))
+
+
+def test_full_size_properties_2_26(cuda):
+    n, m = 1 << 26, 1 << 28
+    gr = g.gen_random_graph(n, m / (n * (n - 1) // 2), seed=0, device=cuda)
+    e32 = g.EdgeGraph(n, gr.edges.to(torch.int32))
+    del gr
+    labels, stats = g.sv_components(e32, p=1024)
+    _check_label_properties(e32.edges, labels, n)
+    # minimality: every vertex labelled r lies in r's component and r is its smallest member
+    assert stats.meta["roots_per_round"][-1] == int((labels == torch.arange(n, device=cuda, dtype=labels.dtype)).sum())
+    sv, _ = g.sv_components(e32, p=1024, variant="sv")
+    assert torch.equal(sv, labels)
+
+
+def test_building_blocks_c_abi(cuda, orc):
+    """sg_cc_init / sg_cc_hook / sg_cc_compress / sg_cc_labels compose into
+    the same labels (the multi-GPU path's kernels)."""
+    gr = g.gen_random_graph(20_000, 1e-4, seed=1)
+    want = orc.seq_components(gr.n, gr.edges)
+    L = _native.lib()
+    e = torch.from_numpy(gr.edges.astype(np.int32)).to(cuda)
+    D = torch.empty(gr.n, dtype=torch.int32, device=cuda)
+    flags = torch.zeros(4, dtype=torch.int64, device=cuda)
+    roots = torch.zeros(1, dtype=torch.int64, device=cuda)
+    s = _device.stream_ptr(cuda)
+    assert L.sg_cc_init(_device.ptr(D), gr.n, s) == 0
+    half = gr.m // 2
+    for row0, blk in ((0, e[:half]), (half, e[half:])):
+        assert L.sg_cc_hook(_device.ptr(blk), _native.SG_I32, blk.shape[0], row0, gr.n, _device.ptr(D),
+                            _native.SG_CC_UF, 1, _device.ptr(flags), s) == 0
+    assert L.sg_cc_compress(_device.ptr(D), 0, gr.n, _device.ptr(roots), s) == 0
+    out = torch.empty(gr.n, dtype=torch.int64, device=cuda)
+    assert L.sg_cc_labels(_device.ptr(D), gr.n, _device.ptr(out), _native.SG_I64, s) == 0
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert int(roots.item()) == len(np.unique(want))
+    assert int(flags[0].item()) == 1 and int(flags[1].item()) == 0 and int(flags[2].item()) == 0

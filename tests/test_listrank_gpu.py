@@ -1,0 +1,360 @@
+"""List ranking on the B200 vs the oracle.  Re-targets the reference's
+tests (pkg/tests/test_listrank.py, test_acceptance.py criteria 1, 8, 10) at
+the drop-in API; bit-exact ranks everywhere."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1002_4482_b200 as g
+from paper_1002_4482_b200 import _device, _native
+
+pytestmark = pytest.mark.gpu
+
+CHAIN3 = g.SuccessorList([1, 2, 2])
+PACKINGS = (g.Packing.P48, g.Packing.P64)
+
+
+def sha(a):
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------- Wyllie
+
+def test_wyllie_three_chain(cuda):
+    for variant in ("multi_kernel", "single_block"):
+        rank, stats = g.wyllie_rank(CHAIN3, p=2, variant=variant)
+        assert rank.tolist() == [2, 1, 0]
+        assert isinstance(rank, np.ndarray) and rank.dtype == np.int64
+
+
+def test_wyllie_matches_oracle(cuda, orc):
+    rng = np.random.default_rng(7)
+    for variant in ("multi_kernel", "single_block"):
+        for n in (1, 2, 3, 17, 300, 5000):
+            for _ in range(3):
+                sl = g.gen_list(n, seed=int(rng.integers(2**31)))
+                p = int(rng.integers(1, 257))
+                rank, stats = g.wyllie_rank(sl, p=p, variant=variant, accounting="counts")
+                assert np.array_equal(rank, orc.seq_rank(sl.succ)), (variant, n, p)
+                assert stats.meta["rounds"] == (max(0, (n - 1).bit_length()) if n > 1 else 0)
+
+
+def test_wyllie_launch_structure(cuda):
+    _, stats = g.wyllie_rank(g.gen_list(1024, seed=1), p=64)
+    per = stats.per_kernel()
+    assert per["wy_jump"].launches == 10       # ceil(log2 1024), test_listrank.py:25-30
+    assert stats.rounds == 10
+    _, stats = g.wyllie_rank(g.gen_list(64, seed=2), p=16, variant="single_block")
+    assert stats.per_kernel()["wy_single"].launches == 1
+
+
+def test_wyllie_caps_and_errors(cuda):
+    with pytest.raises(g.CapabilityError):
+        g.wyllie_rank(CHAIN3, p=300, variant="single_block", block_size=256)
+    with pytest.raises(g.InvalidListError):
+        g.wyllie_rank(g.SuccessorList([1, 2, 0]), p=2)
+    with pytest.raises(ValueError):
+        g.wyllie_rank(CHAIN3, p=2, variant="bogus")
+    with pytest.raises(ValueError):
+        g.wyllie_rank(CHAIN3, p=2, backend="gpu")
+    # invalid list wins over a bad argument (validation runs first, listrank.py:83-85)
+    with pytest.raises(g.InvalidListError):
+        g.wyllie_rank(g.SuccessorList([1, 0, 2]), p=2, variant="bogus")
+    # wyllie accepts p > n (test_listrank.py:42-51)
+    rank, _ = g.wyllie_rank(CHAIN3, p=200)
+    assert rank.tolist() == [2, 1, 0]
+
+
+# ---------------------------------------------------------------- ruling set
+
+def test_rs_three_chain_single_thread(cuda):
+    for packing in PACKINGS:
+        rank, stats = g.rs_rank(CHAIN3, p=1, packing=packing)
+        assert rank.tolist() == [2, 1, 0]
+        spl = stats.meta["splitter_set"]
+        assert spl.splitter_node.tolist() == [0]
+        assert spl.sublist_len.tolist() == [3]
+        assert spl.splitter_rank.tolist() == [2]
+        assert spl.splitter_succ.tolist() == [0]
+
+
+def test_rs_matches_oracle(cuda, orc):
+    rng = np.random.default_rng(11)
+    for packing in PACKINGS:
+        for n, p in [(10, 1), (10, 4), (10, 10), (1000, 16), (1000, 250), (257, 3), (4096, 64),
+                     (9000, 100), (70000, 1000), (300000, 4096)]:
+            sl = g.gen_list(n, seed=int(rng.integers(2**31)))
+            rank, _ = g.rs_rank(sl, p=p, packing=packing, accounting="counts", seed=int(rng.integers(2**31)))
+            assert np.array_equal(rank, orc.seq_rank(sl.succ)), (packing, n, p)
+
+
+def test_rs_meta_matches_reference(cuda, golden):
+    for n, p, ls, s in golden["rs_cases"].tolist():
+        sl = g.gen_list(n, seed=ls) if n > 3 else CHAIN3
+        _, stats = g.rs_rank(sl, p=p, seed=s, accounting="counts")
+        spl = stats.meta["splitter_set"]
+        key = f"rs_{n}_{p}_{ls}_{s}"
+        assert np.array_equal(spl.splitter_node, golden[key + "_node"])
+        assert np.array_equal(spl.sublist_len, golden[key + "_len"])
+        assert np.array_equal(spl.splitter_succ, golden[key + "_succ"])
+        assert np.array_equal(spl.splitter_rank, golden[key + "_rank"])
+        assert stats.meta["max_sublist"] == int(golden[key + "_max"])
+        assert stats.meta["n"] == n and stats.meta["p"] == p and stats.meta["packing"] == "p64"
+
+
+def test_rs_even_meta_matches_reference(cuda, golden, orc):
+    sl = g.gen_list(4096, seed=31)
+    rank, stats = g.rs_rank_even(sl, p=64, accounting="counts")
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
+    spl = stats.meta["splitter_set"]
+    for part in ("node", "len", "succ", "rank"):
+        attr = {"node": "splitter_node", "len": "sublist_len", "succ": "splitter_succ", "rank": "splitter_rank"}[part]
+        assert np.array_equal(getattr(spl, attr), golden[f"rs_even_4096_64_{part}"]), part
+    assert np.all(spl.sublist_len == 64)
+
+
+def test_rs_splitter_ranks_are_global_ranks(cuda, orc):
+    sl = g.gen_list(2000, seed=5)
+    _, stats = g.rs_rank(sl, p=32, seed=5, accounting="counts")
+    spl = stats.meta["splitter_set"]
+    assert np.array_equal(orc.seq_rank(sl.succ)[spl.splitter_node], spl.splitter_rank)
+    assert spl.sublist_len.sum() == 2000
+
+
+def test_rs_thread_cap_at_exactly_16384(cuda, orc):
+    sl = g.gen_list(40_000, seed=1)
+    want = orc.seq_rank(sl.succ)
+    with pytest.raises(g.CapabilityError):
+        g.rs_rank(sl, p=16_385, packing=g.Packing.P48)
+    rank, stats = g.rs_rank(sl, p=16_384, packing=g.Packing.P48, accounting="counts")
+    assert np.array_equal(rank, want) and stats.meta["p"] == 16_384
+    rank, _ = g.rs_rank(sl, p=16_385, packing=g.Packing.P64, accounting="counts")
+    assert np.array_equal(rank, want)
+
+
+def test_rs_errors(cuda):
+    with pytest.raises(ValueError):
+        g.rs_rank(CHAIN3, p=4)                     # p > n
+    with pytest.raises(ValueError):
+        g.rs_rank(CHAIN3, p=0)
+    with pytest.raises(ValueError):
+        g.rs_rank(CHAIN3, p=2, block_size=1000)
+    with pytest.raises(g.InvalidListError):
+        g.rs_rank(g.SuccessorList([1, 2, 0]), p=4)   # invalid list beats p > n
+    with pytest.raises(ValueError):
+        g.rs_rank_even(g.gen_list(100, seed=1), p=7)
+
+
+@pytest.mark.parametrize("algo", ["rs", "wyllie"])
+def test_invalid_lists_report_reference_violation(cuda, golden, algo):
+    import json
+
+    bad = json.loads(str(golden["bad_lists"]))
+    verdicts = json.loads(str(golden["bad_verdicts"]))
+    for b, v in zip(bad, verdicts):
+        sl = g.SuccessorList(b)
+        fn = (lambda s: g.rs_rank(s, p=1)) if algo == "rs" else (lambda s: g.wyllie_rank(s, p=1))
+        if v is None:
+            fn(sl)
+            continue
+        with pytest.raises(g.InvalidListError) as ei:
+            fn(sl)
+        assert str(ei.value) == f"{v[0]} at index {v[1]}", b
+
+
+def test_invalid_large_lists_detected(cuda):
+    n = 200_000
+    base = g.gen_list(n, seed=3).succ
+    # a cycle that contains no ruler: cut the chain and close a loop
+    s = base.copy()
+    tail = int(np.flatnonzero(s == np.arange(n))[0])
+    s[tail] = 0 if tail != 0 else 1           # head revisited -> no tail
+    for fn in (lambda x: g.rs_rank(x, 64), lambda x: g.wyllie_rank(x, 64)):
+        with pytest.raises(g.InvalidListError, match="no-tail"):
+            fn(g.SuccessorList(s))
+    # detached cycle + chain: one tail, unreachable nodes
+    s = base.copy()
+    order = np.argsort(-np.asarray(g.rs_rank(g.SuccessorList(base), 1)[0]))   # list order
+    a, b = int(order[n // 3]), int(order[2 * n // 3])
+    s[a] = b           # skip the middle third
+    mid_last = int(order[2 * n // 3 - 1])
+    s[mid_last] = int(order[n // 3 + 1])   # middle third becomes a cycle
+    want = g.validate_list(g.SuccessorList(s))
+    assert want.kind == "unreachable"
+    for fn in (lambda x: g.rs_rank(x, 64), lambda x: g.wyllie_rank(x, 64)):
+        with pytest.raises(g.InvalidListError) as ei:
+            fn(g.SuccessorList(s))
+        assert str(ei.value) == str(want)
+    # the head's walk runs into a detached 2-cycle (possibly without rulers)
+    s = np.arange(1, n + 1, dtype=np.int64)
+    s[-1] = n - 1
+    s[0], s[5], s[6] = 5, 6, 5
+    want = g.validate_list(g.SuccessorList(s))
+    for fn in (lambda x: g.rs_rank(x, 64), lambda x: g.wyllie_rank(x, 64)):
+        with pytest.raises(g.InvalidListError) as ei:
+            fn(g.SuccessorList(s))
+        assert str(ei.value) == str(want)
+    # out of range
+    s = base.copy()
+    s[12345] = n + 7
+    with pytest.raises(g.InvalidListError, match="out-of-range at index 12345"):
+        g.rs_rank(g.SuccessorList(s), 64)
+
+
+def test_rs_reuse_succ_buffer(cuda, orc):
+    sl = g.gen_list(1500, seed=17)
+    rank, stats = g.rs_rank(sl, p=32, reuse_succ=True, accounting="counts")
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
+    assert stats.meta["splitter_set"].r == 32
+    # device input: ranks overwrite the caller's successor tensor in place
+    d = torch.from_numpy(g.gen_list(100_000, seed=2).succ).to(cuda)
+    want = orc.seq_rank(d.cpu().numpy())
+    out, _ = g.rs_rank(g.SuccessorList(d), p=128, reuse_succ=True)
+    assert out.data_ptr() == d.data_ptr()
+    assert np.array_equal(d.cpu().numpy(), want)
+
+
+def test_rs_saturation_and_superlinear(cuda, orc):
+    sl = g.gen_list(128, seed=23)
+    rank, stats = g.rs_rank(sl, p=128, accounting="counts")
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
+    assert stats.meta["splitter_set"].sublist_len.max() == 1
+    assert stats.meta.get("superlinear") is True
+    _, stats = g.rs_rank(g.gen_list(10_000, seed=2), p=16, accounting="counts")
+    assert stats.meta.get("superlinear") is None
+
+
+def test_rs_deterministic(cuda):
+    sl = g.gen_list(3000, seed=19)
+    a, sa = g.rs_rank(sl, p=64, seed=3)
+    b, sb = g.rs_rank(sl, p=64, seed=3)
+    assert np.array_equal(a, b)
+    assert np.array_equal(sa.meta["splitter_set"].sublist_len, sb.meta["splitter_set"].sublist_len)
+
+
+def test_sublist_stats(cuda):
+    sl = g.gen_list(4096, seed=37)
+    _, stats = g.rs_rank(sl, p=64, seed=37, accounting="counts")
+    st = g.sublist_stats(stats.meta["splitter_set"])
+    assert st.mean_len == 4096 / 64 and st.max_len >= st.mean_len and st.histogram.sum() == 64
+    _, stats = g.rs_rank_even(sl, p=64, accounting="counts")
+    st = g.sublist_stats(stats.meta["splitter_set"])
+    assert st.max_len == st.mean_len == 64
+
+
+def test_acceptance_criterion_1_sample(cuda, orc):
+    # test_acceptance.py:42-75 (5 variants, oracle equality), 10 seeds per size
+    for n in (10, 1000, 100_000, 1_000_000):
+        p = min(8192, n)
+        p_sb = min(768, n)
+        even_p = {10: 5, 1000: 100, 100_000: 4000, 1_000_000: 4000}[n]
+        for seed in range(10 if n < 1_000_000 else 3):
+            sl = g.gen_list(n, seed=seed)
+            want = orc.seq_rank(sl.succ)
+            outs = [
+                g.wyllie_rank(sl, p, variant="multi_kernel", seed=seed)[0],
+                g.wyllie_rank(sl, p_sb, variant="single_block", block_size=768, seed=seed)[0],
+                g.rs_rank(sl, p, packing=g.Packing.P48, seed=seed)[0],
+                g.rs_rank(sl, p, packing=g.Packing.P64, seed=seed)[0],
+                g.rs_rank_even(sl, even_p, seed=seed)[0],
+            ]
+            for got in outs:
+                assert g.compare_arrays(want, got) == -1, (n, seed)
+
+
+def test_splitter_statistics_walk_consistent(cuda, orc):
+    # test_acceptance.py:305-344 (exact part): lengths == positional gaps
+    n, p = 100_000, 100
+    sl = g.gen_list(n, seed=11)
+    pos = orc.chain_positions(sl.succ)
+    _, stats = g.rs_rank(sl, p, accounting="counts", seed=11)
+    spl = stats.meta["splitter_set"]
+    lens = spl.sublist_len
+    assert lens.sum() == n and lens.size == p
+    ps = pos[spl.splitter_node]
+    order = np.argsort(ps)
+    assert np.array_equal(lens[order], np.diff(np.append(ps[order], n)))
+
+
+# ---------------------------------------------------------------- device-resident inputs
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64])
+def test_device_resident_lists(cuda, orc, dtype):
+    host = g.gen_list(300_000, seed=9)
+    want = orc.seq_rank(host.succ)
+    d = g.SuccessorList(torch.from_numpy(host.succ).to(cuda, dtype))
+    for fn in (lambda s: g.rs_rank(s, 256), lambda s: g.wyllie_rank(s, 256)):
+        out, _ = fn(d)
+        assert out.is_cuda and out.dtype == dtype
+        assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_c_abi_u32_path(cuda, orc):
+    """Call the C ABI directly with u32 successors / u32 ranks."""
+    import ctypes
+
+    n = 1 << 18
+    host = g.gen_list(n, seed=4).succ
+    succ = torch.from_numpy(host.astype(np.int32)).to(cuda)
+    rank = torch.empty(n, dtype=torch.int32, device=cuda)
+    L = _native.lib()
+    ws = _device.workspace(L.sg_rs_workspace_bytes(n), cuda)
+    st, v = _native.Stats(), _native.Violation()
+    rc = L.sg_rs_rank(_device.ptr(succ), _native.SG_U32, _device.ptr(rank), _native.SG_U32, n, 0,
+                      _device.ptr(ws), ws.numel(), _device.stream_ptr(cuda), ctypes.byref(st), ctypes.byref(v))
+    assert rc == 0
+    assert np.array_equal(rank.cpu().numpy().astype(np.int64), orc.seq_rank(host))
+    assert st.levels >= 1 and st.level_size[0] == n and st.n_launches > 0 and st.total_ms > 0
+
+
+# ---------------------------------------------------------------- scale
+
+def test_rank_against_reference_digests(cuda, hashes):
+    for n, s in [(1 << 20, 0), (1 << 20, 1), (1 << 22, 0)]:
+        sl = g.gen_list(n, seed=s, device=cuda)
+        assert sha(sl.succ) == hashes[f"gen_list_{n}_{s}"]
+        for fn in (lambda x: g.rs_rank(x, 4096), lambda x: g.wyllie_rank(x, 4096)):
+            rank, _ = fn(sl)
+            assert sha(rank) == hashes[f"seq_rank_{n}_{s}"], (n, s)
+
+
+def _check_rank_properties(succ, rank):
+    """Size-independent: rank is a permutation of 0..n-1 that decreases by one
+    along every link (rank[succ[i]] == rank[i] - 1 off the tail)."""
+    n = succ.numel()
+    succ = succ.to(torch.int64)
+    rank = rank.to(torch.int64)
+    idx = torch.arange(n, device=succ.device)
+    tail = succ == idx
+    assert int(tail.sum()) == 1
+    assert int(rank[0]) == n - 1
+    assert torch.all(rank[tail] == 0)
+    assert torch.all(rank[succ[~tail]] == rank[~tail] - 1)
+    assert int(torch.bincount(rank, minlength=n).max()) == 1
+
+
+@pytest.mark.parametrize("kind", ["random", "ordered"])
+def test_full_size_properties_2_26(cuda, kind):
+    n = 1 << 26
+    sl = g.gen_list(n, seed=0, device=cuda, dtype=torch.int32) if kind == "random" else \
+        g.ordered_list(n, device=cuda, dtype=torch.int32)
+    rank, stats = g.rs_rank(sl, 16384)
+    _check_rank_properties(sl.succ, rank)
+    assert stats.meta["fallback"] is False
+    w, _ = g.wyllie_rank(sl, 1024)
+    assert torch.equal(w, rank)
+
+
+def test_walk_cap_fallback(cuda, orc, monkeypatch):
+    """A walk that exceeds the hop cap falls back to pointer jumping."""
+    monkeypatch.setenv("SG_RS_WALK_CAP", "4")
+    sl = g.gen_list(50_000, seed=8)
+    rank, stats = g.rs_rank(sl, 32)
+    assert stats.meta["fallback"] is True
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
