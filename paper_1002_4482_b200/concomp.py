@@ -96,7 +96,7 @@ def sv_components(graph, p, backend="simulated", accounting="full", block_size=2
                       variant=variant, edge_sweeps=int(st.edge_sweeps), vertex_sweeps=int(st.vertex_sweeps),
                       backend=backend, accounting=accounting, block_size=block_size, seed=seed, workers=workers)
     if host_input:
-        return labels.cpu().numpy(), stats
+        return _device.to_host_numpy(labels), stats
     return labels, stats
 
 

@@ -306,6 +306,7 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
     if (n >= 0x7FFFFFFFull) return SG_ERR_CAPABILITY;
     if (variant != SG_CC_UF && variant != SG_CC_SV) return SG_ERR_VALUE;
     if (label_dtype != SG_U32 && label_dtype != SG_I32 && label_dtype != SG_I64) return SG_ERR_VALUE;
+    ::sg::apply_tuning();
     cudaStream_t s = (cudaStream_t)stream;
     if (st) memset(st, 0, sizeof(sg_stats));
     if (viol) {

@@ -67,6 +67,7 @@ struct ListStatus {
 
 // Error plumbing -------------------------------------------------------------
 void set_cuda_error(cudaError_t e);
+void apply_tuning();
 
 #define SG_CUDA(call)                                   \
     do {                                                \

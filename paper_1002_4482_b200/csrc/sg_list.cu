@@ -63,12 +63,23 @@ __device__ __forceinline__ bool is_ruler(uint32_t i, uint32_t kbits, uint32_t sa
     return i == 0u || ((i * PHI + salt) >> (32u - kbits)) == 0u;
 }
 
+template <class T>
+__device__ __forceinline__ T ld_mode(const T* p, int mode) {
+    switch (mode) {
+        case 1: return __ldcg(p);   // L2 only
+        case 2: return __ldcv(p);   // volatile (no cache)
+        case 3: return *p;          // default (L1 + L2)
+        default: return __ldg(p);   // read-only path
+    }
+}
+
 // level-0 view: node i -> (successor, weight 1)
 template <class SuccT>
 struct Level0 {
     const SuccT* succ;
+    int mode;
     __device__ __forceinline__ void load(uint32_t i, unsigned long long& nx, uint32_t& w) const {
-        nx = as_index<SuccT>(__ldg(succ + i));
+        nx = as_index<SuccT>(ld_mode(succ + i, mode));
         w = 1u;
     }
 };
@@ -227,12 +238,28 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count(const SuccT* __restri
         return;
     }
     uint32_t cnt = 0;
+    if (kValidate) {
+        // all loads first (the atomics below would otherwise serialise them)
+        SuccT v[TILE_ITEMS];
 #pragma unroll
-    for (int j = 0; j < TILE_ITEMS; ++j) {
-        const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
-        if (i < N) {
-            if (kValidate) note_succ(st, i, as_index<SuccT>(succ[i]), N);
-            if (census) cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
+        for (int j = 0; j < TILE_ITEMS; ++j) {
+            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+            v[j] = i < N ? __ldcs(succ + i) : SuccT(0);
+        }
+#pragma unroll
+        for (int j = 0; j < TILE_ITEMS; ++j) {
+            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+            if (i < N) {
+                const unsigned long long x = as_index<SuccT>(v[j]);
+                if (x >= N || x == i) note_succ(st, i, x, N);
+            }
+        }
+    }
+    if (census) {
+#pragma unroll
+        for (int j = 0; j < TILE_ITEMS; ++j) {
+            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+            if (i < N) cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
         }
     }
     if (census) {
@@ -478,6 +505,7 @@ __global__ void k_rs_expand_direct(const uint32_t* __restrict__ IS0, OutT* __res
 struct RsPlan {
     int levels = 0;                              // walked levels (final level = levels)
     uint32_t walk_cap = WALK_CAP_HOPS;
+    int load_mode = 0;
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
     unsigned long long cap[SG_MAX_LEVELS + 1] = {};  // node capacity per level
@@ -507,6 +535,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed) {
     const uint32_t kb1 = env_u32("SG_RS_KBITS", 5, 1, 16);
     const uint32_t fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
+    p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
     p.cap[0] = n;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
@@ -620,7 +649,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
         rec.begin(K_RS4_RANK, 0, 1, 1024, n);
-        k_rs_final<Level0<SuccT>><<<1, 1024, 0, s>>>(Level0<SuccT>{succ}, b.fa, b.fb, b.IS[0], b.st, 0);
+        k_rs_final<Level0<SuccT>><<<1, 1024, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.fa, b.fb, b.IS[0], b.st, 0);
         rec.end();
         SG_LAUNCH_CHECK();
         const uint32_t g = grid_for(n, 256, 1, kSMs * 8);
@@ -655,7 +684,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         SG_LAUNCH_CHECK();
         if (k == 0) {
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
-            k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ}, wk, b.spl[0], b.lvl[1],
+            k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, wk, b.spl[0], b.lvl[1],
                                                                         b.st, 0, p.kbits[0], p.salt[0], p.walk_cap);
         } else {
             rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
@@ -815,6 +844,7 @@ int sg_wyllie_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype,
                    size_t ws_bytes, void* stream, sg_stats* st, sg_violation* viol) {
     if (n == 0 || n >= 0xFFFFFFFFull) return SG_ERR_CAPABILITY;
     if (variant != SG_WY_MULTI_KERNEL && variant != SG_WY_SINGLE_BLOCK) return SG_ERR_VALUE;
+    ::sg::apply_tuning();
     if (st) memset(st, 0, sizeof(sg_stats));
     SG_DISPATCH_LIST(wyllie_entry, succ_dtype, rank_dtype, succ, rank, n, variant, ws, ws_bytes, (cudaStream_t)stream,
                      st, viol);
@@ -823,6 +853,7 @@ int sg_wyllie_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype,
 int sg_rs_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype, uint64_t n, uint64_t seed, void* ws,
                size_t ws_bytes, void* stream, sg_stats* st, sg_violation* viol) {
     if (n == 0 || n >= 0xFFFFFFFFull) return SG_ERR_CAPABILITY;
+    ::sg::apply_tuning();
     if (st) memset(st, 0, sizeof(sg_stats));
     SG_DISPATCH_LIST(rs_entry, succ_dtype, rank_dtype, succ, rank, n, seed, ws, ws_bytes, (cudaStream_t)stream, st,
                      viol);

@@ -1,5 +1,7 @@
 // sg_runtime.cu -- library plumbing: status strings, kernel names, the
 // per-call launch recorder (CUDA events on the launching stream).
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -86,6 +88,28 @@ cudaError_t Recorder::finish() {
         if (cudaEventElapsedTime(&ms, ev_[0], ev_.back()) == cudaSuccess) st_->total_ms = ms;
     }
     return cudaSuccess;
+}
+
+// Optional device tuning from the environment, applied once per process and
+// device: SG_L2_FETCH=<bytes> sets cudaLimitMaxL2FetchGranularity (a hint).
+void apply_tuning() {
+    static thread_local int done_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 31 && (done_mask & (1 << dev))) return;
+    if (dev < 31) done_mask |= 1 << dev;
+    const char* s = getenv("SG_L2_FETCH");
+    size_t old = 0;
+    cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity);
+    if (s && *s) {
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atol(s));
+        size_t now = 0;
+        cudaDeviceGetLimit(&now, cudaLimitMaxL2FetchGranularity);
+        if (getenv("SG_DEBUG")) fprintf(stderr, "[sg] L2 fetch granularity %zu -> %zu\n", old, now);
+    } else if (getenv("SG_DEBUG")) {
+        fprintf(stderr, "[sg] L2 fetch granularity %zu\n", old);
+    }
+    cudaGetLastError();
 }
 
 }  // namespace sg

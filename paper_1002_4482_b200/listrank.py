@@ -22,6 +22,7 @@ validated exactly like ``vkm.Machine`` (vkm.py:434-454) and recorded in
 """
 
 import ctypes
+import functools
 import math
 from collections import namedtuple
 from dataclasses import dataclass
@@ -151,7 +152,7 @@ def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False):
 
 def _finish_rank(rank, host_input):
     if host_input:
-        return rank.to(torch.int64).cpu().numpy()
+        return _device.to_host_numpy(rank)
     return rank
 
 
@@ -193,6 +194,12 @@ def wyllie_rank(sl, p, variant="multi_kernel", backend="simulated", accounting="
 # ruling set
 
 def _draw_splitters(n, r, seed):
+    """Cached copy of the reference's splitter draw (deterministic in its arguments)."""
+    return _draw_splitters_cached(int(n), int(r), int(seed)).copy()
+
+
+@functools.lru_cache(maxsize=64)
+def _draw_splitters_cached(n, r, seed):
     """Head plus r-1 distinct random interior nodes, reproducible by seed
     (listrank.py:211-231): KISS rejection sampling in batches, or a random
     ordering of all interior nodes when more than half of them are needed."""
