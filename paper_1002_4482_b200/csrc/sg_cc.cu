@@ -22,7 +22,11 @@
 //    Rounds repeat until a hook sweep changes nothing (the converge-OR of
 //    sv5, concomp.py:183-205).  Hooks only lower parents (min-monotone), so
 //    per-GPU proposals merge exactly with a min all-reduce (multi-GPU path).
+#include <stdlib.h>
 #include <string.h>
+
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "sg_internal.cuh"
 
@@ -80,13 +84,21 @@ __device__ __forceinline__ bool edge_ok(unsigned long long u, unsigned long long
 
 // root of x given p = D[x]; halves the path on the way (benign races: only
 // ever writes an ancestor, never touches a root)
+//
+// Parent reads go through L1: a stale value is still an ancestor (pointers
+// only ever move up), so finds stay correct; the CAS below is L2-coherent and
+// returns the true parent when a stale root was hooked meanwhile.  Reading
+// through L2 only would funnel every find of the giant component into the one
+// L2 sector that holds its root.
+__device__ __forceinline__ uint32_t ld_parent(const uint32_t* p) { return *p; }
+
 __device__ __forceinline__ uint32_t find_from(uint32_t* D, uint32_t x, uint32_t p) {
     while (p != x) {
-        const uint32_t gp = __ldcg(D + p);
+        const uint32_t gp = ld_parent(D + p);
         if (gp == p) return p;
-        __stcg(D + x, gp);
+        D[x] = gp;
         x = gp;
-        p = __ldcg(D + x);
+        p = ld_parent(D + x);
     }
     return x;
 }
@@ -100,7 +112,7 @@ __device__ __forceinline__ bool unite(uint32_t* D, uint32_t u, uint32_t pu, uint
         const uint32_t old = atomicCAS(D + hi, hi, lo);
         if (old == hi) return true;
         // hi was hooked by someone else: continue from its new tree
-        ru = find_from(D, old, __ldcg(D + old));
+        ru = find_from(D, old, ld_parent(D + old));
         rv = lo;
     }
     return false;
@@ -109,10 +121,15 @@ __device__ __forceinline__ bool unite(uint32_t* D, uint32_t u, uint32_t pu, uint
 template <class E, bool kValidate>
 __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned long long m, unsigned long long row0,
                                                              unsigned long long n, uint32_t* D,
-                                                             unsigned long long* flags) {
+                                                             unsigned long long* flags,
+                                                             const unsigned long long* rng) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     bool any = false;
     unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (rng != nullptr) {  // partition [rng[0], rng[1]) of a partitioned edge list
+        i += rng[0];
+        m = rng[1];
+    }
     // two edges per iteration: four independent parent loads in flight
     for (; i + stride < m; i += 2 * stride) {
         unsigned long long u0, v0, u1, v1;
@@ -123,8 +140,8 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned l
             ok0 = edge_ok(u0, v0, n, row0 + i, flags);
             ok1 = edge_ok(u1, v1, n, row0 + i + stride, flags);
         }
-        const uint32_t pu0 = ok0 ? __ldcg(D + u0) : 0, pv0 = ok0 ? __ldcg(D + v0) : 0;
-        const uint32_t pu1 = ok1 ? __ldcg(D + u1) : 0, pv1 = ok1 ? __ldcg(D + v1) : 0;
+        const uint32_t pu0 = ok0 ? ld_parent(D + u0) : 0, pv0 = ok0 ? ld_parent(D + v0) : 0;
+        const uint32_t pu1 = ok1 ? ld_parent(D + u1) : 0, pv1 = ok1 ? ld_parent(D + v1) : 0;
         if (ok0 && pu0 != pv0) any |= unite(D, (uint32_t)u0, pu0, (uint32_t)v0, pv0);
         if (ok1 && pu1 != pv1) any |= unite(D, (uint32_t)u1, pu1, (uint32_t)v1, pv1);
     }
@@ -132,7 +149,7 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned l
         unsigned long long u, v;
         edges.load(i, u, v);
         if (!kValidate || edge_ok(u, v, n, row0 + i, flags)) {
-            const uint32_t pu = __ldcg(D + u), pv = __ldcg(D + v);
+            const uint32_t pu = ld_parent(D + u), pv = ld_parent(D + v);
             if (pu != pv) any |= unite(D, (uint32_t)u, pu, (uint32_t)v, pv);
         }
     }
@@ -145,14 +162,20 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned l
 template <class E, bool kValidate>
 __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_sv(E edges, unsigned long long m, unsigned long long row0,
                                                              unsigned long long n, uint32_t* D,
-                                                             unsigned long long* flags) {
+                                                             unsigned long long* flags,
+                                                             const unsigned long long* rng) {
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     bool any = false;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (rng != nullptr) {
+        i0 += rng[0];
+        m = rng[1];
+    }
+    for (unsigned long long i = i0; i < m; i += stride) {
         unsigned long long u, v;
         edges.load(i, u, v);
         if (kValidate && !edge_ok(u, v, n, row0 + i, flags)) continue;
-        const uint32_t du = __ldcg(D + u), dv = __ldcg(D + v);
+        const uint32_t du = ld_parent(D + u), dv = ld_parent(D + v);
         if (du != dv) {
             const uint32_t hi = du > dv ? du : dv;
             const uint32_t lo = du > dv ? dv : du;
@@ -178,12 +201,12 @@ __global__ void __launch_bounds__(COMP_THREADS) k_cc_compress(uint32_t* D, unsig
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     uint32_t nroots = 0;
     for (unsigned long long i = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
-        uint32_t r = __ldcg(D + i);
+        uint32_t r = ld_parent(D + i);
         if (r == (uint32_t)i) {
             ++nroots;
         } else {
             for (;;) {
-                const uint32_t p = __ldcg(D + r);
+                const uint32_t p = ld_parent(D + r);  // roots do not move during the shortcut
                 if (p == r) break;
                 r = p;
             }
@@ -204,6 +227,177 @@ __global__ void __launch_bounds__(COMP_THREADS) k_cc_labels(const uint32_t* __re
 }
 
 // ---------------------------------------------------------------------------
+// Stable partition of the edge list by the window of its larger endpoint.
+//
+// Stored rows are (u, v) with the random endpoint v (gen.py:215-217 sorts by
+// u), so the parent gathers D[v] scatter over all of D -- 256 MiB at n = 2^26,
+// twice the L2.  Hooking one window of v at a time keeps those gathers (and
+// the CAS / path-halving writes they lead to) in an L2-resident slice of D,
+// while D[u] and the edges stream.  Invalid rows are reported (first
+// offending original row, core.py:196-206) and dropped here.
+
+constexpr int PART_THREADS = 256;
+constexpr int PART_ITEMS = 16;
+constexpr int PART_TILE = PART_THREADS * PART_ITEMS;
+constexpr int MAX_PARTS = 16;
+
+template <class E>
+__device__ __forceinline__ int part_of(E edges, unsigned long long e, unsigned long long m, unsigned long long n,
+                                       uint32_t shift, unsigned long long* flags, bool validate, uint2& uv) {
+    if (e >= m) return -1;
+    unsigned long long u, v;
+    edges.load(e, u, v);
+    if (u >= n || v >= n) {
+        if (validate) atomicMax(flags + 1, ~e);
+        return -1;
+    }
+    if (u == v) {
+        if (validate) atomicMax(flags + 2, ~e);
+        return -1;
+    }
+    uv = make_uint2((uint32_t)u, (uint32_t)v);
+    return (int)((u > v ? u : v) >> shift);
+}
+
+// per-tile counts of each partition; cnt layout [p * ntiles + tile]
+template <class E>
+__global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigned long long m, unsigned long long n,
+                                                                uint32_t shift, int P, unsigned long long ntiles,
+                                                                uint32_t* __restrict__ cnt,
+                                                                unsigned long long* flags) {
+    __shared__ uint32_t s_cnt[MAX_PARTS + 1];
+    if (threadIdx.x <= MAX_PARTS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * PART_TILE + threadIdx.x;
+    const uint32_t lane = lane_id();
+#pragma unroll 4
+    for (int j = 0; j < PART_ITEMS; ++j) {
+        uint2 uv;
+        int p = part_of(edges, e0 + (unsigned long long)j * PART_THREADS, m, n, shift, flags, true, uv);
+        if (p < 0) p = MAX_PARTS;
+        const unsigned mm = __match_any_sync(0xffffffffu, p);
+        if (lane == (uint32_t)(__ffs(mm) - 1) && p < MAX_PARTS) atomicAdd(&s_cnt[p], (uint32_t)__popc(mm));
+    }
+    __syncthreads();
+    if (threadIdx.x < P) cnt[(unsigned long long)threadIdx.x * ntiles + blockIdx.x] = s_cnt[threadIdx.x];
+}
+
+// multi-block exclusive scan of u32 counts into u64 offsets (3 launches)
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_BLOCK = SCAN_THREADS * SCAN_ITEMS;
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const uint32_t* __restrict__ in, unsigned long long len,
+                                                             unsigned long long* __restrict__ block_sum) {
+    const unsigned long long base = (unsigned long long)blockIdx.x * SCAN_BLOCK;
+    unsigned long long t = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const unsigned long long i = base + (unsigned long long)j * SCAN_THREADS + threadIdx.x;
+        if (i < len) t += in[i];
+    }
+    typedef cub::BlockReduce<unsigned long long, SCAN_THREADS> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const unsigned long long tot = BR(tmp).Sum(t);
+    if (threadIdx.x == 0) block_sum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(unsigned long long* block_sum, unsigned long long nblocks,
+                                                          unsigned long long* total) {
+    const unsigned long long per = (nblocks + SCAN_THREADS - 1) / SCAN_THREADS;
+    const unsigned long long a = threadIdx.x * per, b = min(a + per, nblocks);
+    unsigned long long sum = 0;
+    for (unsigned long long t = a; t < b; ++t) sum += block_sum[t];
+    typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BS;
+    __shared__ typename BS::TempStorage tmp;
+    unsigned long long pre, tot;
+    BS(tmp).ExclusiveSum(sum, pre, tot);
+    for (unsigned long long t = a; t < b; ++t) {
+        const unsigned long long c = block_sum[t];
+        block_sum[t] = pre;
+        pre += c;
+    }
+    if (threadIdx.x == 0 && total) *total = tot;
+}
+
+// out[i] = exclusive prefix; also off_part[i / stride_part] for i % stride_part == 0
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const uint32_t* __restrict__ in, unsigned long long len,
+                                                           const unsigned long long* __restrict__ block_pre,
+                                                           unsigned long long* __restrict__ out,
+                                                           unsigned long long stride_part,
+                                                           unsigned long long* __restrict__ off_part) {
+    const unsigned long long base = (unsigned long long)blockIdx.x * SCAN_BLOCK;
+    // blocked arrangement: thread t owns SCAN_ITEMS consecutive entries
+    uint32_t v[SCAN_ITEMS];
+    unsigned long long t = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const unsigned long long i = base + (unsigned long long)threadIdx.x * SCAN_ITEMS + j;
+        v[j] = i < len ? in[i] : 0u;
+        t += v[j];
+    }
+    typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BS;
+    __shared__ typename BS::TempStorage tmp;
+    unsigned long long pre;
+    BS(tmp).ExclusiveSum(t, pre);
+    pre += block_pre[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const unsigned long long i = base + (unsigned long long)threadIdx.x * SCAN_ITEMS + j;
+        if (i < len) {
+            out[i] = pre;
+            if (off_part && i % stride_part == 0) off_part[i / stride_part] = pre;
+        }
+        pre += v[j];
+    }
+}
+
+// Place every valid edge of the tile at off[p][tile] + its rank among the
+// tile's partition-p edges in index order (stable).  Edges are read
+// coalesced (e = tile + j*256 + t, which is index order for (j, t)); each
+// step is a block multisplit: warp match -> per-warp counts -> per-bin
+// offsets across the 8 warps.
+template <class E>
+__global__ void __launch_bounds__(PART_THREADS) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
+                                                                  uint32_t shift, int P, unsigned long long ntiles,
+                                                                  const unsigned long long* __restrict__ off,
+                                                                  uint2* __restrict__ out) {
+    constexpr int W = PART_THREADS / 32;
+    __shared__ uint32_t s_w[W][MAX_PARTS + 1];
+    __shared__ uint32_t s_tot[MAX_PARTS + 1];
+    __shared__ unsigned long long s_base[MAX_PARTS + 1];
+    const uint32_t lane = lane_id();
+    const int w = threadIdx.x >> 5;
+    if (threadIdx.x < P) s_base[threadIdx.x] = off[(unsigned long long)threadIdx.x * ntiles + blockIdx.x];
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * PART_TILE + threadIdx.x;
+    for (int j = 0; j < PART_ITEMS; ++j) {
+        uint2 uv;
+        int b = part_of(edges, e0 + (unsigned long long)j * PART_THREADS, m, n, shift, nullptr, false, uv);
+        if (b < 0) b = MAX_PARTS;
+        if (lane <= MAX_PARTS) s_w[w][lane] = 0;
+        __syncwarp();
+        const unsigned mm = __match_any_sync(0xffffffffu, b);
+        const uint32_t wrank = __popc(mm & ((1u << lane) - 1u));
+        if (wrank == 0) s_w[w][b] = __popc(mm);
+        __syncthreads();
+        if (threadIdx.x < P) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const uint32_t c = s_w[k][threadIdx.x];
+                s_w[k][threadIdx.x] = acc;
+                acc += c;
+            }
+            s_tot[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        if (b < P) out[s_base[b] + s_w[w][b] + wrank] = uv;
+        __syncthreads();
+        if (threadIdx.x < P) s_base[threadIdx.x] += s_tot[threadIdx.x];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 static uint32_t hook_grid(unsigned long long m) { return grid_for(m, HOOK_THREADS, 2, kSMs * 8); }
@@ -211,19 +405,20 @@ static uint32_t vtx_grid(unsigned long long n) { return grid_for(n, COMP_THREADS
 
 template <class E>
 static int launch_hook(E view, unsigned long long m, unsigned long long row0, unsigned long long n, uint32_t* D,
-                       int variant, bool validate, unsigned long long* flags, cudaStream_t s) {
+                       int variant, bool validate, unsigned long long* flags, cudaStream_t s,
+                       const unsigned long long* rng = nullptr) {
     if (m == 0) return SG_OK;
     const uint32_t g = hook_grid(m);
     if (variant == SG_CC_UF) {
         if (validate)
-            k_cc_hook_uf<E, true><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags);
+            k_cc_hook_uf<E, true><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags, rng);
         else
-            k_cc_hook_uf<E, false><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags);
+            k_cc_hook_uf<E, false><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags, rng);
     } else {
         if (validate)
-            k_cc_hook_sv<E, true><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags);
+            k_cc_hook_sv<E, true><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags, rng);
         else
-            k_cc_hook_sv<E, false><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags);
+            k_cc_hook_sv<E, false><<<g, HOOK_THREADS, 0, s>>>(view, m, row0, n, D, flags, rng);
     }
     SG_LAUNCH_CHECK();
     return SG_OK;
@@ -238,6 +433,78 @@ static int hook_dispatch(const void* edges, int dt, unsigned long long m, unsign
         case SG_I64: return launch_hook(EdgesI64{(const longlong2*)edges}, m, row0, n, D, variant, validate, flags, s);
         default: return SG_ERR_VALUE;
     }
+}
+
+struct CcPlan {
+    int parts = 1;
+    uint32_t shift = 31;
+    unsigned long long ntiles = 0;
+};
+
+static CcPlan plan_cc(unsigned long long n, unsigned long long m) {
+    CcPlan p;
+    const char* e = getenv("SG_CC_WBITS");
+    uint32_t wbits = e && *e ? (uint32_t)atoi(e) : 23u;  // window of 2^23 vertices = 32 MiB of D
+    if (wbits < 10) wbits = 10;
+    if (wbits > 31) wbits = 31;
+    unsigned long long parts = (n + (1ull << wbits) - 1) >> wbits;
+    while (parts > MAX_PARTS) {
+        ++wbits;
+        parts = (n + (1ull << wbits) - 1) >> wbits;
+    }
+    if (parts <= 1 || m < (1ull << 16)) return p;
+    p.parts = (int)parts;
+    p.shift = wbits;
+    p.ntiles = (m + PART_TILE - 1) / PART_TILE;
+    return p;
+}
+
+struct CcPartBufs {
+    unsigned long long* bsum = nullptr;
+    uint32_t* cnt = nullptr;
+    unsigned long long* off = nullptr;
+    unsigned long long* off_part = nullptr;
+    uint2* edges = nullptr;
+};
+
+template <class E>
+static int partition_edges(E view, unsigned long long m, unsigned long long n, const CcPlan& p, CcPartBufs& b,
+                           unsigned long long* flags, cudaStream_t s) {
+    const uint32_t nt = (uint32_t)p.ntiles;
+    k_cc_part_count<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, p.ntiles, b.cnt, flags);
+    SG_LAUNCH_CHECK();
+    const unsigned long long len = (unsigned long long)p.parts * p.ntiles;
+    const unsigned long long nb = (len + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    k_scan_reduce<<<(uint32_t)nb, SCAN_THREADS, 0, s>>>(b.cnt, len, b.bsum);
+    SG_LAUNCH_CHECK();
+    k_scan_top<<<1, SCAN_THREADS, 0, s>>>(b.bsum, nb, b.off_part + p.parts);
+    SG_LAUNCH_CHECK();
+    k_scan_down<<<(uint32_t)nb, SCAN_THREADS, 0, s>>>(b.cnt, len, b.bsum, b.off, p.ntiles, b.off_part);
+    SG_LAUNCH_CHECK();
+    k_cc_part_scatter<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, p.ntiles, b.off, b.edges);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+static int partition_dispatch(const void* edges, int dt, unsigned long long m, unsigned long long n, const CcPlan& p,
+                              CcPartBufs& b, unsigned long long* flags, cudaStream_t s) {
+    switch (dt) {
+        case SG_U32: return partition_edges(EdgesU32{(const uint2*)edges}, m, n, p, b, flags, s);
+        case SG_I32: return partition_edges(EdgesI32{(const int2*)edges}, m, n, p, b, flags, s);
+        case SG_I64: return partition_edges(EdgesI64{(const longlong2*)edges}, m, n, p, b, flags, s);
+        default: return SG_ERR_VALUE;
+    }
+}
+
+// one hook sweep over a partitioned edge list, window by window
+static int hook_partitions(const CcPlan& p, const CcPartBufs& b, unsigned long long m, unsigned long long n,
+                           uint32_t* D, int variant, unsigned long long* flags, cudaStream_t s) {
+    const unsigned long long per = m / p.parts + 1;
+    for (int k = 0; k < p.parts; ++k) {
+        int rc = launch_hook(EdgesU32{b.edges}, per, 0, n, D, variant, false, flags, s, b.off_part + k);
+        if (rc != SG_OK) return rc;
+    }
+    return SG_OK;
 }
 
 static int compress_dispatch(uint32_t* D, unsigned long long lo, unsigned long long hi, unsigned long long* roots,
@@ -292,11 +559,27 @@ using namespace sg;
 
 extern "C" {
 
+static bool carve_cc(Carver& c, uint64_t n, uint64_t m, const CcPlan& p, unsigned long long*& flags, uint32_t*& Dws,
+                     CcPartBufs& b) {
+    flags = c.take<unsigned long long>(8);  // [0..3] flags, [4] roots
+    Dws = c.take<uint32_t>(n);
+    if (p.parts > 1) {
+        b.cnt = c.take<uint32_t>((size_t)p.parts * p.ntiles);
+        b.off = c.take<unsigned long long>((size_t)p.parts * p.ntiles);
+        b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+        b.bsum = c.take<unsigned long long>((size_t)p.parts * p.ntiles / SCAN_BLOCK + 2);
+        b.edges = c.take<uint2>(m);
+    }
+    return c.ok;
+}
+
 size_t sg_cc_workspace_bytes(uint64_t n, uint64_t m) {
-    (void)m;
+    const CcPlan p = plan_cc(n, m);
     Carver c(nullptr, 0);
-    c.take<unsigned long long>(8);
-    c.take<uint32_t>(n);
+    unsigned long long* f;
+    uint32_t* d;
+    CcPartBufs b;
+    carve_cc(c, n, m, p, f, d, b);
     return c.off + 256;
 }
 
@@ -314,10 +597,12 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
         viol->index = -1;
         viol->pad = 0;
     }
+    const CcPlan plan = plan_cc(n, m);
     Carver c(ws, ws_bytes);
-    unsigned long long* flags = c.take<unsigned long long>(8);  // [0..3] flags, [4] roots
-    uint32_t* Dws = c.take<uint32_t>(n);
-    if (!c.ok) return SG_ERR_WORKSPACE;
+    unsigned long long* flags;
+    uint32_t* Dws;
+    CcPartBufs pb;
+    if (!carve_cc(c, n, m, plan, flags, Dws, pb)) return SG_ERR_WORKSPACE;
     // u32/i32 labels: run in place in the output buffer
     uint32_t* D = (label_dtype == SG_I64) ? Dws : (uint32_t*)labels;
     unsigned long long* roots = flags + 4;
@@ -335,9 +620,18 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
         st->vertex_sweeps = 1;
     }
     int rc;
+    const bool parted = plan.parts > 1;
+    if (parted) {
+        rec.begin(K_CC_PARTITION, 0, (uint32_t)plan.ntiles, PART_THREADS, m);
+        rc = partition_dispatch(edges, edge_dtype, m, n, plan, pb, flags, s);
+        rec.end();
+        if (rc != SG_OK) return rc;
+        if (st) st->edge_sweeps = 0;
+    }
     if (variant == SG_CC_UF) {
         rec.begin(K_CC_HOOK_UF, 1, hook_grid(m), HOOK_THREADS, m);
-        rc = hook_dispatch(edges, edge_dtype, m, 0, n, D, SG_CC_UF, true, flags, s);
+        rc = parted ? hook_partitions(plan, pb, m, n, D, SG_CC_UF, flags, s)
+                    : hook_dispatch(edges, edge_dtype, m, 0, n, D, SG_CC_UF, true, flags, s);
         rec.end();
         if (rc != SG_OK) return rc;
         rec.begin(K_CC_COMPRESS, 1, gv, COMP_THREADS, n);
@@ -367,7 +661,8 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
         SG_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned long long), s));
         SG_CUDA(cudaMemsetAsync(roots, 0, sizeof(unsigned long long), s));
         rec.begin(K_CC_HOOK_SV, r, hook_grid(m), HOOK_THREADS, m);
-        rc = hook_dispatch(edges, edge_dtype, m, 0, n, D, SG_CC_SV, r == 1, flags, s);
+        rc = parted ? hook_partitions(plan, pb, m, n, D, SG_CC_SV, flags, s)
+                    : hook_dispatch(edges, edge_dtype, m, 0, n, D, SG_CC_SV, r == 1, flags, s);
         rec.end();
         if (rc != SG_OK) return rc;
         rec.begin(K_CC_COMPRESS, r, gv, COMP_THREADS, n);
@@ -377,7 +672,7 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
         CcHostFlags h;
         rc = read_flags(flags, h, s);
         if (rc != SG_OK) return rc;
-        if (r == 1) {
+        if (r == 1 || parted) {
             rc = graph_violation(h, viol);
             if (rc != SG_OK) return rc;
         }

@@ -48,6 +48,7 @@ enum KernelId : int {
     K_LIST_FROM_ORDER,
     K_EDGE_KEYS,
     K_EDGES_FROM_KEYS,
+    K_CC_PARTITION,   // cc_partition stable split of the edges by endpoint window
     K_COUNT_
 };
 
@@ -60,7 +61,7 @@ struct ListStatus {
     unsigned long long head_sum;    // final inclusive suffix sum at the head
     unsigned long long head_ok;     // 1: the head's pointer reached the tail
     unsigned long long bad;         // walk saw an out-of-range successor
-    unsigned long long pad;
+    unsigned long long local;       // successors within 16 slots of their node (layout locality)
     unsigned long long R[SG_MAX_LEVELS + 1];      // nodes per level (R[0] = n)
     unsigned long long qhead[SG_MAX_LEVELS + 1];  // walk work-queue heads
 };

@@ -106,7 +106,7 @@ __global__ void k_status_init(ListStatus* st, unsigned long long n) {
         st->head_sum = 0;
         st->head_ok = 0;
         st->bad = 0;
-        st->pad = 0;
+        st->local = 0;
     }
     if (threadIdx.x <= SG_MAX_LEVELS) {
         st->R[threadIdx.x] = threadIdx.x == 0 ? n : 0;
@@ -270,6 +270,53 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count(const SuccT* __restri
     }
 }
 
+// level 0: validate the successors, copy them into the packed walk array
+// A[i] = succ[i] (low 32 bits; out-of-range -> 0xFFFFFFFF) and count rulers
+template <class SuccT>
+__global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restrict__ succ,
+                                                            unsigned long long* __restrict__ A,
+                                                            uint32_t* __restrict__ tile_cnt, ListStatus* st,
+                                                            uint32_t kbits, uint32_t salt) {
+    const unsigned long long N = st->R[0];
+    const unsigned long long base = (unsigned long long)blockIdx.x * TILE;
+    if (base >= N) {
+        if (threadIdx.x == 0) tile_cnt[blockIdx.x] = 0;
+        return;
+    }
+    SuccT v[TILE_ITEMS];
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; ++j) {
+        const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+        v[j] = i < N ? __ldcs(succ + i) : SuccT(0);
+    }
+    uint32_t cnt = 0, loc = 0;
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; ++j) {
+        const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+        if (i < N) {
+            const unsigned long long x = as_index<SuccT>(v[j]);
+            if (x >= N || x == i) note_succ(st, i, x, N);
+            A[i] = x < N ? x : 0xFFFFFFFFull;
+            cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
+            loc += (x + 16 > i && x < i + 16) ? 1u : 0u;
+        }
+    }
+    typedef cub::BlockReduce<uint32_t, TILE_THREADS> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const uint32_t tot = BR(tmp).Sum(cnt);
+    __syncthreads();
+    const uint32_t ltot = BR(tmp).Sum(loc);
+    if (threadIdx.x == 0) {
+        tile_cnt[blockIdx.x] = tot;
+        if (ltot) atomicAdd(&st->local, (unsigned long long)ltot);
+    }
+}
+
+// Lists laid out mostly in chain order (successor within 16 slots) walk
+// faster reading the input and writing the words separately: each lane
+// streams its own lines through L1.  Scattered lists use the in-place walk.
+__device__ __forceinline__ bool layout_local(const ListStatus* st) { return st->local * 2 > st->R[0]; }
+
 // single CTA exclusive scan of the tile counts of `level`
 __global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* tile_cnt, ListStatus* st, int level,
                                                   unsigned long long cap) {
@@ -299,6 +346,8 @@ __global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* tile_cnt, ListStatus
 }
 
 // install ruler ids in index order: spl[id] = node, word[node] = id << 32
+// (level 0: the packed array keeps the successor in the low half)
+template <bool kPacked>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __restrict__ tile_off,
                                                             uint32_t* __restrict__ spl,
                                                             unsigned long long* __restrict__ word,
@@ -327,7 +376,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
         if (flags & (1u << j)) {
             if (id < cap) {
                 spl[id] = (uint32_t)(i0 + j);
-                word[i0 + j] = id << 32;
+                word[i0 + j] = kPacked ? ((id << 32) | (word[i0 + j] & 0xFFFFFFFFull)) : (id << 32);
             }
             ++id;
         }
@@ -344,7 +393,9 @@ template <class View>
 __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned long long* __restrict__ word,
                                                           const uint32_t* __restrict__ spl,
                                                           uint2* __restrict__ up, ListStatus* st, int level,
-                                                          uint32_t kbits, uint32_t salt, uint32_t cap_hops) {
+                                                          uint32_t kbits, uint32_t salt, uint32_t cap_hops,
+                                                          bool only_local) {
+    if (only_local && !layout_local(st)) return;  // k_rs_walk0 takes this list
     const unsigned long long N = st->R[level];
     const unsigned long long R = st->R[level + 1];
     unsigned long long* q = &st->qhead[level];
@@ -395,6 +446,72 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
             sid = NIL;
         } else {
             cur = (uint32_t)nx;
+        }
+    }
+}
+
+// Level-0 walk, in place over the packed array: A[cur] holds succ[cur] in
+// its low half until the walk reads it, then becomes {owner, local}.  The
+// store goes to the sector the load just brought into L2, so a hop costs one
+// random DRAM read and one full-sector write-back (a separate word array
+// would add a fill read for every partial 8-byte store).  A ruler keeps its
+// id in the high half from rs2_select on, so a walk that reaches it reads
+// the id without caring whether the ruler's own walk has started.
+__global__ void __launch_bounds__(WALK_THREADS) k_rs_walk0(unsigned long long* __restrict__ A,
+                                                           const uint32_t* __restrict__ spl,
+                                                           uint2* __restrict__ up, ListStatus* st,
+                                                           uint32_t kbits, uint32_t salt, uint32_t cap_hops) {
+    if (layout_local(st)) return;  // k_rs_walk<Level0> takes this list
+    const unsigned long long N = st->R[0];
+    const unsigned long long R = st->R[1];
+    unsigned long long* q = &st->qhead[0];
+    const uint32_t lane = lane_id();
+    uint32_t sid = NIL, cur = 0, prev = 0, pre = 0;
+    bool done = false;
+    for (;;) {
+        const bool need = !done && sid == NIL;
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if ((int)lane == leader) base = atomicAdd(q, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (need) {
+                const unsigned long long s = base + __popc(m & ((1u << lane) - 1u));
+                if (s < R) {
+                    sid = (uint32_t)s;
+                    cur = spl[s];
+                    pre = 0;
+                } else {
+                    done = true;
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        if (done) continue;
+        const uint32_t nx = (uint32_t)A[cur];
+        // the previous node's word: its load completed last hop, its sector is
+        // in L2, and no load to that address is in flight
+        if (pre > 0) A[prev] = ((unsigned long long)sid << 32) | (pre - 1);
+        prev = cur;
+        ++pre;
+        bool end = true;
+        uint2 upv = make_uint2(sid, pre);
+        if (nx == cur) {  // the tail
+        } else if (nx >= N) {  // out-of-range successor (invalid input)
+            st->bad = 1;
+        } else if (is_ruler(nx, kbits, salt)) {
+            upv.x = (uint32_t)(__ldcg(A + nx) >> 32);
+        } else if (pre >= cap_hops) {
+            st->overflow = 1;
+        } else {
+            end = false;
+            cur = nx;
+        }
+        if (end) {  // nx is known, so cur's load has completed
+            A[cur] = ((unsigned long long)sid << 32) | (pre - 1);
+            up[sid] = upv;
+            sid = NIL;
         }
     }
 }
@@ -667,7 +784,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
         if (k == 0) {
             rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, capN);
-            k_rs_count<SuccT, true><<<nt, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, 0, p.kbits[0], p.salt[0], 1);
+            k_rs_count0<SuccT><<<nt, TILE_THREADS, 0, s>>>(succ, b.word0, b.tiles, b.st, p.kbits[0], p.salt[0]);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
             k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, b.tiles, b.st, k, p.kbits[k], p.salt[k], 1);
@@ -679,17 +796,24 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
         rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
-        k_rs_select<<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR);
+        if (k == 0)
+            k_rs_select<true><<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR);
+        else
+            k_rs_select<false><<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR);
         rec.end();
         SG_LAUNCH_CHECK();
         if (k == 0) {
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
-            k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, wk, b.spl[0], b.lvl[1],
-                                                                        b.st, 0, p.kbits[0], p.salt[0], p.walk_cap);
+            k_rs_walk0<<<walk_grid, WALK_THREADS, 0, s>>>(b.word0, b.spl[0], b.lvl[1], b.st, p.kbits[0], p.salt[0],
+                                                           p.walk_cap);
+            SG_LAUNCH_CHECK();
+            k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.word0,
+                                                                        b.spl[0], b.lvl[1], b.st, 0, p.kbits[0],
+                                                                        p.salt[0], p.walk_cap, true);
         } else {
             rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
             k_rs_walk<LevelK><<<walk_grid, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
-                                                                 k, p.kbits[k], p.salt[k], p.walk_cap);
+                                                                 k, p.kbits[k], p.salt[k], p.walk_cap, false);
         }
         rec.end();
         SG_LAUNCH_CHECK();

@@ -200,3 +200,23 @@ def test_building_blocks_c_abi(cuda, orc):
     assert np.array_equal(out.cpu().numpy(), want)
     assert int(roots.item()) == len(np.unique(want))
     assert int(flags[0].item()) == 1 and int(flags[1].item()) == 0 and int(flags[2].item()) == 0
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_partitioned_path_small_windows(cuda, orc, monkeypatch, variant):
+    """Force the windowed (partitioned-edge) hook on small graphs: windows of
+    2^12 vertices -> up to 16 partitions."""
+    monkeypatch.setenv("SG_CC_WBITS", "12")
+    cases = [g.gen_random_graph(60_000, 5e-5, seed=4), g.gen_tree_graph(70_000, 3, seed=2),
+             g.list_to_graph(g.gen_list(66_000, seed=1)), g.gen_random_graph(30_000, 2e-4, seed=9)]
+    for gr in cases:
+        labels, stats = g.sv_components(gr, p=64, variant=variant)
+        assert np.array_equal(labels, orc.seq_components(gr.n, gr.edges)), (gr.n, gr.m)
+        assert any(r.kernel == "cc_partition" for r in stats.launch_log)
+    e = g.gen_random_graph(60_000, 5e-5, seed=4).edges.copy()
+    e[40_000] = [7, 7]
+    e[80_000] = [3, 60_000]
+    with pytest.raises(g.InvalidGraphError, match="self-loop at edge 40000"):
+        g.sv_components(g.EdgeGraph(60_000, e[:70_000]), p=8, variant=variant)
+    with pytest.raises(g.InvalidGraphError, match="out of range at row 80000"):
+        g.sv_components(g.EdgeGraph(60_000, e), p=8, variant=variant)
