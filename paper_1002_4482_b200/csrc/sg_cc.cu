@@ -29,6 +29,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "sg_internal.cuh"
+#include "sg_scan.cuh"
 
 namespace sg {
 
@@ -280,76 +281,6 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
     }
     __syncthreads();
     if (threadIdx.x < P) cnt[(unsigned long long)threadIdx.x * ntiles + blockIdx.x] = s_cnt[threadIdx.x];
-}
-
-// multi-block exclusive scan of u32 counts into u64 offsets (3 launches)
-constexpr int SCAN_THREADS = 1024;
-constexpr int SCAN_ITEMS = 4;
-constexpr int SCAN_BLOCK = SCAN_THREADS * SCAN_ITEMS;
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const uint32_t* __restrict__ in, unsigned long long len,
-                                                             unsigned long long* __restrict__ block_sum) {
-    const unsigned long long base = (unsigned long long)blockIdx.x * SCAN_BLOCK;
-    unsigned long long t = 0;
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-        const unsigned long long i = base + (unsigned long long)j * SCAN_THREADS + threadIdx.x;
-        if (i < len) t += in[i];
-    }
-    typedef cub::BlockReduce<unsigned long long, SCAN_THREADS> BR;
-    __shared__ typename BR::TempStorage tmp;
-    const unsigned long long tot = BR(tmp).Sum(t);
-    if (threadIdx.x == 0) block_sum[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_top(unsigned long long* block_sum, unsigned long long nblocks,
-                                                          unsigned long long* total) {
-    const unsigned long long per = (nblocks + SCAN_THREADS - 1) / SCAN_THREADS;
-    const unsigned long long a = threadIdx.x * per, b = min(a + per, nblocks);
-    unsigned long long sum = 0;
-    for (unsigned long long t = a; t < b; ++t) sum += block_sum[t];
-    typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BS;
-    __shared__ typename BS::TempStorage tmp;
-    unsigned long long pre, tot;
-    BS(tmp).ExclusiveSum(sum, pre, tot);
-    for (unsigned long long t = a; t < b; ++t) {
-        const unsigned long long c = block_sum[t];
-        block_sum[t] = pre;
-        pre += c;
-    }
-    if (threadIdx.x == 0 && total) *total = tot;
-}
-
-// out[i] = exclusive prefix; also off_part[i / stride_part] for i % stride_part == 0
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const uint32_t* __restrict__ in, unsigned long long len,
-                                                           const unsigned long long* __restrict__ block_pre,
-                                                           unsigned long long* __restrict__ out,
-                                                           unsigned long long stride_part,
-                                                           unsigned long long* __restrict__ off_part) {
-    const unsigned long long base = (unsigned long long)blockIdx.x * SCAN_BLOCK;
-    // blocked arrangement: thread t owns SCAN_ITEMS consecutive entries
-    uint32_t v[SCAN_ITEMS];
-    unsigned long long t = 0;
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-        const unsigned long long i = base + (unsigned long long)threadIdx.x * SCAN_ITEMS + j;
-        v[j] = i < len ? in[i] : 0u;
-        t += v[j];
-    }
-    typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BS;
-    __shared__ typename BS::TempStorage tmp;
-    unsigned long long pre;
-    BS(tmp).ExclusiveSum(t, pre);
-    pre += block_pre[blockIdx.x];
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-        const unsigned long long i = base + (unsigned long long)threadIdx.x * SCAN_ITEMS + j;
-        if (i < len) {
-            out[i] = pre;
-            if (off_part && i % stride_part == 0) off_part[i / stride_part] = pre;
-        }
-        pre += v[j];
-    }
 }
 
 // Place every valid edge of the tile at off[p][tile] + its rank among the

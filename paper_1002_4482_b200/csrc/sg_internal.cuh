@@ -49,6 +49,8 @@ enum KernelId : int {
     K_EDGE_KEYS,
     K_EDGES_FROM_KEYS,
     K_CC_PARTITION,   // cc_partition stable split of the edges by endpoint window
+    K_RS5_PARTITION,  // rs5_partition: rank the walk records, split by output window
+    K_RS5_SCATTER,    // rs5_scatter:   node-order scatter, one L2-resident window at a time
     K_COUNT_
 };
 
@@ -64,6 +66,7 @@ struct ListStatus {
     unsigned long long local;       // successors within 16 slots of their node (layout locality)
     unsigned long long R[SG_MAX_LEVELS + 1];      // nodes per level (R[0] = n)
     unsigned long long qhead[SG_MAX_LEVELS + 1];  // walk work-queue heads
+    unsigned long long chunks;      // record chunks handed out by the level-0 record walk
 };
 
 // Error plumbing -------------------------------------------------------------

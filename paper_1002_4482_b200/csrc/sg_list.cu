@@ -31,6 +31,7 @@
 #include <string.h>
 
 #include "sg_internal.cuh"
+#include "sg_scan.cuh"
 
 namespace sg {
 
@@ -107,6 +108,7 @@ __global__ void k_status_init(ListStatus* st, unsigned long long n) {
         st->head_ok = 0;
         st->bad = 0;
         st->local = 0;
+        st->chunks = 0;
     }
     if (threadIdx.x <= SG_MAX_LEVELS) {
         st->R[threadIdx.x] = threadIdx.x == 0 ? n : 0;
@@ -270,11 +272,10 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count(const SuccT* __restri
     }
 }
 
-// level 0: validate the successors, copy them into the packed walk array
-// A[i] = succ[i] (low 32 bits; out-of-range -> 0xFFFFFFFF) and count rulers
+// level 0: validate the successors (range, self-loops), count rulers per tile
+// and measure layout locality (successor within 16 slots)
 template <class SuccT>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restrict__ succ,
-                                                            unsigned long long* __restrict__ A,
                                                             uint32_t* __restrict__ tile_cnt, ListStatus* st,
                                                             uint32_t kbits, uint32_t salt) {
     const unsigned long long N = st->R[0];
@@ -296,7 +297,6 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
         if (i < N) {
             const unsigned long long x = as_index<SuccT>(v[j]);
             if (x >= N || x == i) note_succ(st, i, x, N);
-            A[i] = x < N ? x : 0xFFFFFFFFull;
             cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
             loc += (x + 16 > i && x < i + 16) ? 1u : 0u;
         }
@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
                                                             uint32_t* __restrict__ spl,
                                                             unsigned long long* __restrict__ word,
                                                             const ListStatus* st, int level, uint32_t kbits,
-                                                            uint32_t salt, unsigned long long cap) {
+                                                            uint32_t salt, unsigned long long cap,
+                                                            uint32_t* __restrict__ rid) {
     const unsigned long long N = st->R[level];
     const unsigned long long base = (unsigned long long)blockIdx.x * TILE;
     if (base >= N) return;
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
             if (id < cap) {
                 spl[id] = (uint32_t)(i0 + j);
                 word[i0 + j] = kPacked ? ((id << 32) | (word[i0 + j] & 0xFFFFFFFFull)) : (id << 32);
+                if (rid != nullptr) rid[i0 + j] = (uint32_t)id;
             }
             ++id;
         }
@@ -450,24 +452,54 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
     }
 }
 
-// Level-0 walk, in place over the packed array: A[cur] holds succ[cur] in
-// its low half until the walk reads it, then becomes {owner, local}.  The
-// store goes to the sector the load just brought into L2, so a hop costs one
-// random DRAM read and one full-sector write-back (a separate word array
-// would add a fill read for every partial 8-byte store).  A ruler keeps its
-// id in the high half from rs2_select on, so a walk that reaches it reads
-// the id without caring whether the ruler's own walk has started.
-__global__ void __launch_bounds__(WALK_THREADS) k_rs_walk0(unsigned long long* __restrict__ A,
-                                                           const uint32_t* __restrict__ spl,
-                                                           uint2* __restrict__ up, ListStatus* st,
-                                                           uint32_t kbits, uint32_t salt, uint32_t cap_hops) {
+// ---------------------------------------------------------------------------
+// Level-0 record walk (scattered layouts).
+//
+// HBM serves ~40 G random 64-B atoms/s on this part (tools/ubench_random.cu)
+// whether they are dependent or not, and a random partial store costs a
+// read-modify-write on top.  So the walk only *reads* at random -- succ[cur],
+// one atom per hop -- and appends {cur, sid, local} records contiguously per
+// warp (all active lanes of a warp emit one record per step, compacted with a
+// ballot), i.e. as full-line streaming writes.  Each warp owns 1024-record
+// chunks and keeps a per-chunk histogram of the records' output windows for
+// the partition pass.  The node-order scatter of the ranks then happens window
+// by window inside L2 (rs5_partition / rs5_scatter).
+
+constexpr int REC_CH = 1024;
+constexpr int REC_MAXP = 64;
+
+template <class SuccT>
+__global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_rec(const SuccT* __restrict__ succ,
+                                                              const uint32_t* __restrict__ rid,
+                                                              const uint32_t* __restrict__ spl,
+                                                              uint2* __restrict__ up, uint32_t* __restrict__ rec_cur,
+                                                              unsigned long long* __restrict__ rec_sl,
+                                                              uint32_t* __restrict__ hist, ListStatus* st,
+                                                              uint32_t kbits, uint32_t salt, uint32_t cap_hops,
+                                                              uint32_t wshift, int P, unsigned long long maxchunks) {
     if (layout_local(st)) return;  // k_rs_walk<Level0> takes this list
+    __shared__ uint32_t s_hist[WALK_THREADS / 32][REC_MAXP];
     const unsigned long long N = st->R[0];
     const unsigned long long R = st->R[1];
     unsigned long long* q = &st->qhead[0];
     const uint32_t lane = lane_id();
-    uint32_t sid = NIL, cur = 0, prev = 0, pre = 0;
+    const int w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = lane; k < REC_MAXP; k += 32) s_hist[w][k] = 0;
+    unsigned long long chunk = ~0ull;  // warp-uniform
+    uint32_t fill = REC_CH;            // warp-uniform: records used in the current chunk
+    uint32_t sid = NIL, cur = 0, pre = 0;
     bool done = false;
+    auto close_chunk = [&]() {  // pad the tail with NIL records, publish the window histogram
+        if (chunk == ~0ull) return;
+        for (uint32_t k = fill + lane; k < REC_CH; k += 32) rec_cur[chunk * REC_CH + k] = NIL;
+        __syncwarp();
+        for (int k = lane; k < P; k += 32) {
+            hist[(unsigned long long)k * maxchunks + chunk] = s_hist[w][k];
+            s_hist[w][k] = 0;
+        }
+        __syncwarp();
+    };
     for (;;) {
         const bool need = !done && sid == NIL;
         const unsigned m = __ballot_sync(0xffffffffu, need);
@@ -477,7 +509,7 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk0(unsigned long long* _
             if ((int)lane == leader) base = atomicAdd(q, (unsigned long long)__popc(m));
             base = __shfl_sync(0xffffffffu, base, leader);
             if (need) {
-                const unsigned long long s = base + __popc(m & ((1u << lane) - 1u));
+                const unsigned long long s = base + __popc(m & lt);
                 if (s < R) {
                     sid = (uint32_t)s;
                     cur = spl[s];
@@ -487,32 +519,126 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk0(unsigned long long* _
                 }
             }
         }
-        if (__all_sync(0xffffffffu, done)) break;
-        if (done) continue;
-        const uint32_t nx = (uint32_t)A[cur];
-        // the previous node's word: its load completed last hop, its sector is
-        // in L2, and no load to that address is in flight
-        if (pre > 0) A[prev] = ((unsigned long long)sid << 32) | (pre - 1);
-        prev = cur;
-        ++pre;
-        bool end = true;
-        uint2 upv = make_uint2(sid, pre);
-        if (nx == cur) {  // the tail
-        } else if (nx >= N) {  // out-of-range successor (invalid input)
-            st->bad = 1;
-        } else if (is_ruler(nx, kbits, salt)) {
-            upv.x = (uint32_t)(__ldcg(A + nx) >> 32);
-        } else if (pre >= cap_hops) {
-            st->overflow = 1;
-        } else {
-            end = false;
-            cur = nx;
+        const unsigned act = __ballot_sync(0xffffffffu, !done);
+        if (act == 0) break;
+        unsigned long long nxl = 0;
+        if (!done) nxl = as_index<SuccT>(succ[cur]);
+        // append this step's records, warp-contiguous
+        const uint32_t cnt = __popc(act);
+        if (fill + cnt > REC_CH) {
+            close_chunk();
+            unsigned long long c = 0;
+            if (lane == 0) c = atomicAdd(&st->chunks, 1ull);
+            chunk = __shfl_sync(0xffffffffu, c, 0);
+            fill = 0;
+            if (chunk >= maxchunks) {  // cannot happen for valid inputs; fall back to Wyllie
+                if (lane == 0) st->overflow = 1;
+                chunk = ~0ull;
+                return;
+            }
         }
-        if (end) {  // nx is known, so cur's load has completed
-            A[cur] = ((unsigned long long)sid << 32) | (pre - 1);
-            up[sid] = upv;
-            sid = NIL;
+        if (!done) {
+            const unsigned long long r = chunk * REC_CH + fill + __popc(act & lt);
+            rec_cur[r] = cur;
+            rec_sl[r] = ((unsigned long long)sid << 32) | pre;
+            const uint32_t win = cur >> wshift;
+            const unsigned same = __match_any_sync(act, win);
+            if ((same & lt) == 0) atomicAdd(&s_hist[w][win], (uint32_t)__popc(same));
         }
+        fill += cnt;
+        if (!done) {
+            ++pre;
+            bool end = true;
+            uint2 upv = make_uint2(sid, pre);
+            if (nxl == cur) {  // the tail
+            } else if (nxl >= N) {  // out-of-range successor (invalid input)
+                st->bad = 1;
+            } else if (is_ruler((uint32_t)nxl, kbits, salt)) {
+                upv.x = __ldg(rid + nxl);
+            } else if (pre >= cap_hops) {
+                st->overflow = 1;
+            } else {
+                end = false;
+                cur = (uint32_t)nxl;
+            }
+            if (end) {
+                up[sid] = upv;
+                sid = NIL;
+            }
+        }
+    }
+    close_chunk();
+}
+
+// rank of every record (rank = IS_1[sid] - local - 1, listrank.py:375-379)
+// partitioned stably by output window: pairs[...] = {cur, rank}.  One block
+// per record chunk; block multisplit as in the edge partition.
+__global__ void __launch_bounds__(256) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
+                                                          const unsigned long long* __restrict__ rec_sl,
+                                                          const uint32_t* __restrict__ IS1,
+                                                          const unsigned long long* __restrict__ off,
+                                                          unsigned long long* __restrict__ pairs,
+                                                          const ListStatus* st, uint32_t wshift, int P,
+                                                          unsigned long long maxchunks) {
+    if (layout_local(st) || st->overflow) return;
+    const unsigned long long chunk = blockIdx.x;
+    if (chunk >= st->chunks) return;
+    constexpr int W = 256 / 32;
+    __shared__ uint32_t s_w[W][REC_MAXP + 1];
+    __shared__ uint32_t s_tot[REC_MAXP + 1];
+    __shared__ unsigned long long s_base[REC_MAXP + 1];
+    const unsigned long long R1 = st->R[1];
+    const uint32_t lane = lane_id();
+    const int w = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < P; k += 256) s_base[k] = off[(unsigned long long)k * maxchunks + chunk];
+    for (int j = 0; j < REC_CH / 256; ++j) {
+        const unsigned long long r = chunk * REC_CH + (unsigned long long)j * 256 + threadIdx.x;
+        const uint32_t c = rec_cur[r];
+        int b = REC_MAXP;
+        unsigned long long pr = 0;
+        if (c != NIL) {
+            const unsigned long long sl = rec_sl[r];
+            const unsigned long long o = sl >> 32;
+            const uint32_t rk = o < R1 ? __ldg(IS1 + o) - (uint32_t)sl - 1u : 0u;
+            pr = ((unsigned long long)c << 32) | rk;
+            b = (int)(c >> wshift);
+        }
+        for (int k = lane; k <= REC_MAXP; k += 32) s_w[w][k] = 0;
+        __syncwarp();
+        const unsigned mm = __match_any_sync(0xffffffffu, b);
+        const uint32_t wrank = __popc(mm & ((1u << lane) - 1u));
+        if (wrank == 0) s_w[w][b] = __popc(mm);
+        __syncthreads();
+        for (int k = threadIdx.x; k < P; k += 256) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int x = 0; x < W; ++x) {
+                const uint32_t v = s_w[x][k];
+                s_w[x][k] = acc;
+                acc += v;
+            }
+            s_tot[k] = acc;
+        }
+        __syncthreads();
+        if (b < P) pairs[s_base[b] + s_w[w][b] + wrank] = pr;
+        __syncthreads();
+        for (int k = threadIdx.x; k < P; k += 256) s_base[k] += s_tot[k];
+    }
+}
+
+// node-order scatter of the window-partitioned {cur, rank} pairs: the pairs
+// are window-major, so the grid-stride sweep keeps ~one 32 MiB output window
+// live in L2 and the ranks reach HBM as full lines
+template <class OutT>
+__global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
+                                                        const unsigned long long* __restrict__ off_part, int P,
+                                                        OutT* __restrict__ rank, const ListStatus* st) {
+    if (layout_local(st) || st->overflow) return;
+    const unsigned long long total = off_part[P];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const unsigned long long pr = __ldcs(pairs + i);
+        rank[pr >> 32] = (OutT)(uint32_t)pr;
     }
 }
 
@@ -587,7 +713,7 @@ template <class OutT>
 __global__ void __launch_bounds__(256) k_rs_expand0(const unsigned long long* __restrict__ word,
                                                     const uint32_t* __restrict__ IS1, OutT* __restrict__ rank,
                                                     unsigned long long n, const ListStatus* st) {
-    if (st->overflow) return;  // host re-ranks with Wyllie; keep succ intact if aliased
+    if (st->overflow || !layout_local(st)) return;  // overflow: Wyllie re-ranks; scattered: record path
     const unsigned long long R1 = st->R[1];
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long npair = n >> 1;
@@ -623,6 +749,10 @@ struct RsPlan {
     int levels = 0;                              // walked levels (final level = levels)
     uint32_t walk_cap = WALK_CAP_HOPS;
     int load_mode = 0;
+    uint32_t wshift = 23;                        // record path: output window = 2^wshift nodes
+    int parts = 1;                               // number of output windows
+    uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
+    unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
     unsigned long long cap[SG_MAX_LEVELS + 1] = {};  // node capacity per level
@@ -646,8 +776,21 @@ static uint32_t mix32(uint64_t x) {
     return (uint32_t)x;
 }
 
-static RsPlan plan_rs(uint64_t n, uint64_t seed) {
+static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     RsPlan p;
+    // 32 MiB of output per window; at most REC_MAXP windows
+    uint32_t ws = out_bytes >= 8 ? 22 : 23;
+    while (((n + (1ull << ws) - 1) >> ws) > (unsigned long long)REC_MAXP) ++ws;
+    p.wshift = ws;
+    p.parts = (int)((n + (1ull << ws) - 1) >> ws);
+    if (p.parts < 1) p.parts = 1;
+    // one lane per ruler is plenty; every warp that walks may leave one partial chunk
+    unsigned long long wg = ((n >> 5) + 2 * WALK_THREADS - 1) / (2 * WALK_THREADS);
+    if (wg < (unsigned long long)kSMs) wg = kSMs;
+    if (wg > (unsigned long long)kSMs * (2048 / WALK_THREADS)) wg = kSMs * (2048 / WALK_THREADS);
+    p.walk_grid = (uint32_t)wg;
+    const unsigned long long warps = wg * (WALK_THREADS / 32);
+    p.maxchunks = n / (REC_CH - 32) + warps + 2;
     const uint32_t kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);
     const uint32_t kb1 = env_u32("SG_RS_KBITS", 5, 1, 16);
     const uint32_t fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
@@ -672,6 +815,14 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed) {
 struct RsBufs {
     ListStatus* st = nullptr;
     unsigned long long* word0 = nullptr;
+    uint32_t* rid = nullptr;
+    uint32_t* rec_cur = nullptr;
+    unsigned long long* rec_sl = nullptr;
+    unsigned long long* pairs = nullptr;
+    uint32_t* hist = nullptr;
+    unsigned long long* hoff = nullptr;
+    unsigned long long* bsum = nullptr;
+    unsigned long long* off_part = nullptr;
     uint32_t* tiles = nullptr;
     uint32_t* spl[SG_MAX_LEVELS] = {};
     uint2* lvl[SG_MAX_LEVELS + 1] = {};
@@ -684,6 +835,18 @@ struct RsBufs {
 static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     b.st = c.take<ListStatus>(1);
     b.word0 = c.take<unsigned long long>(n);
+    if (p.levels > 0) {
+        const unsigned long long nrec = p.maxchunks * REC_CH;
+        const unsigned long long nh = (unsigned long long)p.parts * p.maxchunks;
+        b.rid = c.take<uint32_t>(n);
+        b.rec_cur = c.take<uint32_t>(nrec);
+        b.rec_sl = c.take<unsigned long long>(nrec);
+        b.pairs = c.take<unsigned long long>(nrec);
+        b.hist = c.take<uint32_t>(nh);
+        b.hoff = c.take<unsigned long long>(nh);
+        b.bsum = c.take<unsigned long long>(nh / SCAN_BLOCK + 2);
+        b.off_part = c.take<unsigned long long>(REC_MAXP + 2);
+    }
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     b.tiles = c.take<uint32_t>(ntiles + 1);
     for (int k = 0; k < p.levels; ++k) {
@@ -758,7 +921,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     k_status_init<<<1, 32, 0, s>>>(b.st, n);
     rec.end();
     SG_LAUNCH_CHECK();
-    const uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
+    const uint32_t walk_grid = p.walk_grid;
     if (p.levels == 0) {
         const uint32_t nt = (uint32_t)((n + TILE - 1) / TILE);
         rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, n);
@@ -784,7 +947,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
         if (k == 0) {
             rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, capN);
-            k_rs_count0<SuccT><<<nt, TILE_THREADS, 0, s>>>(succ, b.word0, b.tiles, b.st, p.kbits[0], p.salt[0]);
+            k_rs_count0<SuccT><<<nt, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, p.kbits[0], p.salt[0]);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
             k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, b.tiles, b.st, k, p.kbits[k], p.salt[k], 1);
@@ -796,16 +959,16 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
         rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
-        if (k == 0)
-            k_rs_select<true><<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR);
-        else
-            k_rs_select<false><<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR);
+        k_rs_select<false><<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
+                                                        k == 0 ? b.rid : nullptr);
         rec.end();
         SG_LAUNCH_CHECK();
         if (k == 0) {
+            SG_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * (size_t)p.parts * p.maxchunks, s));
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
-            k_rs_walk0<<<walk_grid, WALK_THREADS, 0, s>>>(b.word0, b.spl[0], b.lvl[1], b.st, p.kbits[0], p.salt[0],
-                                                           p.walk_cap);
+            k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rid, b.spl[0], b.lvl[1], b.rec_cur,
+                                                                    b.rec_sl, b.hist, b.st, p.kbits[0], p.salt[0],
+                                                                    p.walk_cap, p.wshift, p.parts, p.maxchunks);
             SG_LAUNCH_CHECK();
             k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.word0,
                                                                         b.spl[0], b.lvl[1], b.st, 0, p.kbits[0],
@@ -834,7 +997,20 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     const uint32_t g = grid_for(n / 2 + 1, 256, 1, kSMs * 8);
     rec.begin(K_RS5_EXPAND, 0, g, 256, n);
-    k_rs_expand0<OutT><<<g, 256, 0, s>>>(b.word0, b.IS[1], rank, n, b.st);
+    k_rs_expand0<OutT><<<g, 256, 0, s>>>(b.word0, b.IS[1], rank, n, b.st);  // local layouts
+    rec.end();
+    SG_LAUNCH_CHECK();
+    // scattered layouts: rank the records, partition them by output window, scatter
+    const unsigned long long nh = (unsigned long long)p.parts * p.maxchunks;
+    rec.begin(K_RS5_PARTITION, 0, (uint32_t)p.maxchunks, 256, n);
+    launch_scan(b.hist, nh, b.bsum, b.hoff, p.maxchunks, b.off_part, p.parts, s);
+    SG_LAUNCH_CHECK();
+    k_rs_rec_partition<<<(uint32_t)p.maxchunks, 256, 0, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.hoff, b.pairs, b.st,
+                                                             p.wshift, p.parts, p.maxchunks);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    rec.begin(K_RS5_SCATTER, 0, kSMs * 8, 256, n);
+    k_rs_rec_scatter<OutT><<<kSMs * 8, 256, 0, s>>>(b.pairs, b.off_part, p.parts, rank, b.st);
     rec.end();
     SG_LAUNCH_CHECK();
     if (stats) {
@@ -896,7 +1072,7 @@ static int wyllie_entry(const void* succ_v, void* rank_v, uint64_t n, int varian
 template <class SuccT, class OutT>
 static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
                     cudaStream_t s, sg_stats* stats, sg_violation* viol) {
-    const RsPlan p = plan_rs(n, seed);
+    const RsPlan p = plan_rs(n, seed, (int)sizeof(OutT));
     Carver c(ws, ws_bytes);
     RsBufs b;
     if (!carve_rs(c, n, p, b)) return SG_ERR_WORKSPACE;
@@ -957,7 +1133,7 @@ size_t sg_wyllie_workspace_bytes(uint64_t n) {
 }
 
 size_t sg_rs_workspace_bytes(uint64_t n) {
-    const RsPlan p = plan_rs(n, 0);
+    const RsPlan p = plan_rs(n, 0, 8);  // the widest output needs the most windows
     Carver c(nullptr, 0);
     RsBufs b;
     carve_rs(c, n, p, b);

@@ -61,7 +61,7 @@ def test_workspace_sizes_scale():
         r = L.sg_rs_workspace_bytes(n)
         assert w >= 8 * n
         assert r >= 8 * n
-        assert r <= 8 * n + 2 * n + (1 << 20)   # level words + ruler lists stay O(n/32)
+        assert r <= 48 * n + (256 << 20)   # words, ruler ids, walk records, window pairs: O(n)
     assert L.sg_cc_workspace_bytes(1 << 20, 1 << 22) >= 4 << 20
 
 

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Full measurement pass: all bench workloads + reference arm + ncu launch list + captures.
+O=gpurun_out
+python -c "import __graft_entry__ as e; e.build()"
+timeout 600 python bench.py > $O/bench_lr26.json 2> $O/bench_lr26.err
+for w in lr28 lr28o cc22 cc26; do timeout 600 python bench.py --workload $w > $O/bench_$w.json 2> $O/bench_$w.err; done
+timeout 300 python bench.py --workload cc26 --variant sv --no-cpu --no-e2e > $O/bench_cc26sv.json 2>&1
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_lr26.json 2>&1
+timeout 300 python bench.py --impl reference --workload cc26 --steps 3 --warmup 1 > $O/bench_ref_cc26.json 2>&1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --workload cc26 --no-cpu --no-e2e > $O/bench_cc26_torchrun1.json 2> $O/bench_cc26_torchrun1.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_lr26.csv \
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-secondary > $O/ncu_launch_bench.log 2>&1
+for spec in "lr26:k_rs_walk0:walk26" "lr28:k_rs_walk0:walk28" "lr26:k_rs_expand0:expand26" "cc26:k_cc_hook_uf:hookuf26" "cc26:k_cc_part_scatter:partscatter26"; do
+  IFS=: read -r wl kern name <<< "$spec"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kern -c 1 -o $O/prof_$name \
+      python tools/prof_target.py $wl > $O/ncu_$name.log 2>&1
+done
