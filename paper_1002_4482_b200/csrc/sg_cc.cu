@@ -29,7 +29,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "sg_internal.cuh"
-#include "sg_scan.cuh"
+#include "sg_bucket.cuh"
 
 namespace sg {
 
@@ -260,11 +260,12 @@ __device__ __forceinline__ int part_of(E edges, unsigned long long e, unsigned l
     return (int)((u > v ? u : v) >> shift);
 }
 
-// per-tile counts of each partition; cnt layout [p * ntiles + tile]
+// partition sizes: per-tile counts (warp-aggregated in shared memory), one
+// atomic per partition per tile into the global totals; validates rows
 template <class E>
 __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigned long long m, unsigned long long n,
-                                                                uint32_t shift, int P, unsigned long long ntiles,
-                                                                uint32_t* __restrict__ cnt,
+                                                                uint32_t shift, int P,
+                                                                unsigned long long* __restrict__ totals,
                                                                 unsigned long long* flags) {
     __shared__ uint32_t s_cnt[MAX_PARTS + 1];
     if (threadIdx.x <= MAX_PARTS) s_cnt[threadIdx.x] = 0;
@@ -280,52 +281,42 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
         if (lane == (uint32_t)(__ffs(mm) - 1) && p < MAX_PARTS) atomicAdd(&s_cnt[p], (uint32_t)__popc(mm));
     }
     __syncthreads();
-    if (threadIdx.x < P) cnt[(unsigned long long)threadIdx.x * ntiles + blockIdx.x] = s_cnt[threadIdx.x];
+    if (threadIdx.x < P && s_cnt[threadIdx.x]) atomicAdd(totals + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
 }
 
-// Place every valid edge of the tile at off[p][tile] + its rank among the
-// tile's partition-p edges in index order (stable).  Edges are read
-// coalesced (e = tile + j*256 + t, which is index order for (j, t)); each
-// step is a block multisplit: warp match -> per-warp counts -> per-bin
-// offsets across the 8 warps.
-template <class E>
-__global__ void __launch_bounds__(PART_THREADS) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
-                                                                  uint32_t shift, int P, unsigned long long ntiles,
-                                                                  const unsigned long long* __restrict__ off,
-                                                                  uint2* __restrict__ out) {
-    constexpr int W = PART_THREADS / 32;
-    __shared__ uint32_t s_w[W][MAX_PARTS + 1];
-    __shared__ uint32_t s_tot[MAX_PARTS + 1];
-    __shared__ unsigned long long s_base[MAX_PARTS + 1];
-    const uint32_t lane = lane_id();
-    const int w = threadIdx.x >> 5;
-    if (threadIdx.x < P) s_base[threadIdx.x] = off[(unsigned long long)threadIdx.x * ntiles + blockIdx.x];
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * PART_TILE + threadIdx.x;
-    for (int j = 0; j < PART_ITEMS; ++j) {
-        uint2 uv;
-        int b = part_of(edges, e0 + (unsigned long long)j * PART_THREADS, m, n, shift, nullptr, false, uv);
-        if (b < 0) b = MAX_PARTS;
-        if (lane <= MAX_PARTS) s_w[w][lane] = 0;
-        __syncwarp();
-        const unsigned mm = __match_any_sync(0xffffffffu, b);
-        const uint32_t wrank = __popc(mm & ((1u << lane) - 1u));
-        if (wrank == 0) s_w[w][b] = __popc(mm);
-        __syncthreads();
-        if (threadIdx.x < P) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const uint32_t c = s_w[k][threadIdx.x];
-                s_w[k][threadIdx.x] = acc;
-                acc += c;
-            }
-            s_tot[threadIdx.x] = acc;
+// off_part = exclusive prefix of the P totals (off_part[P] = valid edges)
+__global__ void k_cc_part_offsets(const unsigned long long* __restrict__ totals, int P,
+                                  unsigned long long* __restrict__ off_part) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (int p = 0; p < P; ++p) {
+            off_part[p] = acc;
+            acc += totals[p];
         }
-        __syncthreads();
-        if (b < P) out[s_base[b] + s_w[w][b] + wrank] = uv;
-        __syncthreads();
-        if (threadIdx.x < P) s_base[threadIdx.x] += s_tot[threadIdx.x];
+        off_part[P] = acc;
     }
+}
+
+// scatter every valid edge into its partition (order inside a partition
+// follows the tiles' cursor grabs; hooking does not depend on it)
+template <class E>
+__global__ void __launch_bounds__(BK_THREADS) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
+                                                                uint32_t shift, int P,
+                                                                const unsigned long long* __restrict__ off_part,
+                                                                uint32_t* __restrict__ cursor, uint2* __restrict__ out) {
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * BK_TILE;
+    if (e0 >= m) return;
+    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool) -> bool {
+        uint2 uv;
+        const int p = part_of(edges, e, m, n, shift, nullptr, false, uv);
+        if (p < 0) return false;
+        pr = ((unsigned long long)uv.y << 32) | uv.x;
+        b = (uint32_t)p;
+        return true;
+    };
+    auto slot = [&](unsigned long long b) { return make_ulonglong2(off_part[b], off_part[b + 1] - off_part[b]); };
+    bucket_tile(get, slot, e0, min(e0 + BK_TILE, m), (uint32_t)P, 0, cursor,
+                reinterpret_cast<unsigned long long*>(out));
 }
 
 // ---------------------------------------------------------------------------
@@ -391,10 +382,9 @@ static CcPlan plan_cc(unsigned long long n, unsigned long long m) {
 }
 
 struct CcPartBufs {
-    unsigned long long* bsum = nullptr;
-    uint32_t* cnt = nullptr;
-    unsigned long long* off = nullptr;
-    unsigned long long* off_part = nullptr;
+    unsigned long long* totals = nullptr;   // [MAX_PARTS]
+    uint32_t* cursor = nullptr;             // [MAX_PARTS]
+    unsigned long long* off_part = nullptr; // [MAX_PARTS + 2]
     uint2* edges = nullptr;
 };
 
@@ -402,17 +392,14 @@ template <class E>
 static int partition_edges(E view, unsigned long long m, unsigned long long n, const CcPlan& p, CcPartBufs& b,
                            unsigned long long* flags, cudaStream_t s) {
     const uint32_t nt = (uint32_t)p.ntiles;
-    k_cc_part_count<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, p.ntiles, b.cnt, flags);
+    SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
+    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(uint32_t) * MAX_PARTS, s));
+    k_cc_part_count<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.totals, flags);
     SG_LAUNCH_CHECK();
-    const unsigned long long len = (unsigned long long)p.parts * p.ntiles;
-    const unsigned long long nb = (len + SCAN_BLOCK - 1) / SCAN_BLOCK;
-    k_scan_reduce<<<(uint32_t)nb, SCAN_THREADS, 0, s>>>(b.cnt, len, b.bsum);
+    k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
-    k_scan_top<<<1, SCAN_THREADS, 0, s>>>(b.bsum, nb, b.off_part + p.parts);
-    SG_LAUNCH_CHECK();
-    k_scan_down<<<(uint32_t)nb, SCAN_THREADS, 0, s>>>(b.cnt, len, b.bsum, b.off, p.ntiles, b.off_part);
-    SG_LAUNCH_CHECK();
-    k_cc_part_scatter<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, p.ntiles, b.off, b.edges);
+    const uint32_t ns = (uint32_t)((m + BK_TILE - 1) / BK_TILE);
+    k_cc_part_scatter<E><<<ns, BK_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
     SG_LAUNCH_CHECK();
     return SG_OK;
 }
@@ -495,10 +482,9 @@ static bool carve_cc(Carver& c, uint64_t n, uint64_t m, const CcPlan& p, unsigne
     flags = c.take<unsigned long long>(8);  // [0..3] flags, [4] roots
     Dws = c.take<uint32_t>(n);
     if (p.parts > 1) {
-        b.cnt = c.take<uint32_t>((size_t)p.parts * p.ntiles);
-        b.off = c.take<unsigned long long>((size_t)p.parts * p.ntiles);
+        b.totals = c.take<unsigned long long>(MAX_PARTS);
+        b.cursor = c.take<uint32_t>(MAX_PARTS);
         b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
-        b.bsum = c.take<unsigned long long>((size_t)p.parts * p.ntiles / SCAN_BLOCK + 2);
         b.edges = c.take<uint2>(m);
     }
     return c.ok;

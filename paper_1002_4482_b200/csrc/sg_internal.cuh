@@ -50,7 +50,8 @@ enum KernelId : int {
     K_EDGES_FROM_KEYS,
     K_CC_PARTITION,   // cc_partition stable split of the edges by endpoint window
     K_RS5_PARTITION,  // rs5_partition: rank the walk records, split by output window
-    K_RS5_SCATTER,    // rs5_scatter:   node-order scatter, one L2-resident window at a time
+    K_RS5_SCATTER,    // rs5_scatter:   fine window -> shared memory -> coalesced ranks
+    K_RS5_REFINE,     // rs5_refine:    coarse window -> fine windows
     K_COUNT_
 };
 

@@ -31,7 +31,7 @@
 #include <string.h>
 
 #include "sg_internal.cuh"
-#include "sg_scan.cuh"
+#include "sg_bucket.cuh"
 
 namespace sg {
 
@@ -391,6 +391,42 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
 // Lanes pull rulers from a global queue (warp-aggregated atomics), so a long
 // sublist never holds a whole warp's share of work hostage.
 
+// Warp-local pool of ruler ids: a warp claims QBATCH rulers from the level's
+// global queue with one atomic and hands them to its lanes as their chains
+// end.  (One atomic per refill from every warp serialised the walk on the
+// queue head: half of all stall samples sat on that broadcast.)
+constexpr uint32_t QBATCH = 64;
+
+struct ChainPool {
+    unsigned long long base = 0;   // next unclaimed id in the warp's batch (warp-uniform)
+    uint32_t left = 0;             // ids left in the batch (warp-uniform)
+
+    // lanes with `need` get an id < R (or none once the queue is dry);
+    // returns the lane's id or ~0ull
+    __device__ __forceinline__ unsigned long long take(bool need, unsigned long long* q, unsigned long long R,
+                                                       uint32_t lane) {
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        if (m == 0) return ~0ull;
+        const uint32_t cnt = __popc(m);
+        const uint32_t r = __popc(m & ((1u << lane) - 1u));
+        unsigned long long id;
+        if (cnt <= left) {
+            id = base + r;
+            base += cnt;
+            left -= cnt;
+        } else {
+            unsigned long long nb = 0;
+            if (lane == 0) nb = atomicAdd(q, (unsigned long long)QBATCH);
+            nb = __shfl_sync(0xffffffffu, nb, 0);
+            id = r < left ? base + r : nb + (r - left);
+            const uint32_t used_new = cnt - left;
+            base = nb + used_new;
+            left = QBATCH - used_new;
+        }
+        return (need && id < R) ? id : ~0ull;
+    }
+};
+
 template <class View>
 __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned long long* __restrict__ word,
                                                           const uint32_t* __restrict__ spl,
@@ -404,24 +440,18 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
     const uint32_t lane = lane_id();
     uint32_t sid = NIL, cur = 0, pre = 0, hops = 0;
     bool done = false;
+    ChainPool pool;
     for (;;) {
         const bool need = !done && sid == NIL;
-        const unsigned m = __ballot_sync(0xffffffffu, need);
-        if (m) {
-            const int leader = __ffs(m) - 1;
-            unsigned long long base = 0;
-            if ((int)lane == leader) base = atomicAdd(q, (unsigned long long)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (need) {
-                const unsigned long long s = base + __popc(m & ((1u << lane) - 1u));
-                if (s < R) {
-                    sid = (uint32_t)s;
-                    cur = spl[s];
-                    pre = 0;
-                    hops = 0;
-                } else {
-                    done = true;
-                }
+        const unsigned long long s = pool.take(need, q, R, lane);
+        if (need) {
+            if (s != ~0ull) {
+                sid = (uint32_t)s;
+                cur = spl[s];
+                pre = 0;
+                hops = 0;
+            } else {
+                done = true;
             }
         }
         if (__all_sync(0xffffffffu, done)) break;
@@ -466,7 +496,6 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
 // by window inside L2 (rs5_partition / rs5_scatter).
 
 constexpr int REC_CH = 1024;
-constexpr int REC_MAXP = 64;
 
 template <class SuccT>
 __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_rec(const SuccT* __restrict__ succ,
@@ -474,49 +503,33 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
                                                               const uint32_t* __restrict__ spl,
                                                               uint2* __restrict__ up, uint32_t* __restrict__ rec_cur,
                                                               unsigned long long* __restrict__ rec_sl,
-                                                              uint32_t* __restrict__ hist, ListStatus* st,
-                                                              uint32_t kbits, uint32_t salt, uint32_t cap_hops,
-                                                              uint32_t wshift, int P, unsigned long long maxchunks) {
+                                                              ListStatus* st, uint32_t kbits, uint32_t salt,
+                                                              uint32_t cap_hops, unsigned long long maxchunks) {
     if (layout_local(st)) return;  // k_rs_walk<Level0> takes this list
-    __shared__ uint32_t s_hist[WALK_THREADS / 32][REC_MAXP];
     const unsigned long long N = st->R[0];
     const unsigned long long R = st->R[1];
     unsigned long long* q = &st->qhead[0];
     const uint32_t lane = lane_id();
-    const int w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    for (int k = lane; k < REC_MAXP; k += 32) s_hist[w][k] = 0;
     unsigned long long chunk = ~0ull;  // warp-uniform
     uint32_t fill = REC_CH;            // warp-uniform: records used in the current chunk
     uint32_t sid = NIL, cur = 0, pre = 0;
     bool done = false;
-    auto close_chunk = [&]() {  // pad the tail with NIL records, publish the window histogram
+    auto close_chunk = [&]() {  // pad the tail with NIL records
         if (chunk == ~0ull) return;
         for (uint32_t k = fill + lane; k < REC_CH; k += 32) rec_cur[chunk * REC_CH + k] = NIL;
-        __syncwarp();
-        for (int k = lane; k < P; k += 32) {
-            hist[(unsigned long long)k * maxchunks + chunk] = s_hist[w][k];
-            s_hist[w][k] = 0;
-        }
-        __syncwarp();
     };
+    ChainPool pool;
     for (;;) {
         const bool need = !done && sid == NIL;
-        const unsigned m = __ballot_sync(0xffffffffu, need);
-        if (m) {
-            const int leader = __ffs(m) - 1;
-            unsigned long long base = 0;
-            if ((int)lane == leader) base = atomicAdd(q, (unsigned long long)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (need) {
-                const unsigned long long s = base + __popc(m & lt);
-                if (s < R) {
-                    sid = (uint32_t)s;
-                    cur = spl[s];
-                    pre = 0;
-                } else {
-                    done = true;
-                }
+        const unsigned long long s = pool.take(need, q, R, lane);
+        if (need) {
+            if (s != ~0ull) {
+                sid = (uint32_t)s;
+                cur = spl[s];
+                pre = 0;
+            } else {
+                done = true;
             }
         }
         const unsigned act = __ballot_sync(0xffffffffu, !done);
@@ -541,9 +554,6 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
             const unsigned long long r = chunk * REC_CH + fill + __popc(act & lt);
             rec_cur[r] = cur;
             rec_sl[r] = ((unsigned long long)sid << 32) | pre;
-            const uint32_t win = cur >> wshift;
-            const unsigned same = __match_any_sync(act, win);
-            if ((same & lt) == 0) atomicAdd(&s_hist[w][win], (uint32_t)__popc(same));
         }
         fill += cnt;
         if (!done) {
@@ -570,76 +580,84 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
     close_chunk();
 }
 
-// rank of every record (rank = IS_1[sid] - local - 1, listrank.py:375-379)
-// partitioned stably by output window: pairs[...] = {cur, rank}.  One block
-// per record chunk; block multisplit as in the edge partition.
-__global__ void __launch_bounds__(256) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
-                                                          const unsigned long long* __restrict__ rec_sl,
-                                                          const uint32_t* __restrict__ IS1,
-                                                          const unsigned long long* __restrict__ off,
-                                                          unsigned long long* __restrict__ pairs,
-                                                          const ListStatus* st, uint32_t wshift, int P,
-                                                          unsigned long long maxchunks) {
+// Node-order materialisation of the ranks in three streaming passes.  For a
+// valid list every node appears in exactly one record, so every output window
+// receives exactly its own node count: window w of size S owns the slots
+// [w*S, w*S + S) of the next buffer, and a global cursor per window (one
+// atomic per window per tile) is all the bookkeeping needed.
+//   rs5_partition: records -> {cur, rank} pairs by coarse window (2^cshift nodes)
+//   rs5_refine:    coarse window -> fine windows (2^fshift nodes, one CTA's smem)
+//   rs5_scatter:   fine window -> shared memory -> coalesced rank stores
+// Invalid inputs can overfill a window; such writes are dropped (the call
+// reports the list invalid anyway).
+__global__ void __launch_bounds__(BK_THREADS) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
+                                                                 const unsigned long long* __restrict__ rec_sl,
+                                                                 const uint32_t* __restrict__ IS1,
+                                                                 uint32_t* __restrict__ cursor,
+                                                                 unsigned long long* __restrict__ pairs,
+                                                                 ListStatus* st, uint32_t cshift, uint32_t nbins) {
     if (layout_local(st) || st->overflow) return;
-    const unsigned long long chunk = blockIdx.x;
-    if (chunk >= st->chunks) return;
-    constexpr int W = 256 / 32;
-    __shared__ uint32_t s_w[W][REC_MAXP + 1];
-    __shared__ uint32_t s_tot[REC_MAXP + 1];
-    __shared__ unsigned long long s_base[REC_MAXP + 1];
+    const unsigned long long total = st->chunks * REC_CH;
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * BK_TILE;
+    if (e0 >= total) return;
     const unsigned long long R1 = st->R[1];
-    const uint32_t lane = lane_id();
-    const int w = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < P; k += 256) s_base[k] = off[(unsigned long long)k * maxchunks + chunk];
-    for (int j = 0; j < REC_CH / 256; ++j) {
-        const unsigned long long r = chunk * REC_CH + (unsigned long long)j * 256 + threadIdx.x;
-        const uint32_t c = rec_cur[r];
-        int b = REC_MAXP;
-        unsigned long long pr = 0;
-        if (c != NIL) {
-            const unsigned long long sl = rec_sl[r];
+    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool want) -> bool {
+        const uint32_t c = rec_cur[e];
+        if (c == NIL) return false;
+        b = c >> cshift;
+        if (want) {  // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
+            const unsigned long long sl = rec_sl[e];
             const unsigned long long o = sl >> 32;
             const uint32_t rk = o < R1 ? __ldg(IS1 + o) - (uint32_t)sl - 1u : 0u;
             pr = ((unsigned long long)c << 32) | rk;
-            b = (int)(c >> wshift);
         }
-        for (int k = lane; k <= REC_MAXP; k += 32) s_w[w][k] = 0;
-        __syncwarp();
-        const unsigned mm = __match_any_sync(0xffffffffu, b);
-        const uint32_t wrank = __popc(mm & ((1u << lane) - 1u));
-        if (wrank == 0) s_w[w][b] = __popc(mm);
-        __syncthreads();
-        for (int k = threadIdx.x; k < P; k += 256) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int x = 0; x < W; ++x) {
-                const uint32_t v = s_w[x][k];
-                s_w[x][k] = acc;
-                acc += v;
-            }
-            s_tot[k] = acc;
-        }
-        __syncthreads();
-        if (b < P) pairs[s_base[b] + s_w[w][b] + wrank] = pr;
-        __syncthreads();
-        for (int k = threadIdx.x; k < P; k += 256) s_base[k] += s_tot[k];
-    }
+        return true;
+    };
+    auto slot = [&](unsigned long long b) { return make_ulonglong2(b << cshift, 1ull << cshift); };
+    if (bucket_tile(get, slot, e0, min(e0 + BK_TILE, total), nbins, 0, cursor, pairs)) st->bad = 1;
 }
 
-// node-order scatter of the window-partitioned {cur, rank} pairs: the pairs
-// are window-major, so the grid-stride sweep keeps ~one 32 MiB output window
-// live in L2 and the ranks reach HBM as full lines
-template <class OutT>
-__global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
-                                                        const unsigned long long* __restrict__ off_part, int P,
-                                                        OutT* __restrict__ rank, const ListStatus* st) {
+__global__ void __launch_bounds__(BK_THREADS) k_rs_rec_refine(const unsigned long long* __restrict__ in,
+                                                              uint32_t* __restrict__ cursor,
+                                                              unsigned long long* __restrict__ out, ListStatus* st,
+                                                              unsigned long long n, uint32_t cshift, uint32_t fshift) {
     if (layout_local(st) || st->overflow) return;
-    const unsigned long long total = off_part[P];
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const unsigned long long pr = __ldcs(pairs + i);
-        rank[pr >> 32] = (OutT)(uint32_t)pr;
+    // tiles never straddle a coarse window (2^cshift is a multiple of BK_TILE)
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * BK_TILE;
+    if (e0 >= n) return;
+    const unsigned long long c = e0 >> cshift;
+    const uint32_t fb = 1u << (cshift - fshift);
+    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool) -> bool {
+        pr = in[e];
+        const unsigned long long cur = pr >> 32;
+        if ((cur >> cshift) != c) return false;  // only for invalid inputs
+        b = (uint32_t)((cur >> fshift) & (fb - 1));
+        return true;
+    };
+    auto slot = [&](unsigned long long b) { return make_ulonglong2(b << fshift, 1ull << fshift); };
+    if (bucket_tile(get, slot, e0, min(e0 + BK_TILE, n), fb, c * fb, cursor, out)) st->bad = 1;
+}
+
+// one CTA per fine window: scatter its pairs into shared memory, then store
+// the window coalesced
+template <class OutT>
+__global__ void __launch_bounds__(BK_THREADS) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
+                                                               OutT* __restrict__ rank, unsigned long long n,
+                                                               uint32_t fshift, const ListStatus* st) {
+    if (layout_local(st) || st->overflow) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    OutT* win = reinterpret_cast<OutT*>(smem_raw);
+    const unsigned long long w0 = (unsigned long long)blockIdx.x << fshift;
+    if (w0 >= n) return;
+    const uint32_t size = (uint32_t)min((unsigned long long)1 << fshift, n - w0);
+    const uint32_t mask = (1u << fshift) - 1u;
+    for (uint32_t i = threadIdx.x; i < size; i += BK_THREADS) {
+        const unsigned long long pr = __ldcs(pairs + w0 + i);
+        const unsigned long long cur = pr >> 32;
+        if ((cur >> fshift) == (w0 >> fshift)) win[cur & mask] = (OutT)(uint32_t)pr;
     }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < size; i += BK_THREADS) rank[w0 + i] = win[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -749,8 +767,9 @@ struct RsPlan {
     int levels = 0;                              // walked levels (final level = levels)
     uint32_t walk_cap = WALK_CAP_HOPS;
     int load_mode = 0;
-    uint32_t wshift = 23;                        // record path: output window = 2^wshift nodes
-    int parts = 1;                               // number of output windows
+    uint32_t cshift = 19;                        // record path: coarse window = 2^cshift nodes
+    uint32_t fshift = 13;                        // fine window = 2^fshift nodes (32 KiB of output)
+    uint32_t cbins = 1;                          // number of coarse windows
     uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
@@ -778,12 +797,15 @@ static uint32_t mix32(uint64_t x) {
 
 static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     RsPlan p;
-    // 32 MiB of output per window; at most REC_MAXP windows
-    uint32_t ws = out_bytes >= 8 ? 22 : 23;
-    while (((n + (1ull << ws) - 1) >> ws) > (unsigned long long)REC_MAXP) ++ws;
-    p.wshift = ws;
-    p.parts = (int)((n + (1ull << ws) - 1) >> ws);
-    if (p.parts < 1) p.parts = 1;
+    // fine windows fill 32 KiB of shared memory; <= 256 coarse windows keep the
+    // partition pass writing >= 512-byte runs per bin and tile
+    p.fshift = out_bytes >= 8 ? 12 : 13;
+    uint32_t cs = p.fshift + 1;
+    if (cs < 14) cs = 14;  // 2^cshift must be a multiple of BK_TILE
+    while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
+    if (cs - p.fshift > 11) p.fshift = cs - 11;  // <= BK_MAXB fine bins per coarse window
+    p.cshift = cs;
+    p.cbins = (uint32_t)((n + (1ull << cs) - 1) >> cs);
     // one lane per ruler is plenty; every warp that walks may leave one partial chunk
     unsigned long long wg = ((n >> 5) + 2 * WALK_THREADS - 1) / (2 * WALK_THREADS);
     if (wg < (unsigned long long)kSMs) wg = kSMs;
@@ -819,10 +841,7 @@ struct RsBufs {
     uint32_t* rec_cur = nullptr;
     unsigned long long* rec_sl = nullptr;
     unsigned long long* pairs = nullptr;
-    uint32_t* hist = nullptr;
-    unsigned long long* hoff = nullptr;
-    unsigned long long* bsum = nullptr;
-    unsigned long long* off_part = nullptr;
+    uint32_t* cursor = nullptr;      // coarse cursors, then fine cursors
     uint32_t* tiles = nullptr;
     uint32_t* spl[SG_MAX_LEVELS] = {};
     uint2* lvl[SG_MAX_LEVELS + 1] = {};
@@ -837,15 +856,12 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     b.word0 = c.take<unsigned long long>(n);
     if (p.levels > 0) {
         const unsigned long long nrec = p.maxchunks * REC_CH;
-        const unsigned long long nh = (unsigned long long)p.parts * p.maxchunks;
+        const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
         b.rid = c.take<uint32_t>(n);
         b.rec_cur = c.take<uint32_t>(nrec);
-        b.rec_sl = c.take<unsigned long long>(nrec);
-        b.pairs = c.take<unsigned long long>(nrec);
-        b.hist = c.take<uint32_t>(nh);
-        b.hoff = c.take<unsigned long long>(nh);
-        b.bsum = c.take<unsigned long long>(nh / SCAN_BLOCK + 2);
-        b.off_part = c.take<unsigned long long>(REC_MAXP + 2);
+        b.rec_sl = c.take<unsigned long long>(nrec > npad ? nrec : npad);  // reused for the fine pass
+        b.pairs = c.take<unsigned long long>(npad);
+        b.cursor = c.take<uint32_t>(p.cbins + (npad >> p.fshift));
     }
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     b.tiles = c.take<uint32_t>(ntiles + 1);
@@ -964,11 +980,10 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
         if (k == 0) {
-            SG_CUDA(cudaMemsetAsync(b.hist, 0, sizeof(uint32_t) * (size_t)p.parts * p.maxchunks, s));
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
             k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rid, b.spl[0], b.lvl[1], b.rec_cur,
-                                                                    b.rec_sl, b.hist, b.st, p.kbits[0], p.salt[0],
-                                                                    p.walk_cap, p.wshift, p.parts, p.maxchunks);
+                                                                    b.rec_sl, b.st, p.kbits[0], p.salt[0],
+                                                                    p.walk_cap, p.maxchunks);
             SG_LAUNCH_CHECK();
             k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.word0,
                                                                         b.spl[0], b.lvl[1], b.st, 0, p.kbits[0],
@@ -1000,17 +1015,24 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     k_rs_expand0<OutT><<<g, 256, 0, s>>>(b.word0, b.IS[1], rank, n, b.st);  // local layouts
     rec.end();
     SG_LAUNCH_CHECK();
-    // scattered layouts: rank the records, partition them by output window, scatter
-    const unsigned long long nh = (unsigned long long)p.parts * p.maxchunks;
-    rec.begin(K_RS5_PARTITION, 0, (uint32_t)p.maxchunks, 256, n);
-    launch_scan(b.hist, nh, b.bsum, b.hoff, p.maxchunks, b.off_part, p.parts, s);
-    SG_LAUNCH_CHECK();
-    k_rs_rec_partition<<<(uint32_t)p.maxchunks, 256, 0, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.hoff, b.pairs, b.st,
-                                                             p.wshift, p.parts, p.maxchunks);
+    // scattered layouts: rank the records, bucket them by output window, scatter
+    const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
+    const unsigned long long nfine = npad >> p.fshift;
+    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(uint32_t) * (size_t)(p.cbins + nfine), s));
+    const uint32_t gpart = (uint32_t)((p.maxchunks * REC_CH + BK_TILE - 1) / BK_TILE);
+    rec.begin(K_RS5_PARTITION, 0, gpart, BK_THREADS, n);
+    k_rs_rec_partition<<<gpart, BK_THREADS, 0, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
+                                                     p.cshift, p.cbins);
     rec.end();
     SG_LAUNCH_CHECK();
-    rec.begin(K_RS5_SCATTER, 0, kSMs * 8, 256, n);
-    k_rs_rec_scatter<OutT><<<kSMs * 8, 256, 0, s>>>(b.pairs, b.off_part, p.parts, rank, b.st);
+    const uint32_t gref = (uint32_t)((n + BK_TILE - 1) / BK_TILE);
+    rec.begin(K_RS5_REFINE, 0, gref, BK_THREADS, n);
+    k_rs_rec_refine<<<gref, BK_THREADS, 0, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    const uint32_t gsc = (uint32_t)((n + (1ull << p.fshift) - 1) >> p.fshift);
+    rec.begin(K_RS5_SCATTER, 0, gsc, BK_THREADS, n);
+    k_rs_rec_scatter<OutT><<<gsc, BK_THREADS, sizeof(OutT) << p.fshift, s>>>(b.rec_sl, rank, n, p.fshift, b.st);
     rec.end();
     SG_LAUNCH_CHECK();
     if (stats) {
@@ -1133,11 +1155,15 @@ size_t sg_wyllie_workspace_bytes(uint64_t n) {
 }
 
 size_t sg_rs_workspace_bytes(uint64_t n) {
-    const RsPlan p = plan_rs(n, 0, 8);  // the widest output needs the most windows
-    Carver c(nullptr, 0);
-    RsBufs b;
-    carve_rs(c, n, p, b);
-    return c.off + 256;
+    size_t best = 0;
+    for (int ob : {4, 8}) {  // window geometry depends on the output width
+        const RsPlan p = plan_rs(n, 0, ob);
+        Carver c(nullptr, 0);
+        RsBufs b;
+        carve_rs(c, n, p, b);
+        if (c.off + 256 > best) best = c.off + 256;
+    }
+    return best;
 }
 
 int sg_wyllie_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype, uint64_t n, int variant, void* ws,

@@ -200,6 +200,15 @@ def test_invalid_large_lists_detected(cuda):
         with pytest.raises(g.InvalidListError) as ei:
             fn(g.SuccessorList(s))
         assert str(ei.value) == str(want)
+    # two nodes share a successor (in-degree 2): the skipped node is unreachable
+    s = base.copy()
+    a = int(order[n // 2])
+    s[a] = s[int(s[a])]
+    want = g.validate_list(g.SuccessorList(s))
+    for fn in (lambda x: g.rs_rank(x, 64), lambda x: g.wyllie_rank(x, 64)):
+        with pytest.raises(g.InvalidListError) as ei:
+            fn(g.SuccessorList(s))
+        assert str(ei.value) == str(want)
     # out of range
     s = base.copy()
     s[12345] = n + 7
