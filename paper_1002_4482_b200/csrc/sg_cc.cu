@@ -29,7 +29,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "sg_internal.cuh"
-#include "sg_bucket.cuh"
+#include "sg_msplit.cuh"
 
 namespace sg {
 
@@ -297,15 +297,21 @@ __global__ void k_cc_part_offsets(const unsigned long long* __restrict__ totals,
     }
 }
 
-// scatter every valid edge into its partition (order inside a partition
-// follows the tiles' cursor grabs; hooking does not depend on it)
+// Scatter every valid edge into its partition (block multisplit by ballots,
+// sg_msplit.cuh; one global atomic per partition per 4096-edge tile).
+constexpr int PS_ITEMS = 16;
+constexpr int PS_TILE = MS_THREADS * PS_ITEMS;
+
 template <class E>
-__global__ void __launch_bounds__(BK_THREADS) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
+__global__ void __launch_bounds__(MS_THREADS) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
                                                                 uint32_t shift, int P,
                                                                 const unsigned long long* __restrict__ off_part,
-                                                                uint32_t* __restrict__ cursor, uint2* __restrict__ out) {
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * BK_TILE;
+                                                                unsigned long long* __restrict__ cursor,
+                                                                uint2* __restrict__ out) {
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * PS_TILE;
     if (e0 >= m) return;
+    int nbits = 0;
+    while ((1 << nbits) < P) ++nbits;
     auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool) -> bool {
         uint2 uv;
         const int p = part_of(edges, e, m, n, shift, nullptr, false, uv);
@@ -314,9 +320,9 @@ __global__ void __launch_bounds__(BK_THREADS) k_cc_part_scatter(E edges, unsigne
         b = (uint32_t)p;
         return true;
     };
-    auto slot = [&](unsigned long long b) { return make_ulonglong2(off_part[b], off_part[b + 1] - off_part[b]); };
-    bucket_tile(get, slot, e0, min(e0 + BK_TILE, m), (uint32_t)P, 0, cursor,
-                reinterpret_cast<unsigned long long*>(out));
+    auto slot = [&](uint32_t b) { return make_ulonglong2(off_part[b], off_part[b + 1] - off_part[b]); };
+    ms_tile<PS_ITEMS>(get, slot, e0, min(e0 + PS_TILE, m), (uint32_t)P, nbits, cursor,
+                      reinterpret_cast<unsigned long long*>(out));
 }
 
 // ---------------------------------------------------------------------------
@@ -383,7 +389,7 @@ static CcPlan plan_cc(unsigned long long n, unsigned long long m) {
 
 struct CcPartBufs {
     unsigned long long* totals = nullptr;   // [MAX_PARTS]
-    uint32_t* cursor = nullptr;             // [MAX_PARTS]
+    unsigned long long* cursor = nullptr;   // [MAX_PARTS]
     unsigned long long* off_part = nullptr; // [MAX_PARTS + 2]
     uint2* edges = nullptr;
 };
@@ -393,13 +399,13 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
                            unsigned long long* flags, cudaStream_t s) {
     const uint32_t nt = (uint32_t)p.ntiles;
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
-    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(uint32_t) * MAX_PARTS, s));
+    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     k_cc_part_count<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.totals, flags);
     SG_LAUNCH_CHECK();
     k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
-    const uint32_t ns = (uint32_t)((m + BK_TILE - 1) / BK_TILE);
-    k_cc_part_scatter<E><<<ns, BK_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
+    const uint32_t ns = (uint32_t)((m + PS_TILE - 1) / PS_TILE);
+    k_cc_part_scatter<E><<<ns, MS_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
     SG_LAUNCH_CHECK();
     return SG_OK;
 }
@@ -483,7 +489,7 @@ static bool carve_cc(Carver& c, uint64_t n, uint64_t m, const CcPlan& p, unsigne
     Dws = c.take<uint32_t>(n);
     if (p.parts > 1) {
         b.totals = c.take<unsigned long long>(MAX_PARTS);
-        b.cursor = c.take<uint32_t>(MAX_PARTS);
+        b.cursor = c.take<unsigned long long>(MAX_PARTS);
         b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
         b.edges = c.take<uint2>(m);
     }

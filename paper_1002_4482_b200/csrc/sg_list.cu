@@ -31,7 +31,7 @@
 #include <string.h>
 
 #include "sg_internal.cuh"
-#include "sg_bucket.cuh"
+#include "sg_msplit.cuh"
 
 namespace sg {
 
@@ -278,38 +278,38 @@ template <class SuccT>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restrict__ succ,
                                                             uint32_t* __restrict__ tile_cnt, ListStatus* st,
                                                             uint32_t kbits, uint32_t salt) {
-    const unsigned long long N = st->R[0];
-    const unsigned long long base = (unsigned long long)blockIdx.x * TILE;
-    if (base >= N) {
-        if (threadIdx.x == 0) tile_cnt[blockIdx.x] = 0;
-        return;
-    }
-    SuccT v[TILE_ITEMS];
-#pragma unroll
-    for (int j = 0; j < TILE_ITEMS; ++j) {
-        const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
-        v[j] = i < N ? __ldcs(succ + i) : SuccT(0);
-    }
-    uint32_t cnt = 0, loc = 0;
-#pragma unroll
-    for (int j = 0; j < TILE_ITEMS; ++j) {
-        const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
-        if (i < N) {
-            const unsigned long long x = as_index<SuccT>(v[j]);
-            if (x >= N || x == i) note_succ(st, i, x, N);
-            cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
-            loc += (x + 16 > i && x < i + 16) ? 1u : 0u;
-        }
-    }
     typedef cub::BlockReduce<uint32_t, TILE_THREADS> BR;
     __shared__ typename BR::TempStorage tmp;
-    const uint32_t tot = BR(tmp).Sum(cnt);
-    __syncthreads();
-    const uint32_t ltot = BR(tmp).Sum(loc);
-    if (threadIdx.x == 0) {
-        tile_cnt[blockIdx.x] = tot;
-        if (ltot) atomicAdd(&st->local, (unsigned long long)ltot);
+    const unsigned long long N = st->R[0];
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
+    uint32_t loc = 0;
+    // persistent blocks walk the tiles; all loads of a tile are issued before
+    // the (rare) atomics of the self-loop / range census
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long base = tile * TILE;
+        SuccT v[TILE_ITEMS];
+#pragma unroll
+        for (int j = 0; j < TILE_ITEMS; ++j) {
+            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+            v[j] = i < N ? __ldcs(succ + i) : SuccT(0);
+        }
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int j = 0; j < TILE_ITEMS; ++j) {
+            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
+            if (i < N) {
+                const unsigned long long x = as_index<SuccT>(v[j]);
+                if (x >= N || x == i) note_succ(st, i, x, N);
+                cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
+                loc += (x + 16 > i && x < i + 16) ? 1u : 0u;
+            }
+        }
+        const uint32_t tot = BR(tmp).Sum(cnt);
+        if (threadIdx.x == 0) tile_cnt[tile] = tot;
+        __syncthreads();
     }
+    const uint32_t ltot = BR(tmp).Sum(loc);
+    if (threadIdx.x == 0 && ltot) atomicAdd(&st->local, (unsigned long long)ltot);
 }
 
 // Lists laid out mostly in chain order (successor within 16 slots) walk
@@ -377,8 +377,10 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
         if (flags & (1u << j)) {
             if (id < cap) {
                 spl[id] = (uint32_t)(i0 + j);
-                word[i0 + j] = kPacked ? ((id << 32) | (word[i0 + j] & 0xFFFFFFFFull)) : (id << 32);
-                if (rid != nullptr) rid[i0 + j] = (uint32_t)id;
+                if (rid != nullptr)
+                    rid[i0 + j] = (uint32_t)id;  // level 0: ids live in rid[]
+                else
+                    word[i0 + j] = kPacked ? ((id << 32) | (word[i0 + j] & 0xFFFFFFFFull)) : (id << 32);
             }
             ++id;
         }
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
                                                           const uint32_t* __restrict__ spl,
                                                           uint2* __restrict__ up, ListStatus* st, int level,
                                                           uint32_t kbits, uint32_t salt, uint32_t cap_hops,
-                                                          bool only_local) {
+                                                          bool only_local, const uint32_t* __restrict__ rid) {
     if (only_local && !layout_local(st)) return;  // k_rs_walk0 takes this list
     const unsigned long long N = st->R[level];
     const unsigned long long R = st->R[level + 1];
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
             up[sid] = make_uint2(sid, pre);
             sid = NIL;
         } else if (is_ruler((uint32_t)nx, kbits, salt)) {
-            up[sid] = make_uint2((uint32_t)(word[nx] >> 32), pre);
+            up[sid] = make_uint2(rid != nullptr ? __ldg(rid + nx) : (uint32_t)(word[nx] >> 32), pre);
             sid = NIL;
         } else if (hops >= cap_hops) {
             st->overflow = 1;
@@ -504,7 +506,8 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
                                                               uint2* __restrict__ up, uint32_t* __restrict__ rec_cur,
                                                               unsigned long long* __restrict__ rec_sl,
                                                               ListStatus* st, uint32_t kbits, uint32_t salt,
-                                                              uint32_t cap_hops, unsigned long long maxchunks) {
+                                                              uint32_t cap_hops, unsigned long long maxchunks,
+                                                              int load_mode) {
     if (layout_local(st)) return;  // k_rs_walk<Level0> takes this list
     const unsigned long long N = st->R[0];
     const unsigned long long R = st->R[1];
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
         const unsigned act = __ballot_sync(0xffffffffu, !done);
         if (act == 0) break;
         unsigned long long nxl = 0;
-        if (!done) nxl = as_index<SuccT>(succ[cur]);
+        if (!done) nxl = as_index<SuccT>(ld_mode(succ + cur, load_mode));
         // append this step's records, warp-contiguous
         const uint32_t cnt = __popc(act);
         if (fill + cnt > REC_CH) {
@@ -582,23 +585,32 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
 
 // Node-order materialisation of the ranks in three streaming passes.  For a
 // valid list every node appears in exactly one record, so every output window
-// receives exactly its own node count: window w of size S owns the slots
-// [w*S, w*S + S) of the next buffer, and a global cursor per window (one
-// atomic per window per tile) is all the bookkeeping needed.
-//   rs5_partition: records -> {cur, rank} pairs by coarse window (2^cshift nodes)
-//   rs5_refine:    coarse window -> fine windows (2^fshift nodes, one CTA's smem)
-//   rs5_scatter:   fine window -> shared memory -> coalesced rank stores
-// Invalid inputs can overfill a window; such writes are dropped (the call
-// reports the list invalid anyway).
-__global__ void __launch_bounds__(BK_THREADS) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
+// receives exactly its own node count: window w of 2^shift nodes owns the
+// slots [w << shift, (w + 1) << shift) of the next buffer.
+//   rs5_partition: record -> {cur, rank} pair, by coarse window (<= MS_MAXB bins)
+//   rs5_refine:    coarse window -> fine windows (2^fshift nodes)
+//   rs5_scatter:   one CTA per fine window: shared memory -> coalesced ranks
+// Both bucketing passes are ballot multisplits (sg_msplit.cuh).  Invalid
+// inputs can overfill a window; such writes are dropped (the call reports
+// the list invalid anyway).
+constexpr int RP_ITEMS = 64;
+constexpr int RP_TILE = MS_THREADS * RP_ITEMS;
+
+__device__ __forceinline__ int ceil_log2(uint32_t x) {
+    int b = 0;
+    while ((1u << b) < x) ++b;
+    return b;
+}
+
+__global__ void __launch_bounds__(MS_THREADS) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
                                                                  const unsigned long long* __restrict__ rec_sl,
                                                                  const uint32_t* __restrict__ IS1,
-                                                                 uint32_t* __restrict__ cursor,
+                                                                 unsigned long long* __restrict__ cursor,
                                                                  unsigned long long* __restrict__ pairs,
-                                                                 ListStatus* st, uint32_t cshift, uint32_t nbins) {
+                                                                 ListStatus* st, uint32_t cshift, uint32_t cbins) {
     if (layout_local(st) || st->overflow) return;
     const unsigned long long total = st->chunks * REC_CH;
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * BK_TILE;
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * RP_TILE;
     if (e0 >= total) return;
     const unsigned long long R1 = st->R[1];
     auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool want) -> bool {
@@ -613,17 +625,18 @@ __global__ void __launch_bounds__(BK_THREADS) k_rs_rec_partition(const uint32_t*
         }
         return true;
     };
-    auto slot = [&](unsigned long long b) { return make_ulonglong2(b << cshift, 1ull << cshift); };
-    if (bucket_tile(get, slot, e0, min(e0 + BK_TILE, total), nbins, 0, cursor, pairs)) st->bad = 1;
+    auto slot = [&](uint32_t b) { return make_ulonglong2((unsigned long long)b << cshift, 1ull << cshift); };
+    if (ms_tile<RP_ITEMS>(get, slot, e0, min(e0 + RP_TILE, total), cbins, ceil_log2(cbins), cursor, pairs))
+        st->bad = 1;
 }
 
-__global__ void __launch_bounds__(BK_THREADS) k_rs_rec_refine(const unsigned long long* __restrict__ in,
-                                                              uint32_t* __restrict__ cursor,
+__global__ void __launch_bounds__(MS_THREADS) k_rs_rec_refine(const unsigned long long* __restrict__ in,
+                                                              unsigned long long* __restrict__ cursor,
                                                               unsigned long long* __restrict__ out, ListStatus* st,
                                                               unsigned long long n, uint32_t cshift, uint32_t fshift) {
     if (layout_local(st) || st->overflow) return;
-    // tiles never straddle a coarse window (2^cshift is a multiple of BK_TILE)
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * BK_TILE;
+    // tiles never straddle a coarse window (2^cshift is a multiple of RP_TILE)
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * RP_TILE;
     if (e0 >= n) return;
     const unsigned long long c = e0 >> cshift;
     const uint32_t fb = 1u << (cshift - fshift);
@@ -634,14 +647,17 @@ __global__ void __launch_bounds__(BK_THREADS) k_rs_rec_refine(const unsigned lon
         b = (uint32_t)((cur >> fshift) & (fb - 1));
         return true;
     };
-    auto slot = [&](unsigned long long b) { return make_ulonglong2(b << fshift, 1ull << fshift); };
-    if (bucket_tile(get, slot, e0, min(e0 + BK_TILE, n), fb, c * fb, cursor, out)) st->bad = 1;
+    auto slot = [&](uint32_t b) {
+        return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift);
+    };
+    if (ms_tile<RP_ITEMS>(get, slot, e0, min(e0 + RP_TILE, n), fb, (int)(cshift - fshift), cursor + c * fb, out))
+        st->bad = 1;
 }
 
 // one CTA per fine window: scatter its pairs into shared memory, then store
 // the window coalesced
 template <class OutT>
-__global__ void __launch_bounds__(BK_THREADS) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
+__global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
                                                                OutT* __restrict__ rank, unsigned long long n,
                                                                uint32_t fshift, const ListStatus* st) {
     if (layout_local(st) || st->overflow) return;
@@ -651,13 +667,13 @@ __global__ void __launch_bounds__(BK_THREADS) k_rs_rec_scatter(const unsigned lo
     if (w0 >= n) return;
     const uint32_t size = (uint32_t)min((unsigned long long)1 << fshift, n - w0);
     const uint32_t mask = (1u << fshift) - 1u;
-    for (uint32_t i = threadIdx.x; i < size; i += BK_THREADS) {
+    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) {
         const unsigned long long pr = __ldcs(pairs + w0 + i);
         const unsigned long long cur = pr >> 32;
         if ((cur >> fshift) == (w0 >> fshift)) win[cur & mask] = (OutT)(uint32_t)pr;
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < size; i += BK_THREADS) rank[w0 + i] = win[i];
+    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) rank[w0 + i] = win[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -767,9 +783,10 @@ struct RsPlan {
     int levels = 0;                              // walked levels (final level = levels)
     uint32_t walk_cap = WALK_CAP_HOPS;
     int load_mode = 0;
-    uint32_t cshift = 19;                        // record path: coarse window = 2^cshift nodes
-    uint32_t fshift = 13;                        // fine window = 2^fshift nodes (32 KiB of output)
+    uint32_t fshift = 13;                        // record path: fine window = 2^fshift nodes (32 KiB)
+    uint32_t cshift = 20;                        // coarse window = 2^cshift nodes
     uint32_t cbins = 1;                          // number of coarse windows
+    unsigned long long nwin = 1;                 // number of fine windows
     uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
@@ -797,15 +814,16 @@ static uint32_t mix32(uint64_t x) {
 
 static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     RsPlan p;
-    // fine windows fill 32 KiB of shared memory; <= 256 coarse windows keep the
-    // partition pass writing >= 512-byte runs per bin and tile
+    // a fine window fills 32 KiB of shared memory in rs5_scatter; coarse
+    // windows: few enough bins for one multisplit, >= 64 pairs per bin per tile
     p.fshift = out_bytes >= 8 ? 12 : 13;
     uint32_t cs = p.fshift + 1;
-    if (cs < 14) cs = 14;  // 2^cshift must be a multiple of BK_TILE
+    if (cs < 14) cs = 14;  // 2^cshift must be a multiple of RP_TILE
     while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
-    if (cs - p.fshift > 11) p.fshift = cs - 11;  // <= BK_MAXB fine bins per coarse window
+    while (cs - p.fshift > 10) ++p.fshift;  // <= MS_MAXB fine windows per coarse window
     p.cshift = cs;
     p.cbins = (uint32_t)((n + (1ull << cs) - 1) >> cs);
+    p.nwin = (unsigned long long)p.cbins << (cs - p.fshift);
     // one lane per ruler is plenty; every warp that walks may leave one partial chunk
     unsigned long long wg = ((n >> 5) + 2 * WALK_THREADS - 1) / (2 * WALK_THREADS);
     if (wg < (unsigned long long)kSMs) wg = kSMs;
@@ -841,7 +859,7 @@ struct RsBufs {
     uint32_t* rec_cur = nullptr;
     unsigned long long* rec_sl = nullptr;
     unsigned long long* pairs = nullptr;
-    uint32_t* cursor = nullptr;      // coarse cursors, then fine cursors
+    unsigned long long* cursor = nullptr;  // coarse cursors, then fine cursors
     uint32_t* tiles = nullptr;
     uint32_t* spl[SG_MAX_LEVELS] = {};
     uint2* lvl[SG_MAX_LEVELS + 1] = {};
@@ -856,12 +874,12 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     b.word0 = c.take<unsigned long long>(n);
     if (p.levels > 0) {
         const unsigned long long nrec = p.maxchunks * REC_CH;
-        const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
         b.rid = c.take<uint32_t>(n);
         b.rec_cur = c.take<uint32_t>(nrec);
-        b.rec_sl = c.take<unsigned long long>(nrec > npad ? nrec : npad);  // reused for the fine pass
-        b.pairs = c.take<unsigned long long>(npad);
-        b.cursor = c.take<uint32_t>(p.cbins + (npad >> p.fshift));
+        const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
+        b.rec_sl = c.take<unsigned long long>(nrec > npad ? nrec : npad);  // reused by rs5_refine
+        b.pairs = c.take<unsigned long long>((unsigned long long)p.cbins << p.cshift);
+        b.cursor = c.take<unsigned long long>(p.cbins + p.nwin);
     }
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     b.tiles = c.take<uint32_t>(ntiles + 1);
@@ -963,7 +981,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
         if (k == 0) {
             rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, capN);
-            k_rs_count0<SuccT><<<nt, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, p.kbits[0], p.salt[0]);
+            k_rs_count0<SuccT><<<nt < kSMs * 8 ? nt : kSMs * 8, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, p.kbits[0],
+                                                                                   p.salt[0]);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
             k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, b.tiles, b.st, k, p.kbits[k], p.salt[k], 1);
@@ -983,15 +1002,15 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
             k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rid, b.spl[0], b.lvl[1], b.rec_cur,
                                                                     b.rec_sl, b.st, p.kbits[0], p.salt[0],
-                                                                    p.walk_cap, p.maxchunks);
+                                                                    p.walk_cap, p.maxchunks, p.load_mode);
             SG_LAUNCH_CHECK();
             k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.word0,
                                                                         b.spl[0], b.lvl[1], b.st, 0, p.kbits[0],
-                                                                        p.salt[0], p.walk_cap, true);
+                                                                        p.salt[0], p.walk_cap, true, b.rid);
         } else {
             rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
             k_rs_walk<LevelK><<<walk_grid, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
-                                                                 k, p.kbits[k], p.salt[k], p.walk_cap, false);
+                                                                 k, p.kbits[k], p.salt[k], p.walk_cap, false, nullptr);
         }
         rec.end();
         SG_LAUNCH_CHECK();
@@ -1015,24 +1034,22 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     k_rs_expand0<OutT><<<g, 256, 0, s>>>(b.word0, b.IS[1], rank, n, b.st);  // local layouts
     rec.end();
     SG_LAUNCH_CHECK();
-    // scattered layouts: rank the records, bucket them by output window, scatter
-    const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
-    const unsigned long long nfine = npad >> p.fshift;
-    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(uint32_t) * (size_t)(p.cbins + nfine), s));
-    const uint32_t gpart = (uint32_t)((p.maxchunks * REC_CH + BK_TILE - 1) / BK_TILE);
-    rec.begin(K_RS5_PARTITION, 0, gpart, BK_THREADS, n);
-    k_rs_rec_partition<<<gpart, BK_THREADS, 0, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
+    // scattered layouts: rank the records, bucket them by window, scatter
+    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
+    const uint32_t gpart = (uint32_t)((p.maxchunks * REC_CH + RP_TILE - 1) / RP_TILE);
+    rec.begin(K_RS5_PARTITION, 0, gpart, MS_THREADS, n);
+    k_rs_rec_partition<<<gpart, MS_THREADS, 0, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
                                                      p.cshift, p.cbins);
     rec.end();
     SG_LAUNCH_CHECK();
-    const uint32_t gref = (uint32_t)((n + BK_TILE - 1) / BK_TILE);
-    rec.begin(K_RS5_REFINE, 0, gref, BK_THREADS, n);
-    k_rs_rec_refine<<<gref, BK_THREADS, 0, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
+    const uint32_t gref = (uint32_t)((n + RP_TILE - 1) / RP_TILE);
+    rec.begin(K_RS5_REFINE, 0, gref, MS_THREADS, n);
+    k_rs_rec_refine<<<gref, MS_THREADS, 0, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
     rec.end();
     SG_LAUNCH_CHECK();
-    const uint32_t gsc = (uint32_t)((n + (1ull << p.fshift) - 1) >> p.fshift);
-    rec.begin(K_RS5_SCATTER, 0, gsc, BK_THREADS, n);
-    k_rs_rec_scatter<OutT><<<gsc, BK_THREADS, sizeof(OutT) << p.fshift, s>>>(b.rec_sl, rank, n, p.fshift, b.st);
+    rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);
+    k_rs_rec_scatter<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(b.rec_sl, rank, n, p.fshift,
+                                                                                  b.st);
     rec.end();
     SG_LAUNCH_CHECK();
     if (stats) {

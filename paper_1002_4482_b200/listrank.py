@@ -223,31 +223,49 @@ def _draw_splitters_cached(n, r, seed):
     return np.concatenate([[0], picks]).astype(np.int64)
 
 
-def _splitter_set(rank, spl_nodes, n):
+_IDX_CACHE = {}
+
+
+def _device_index(spl_nodes, dev, key):
+    """Device copy of a splitter-node array; cached when `key` names a
+    deterministic draw (n, p, seed)."""
+    if key is None:
+        return torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
+    key = (str(dev),) + tuple(key)
+    t = _IDX_CACHE.get(key)
+    if t is None:
+        if len(_IDX_CACHE) > 32:
+            _IDX_CACHE.clear()
+        t = torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
+        _IDX_CACHE[key] = t
+    return t
+
+
+def _splitter_set(rank, spl_nodes, n, key=None):
     """meta["splitter_set"] from the device ranks: splitter ranks are global
     ranks (listrank.py:355-356); in list order (descending rank) each
     sublist runs to the next splitter, the last one to the tail
-    (listrank.py:252-299)."""
+    (listrank.py:252-299).  One device sort, one D2H copy."""
     dev = rank.device
     r = len(spl_nodes)
-    idx = torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
+    idx = _device_index(spl_nodes, dev, key)
     srank = rank.index_select(0, idx).to(torch.int64)
-    order = torch.argsort(srank, descending=True)
-    sr_sorted = srank[order]
+    sr_sorted, order = torch.sort(srank, descending=True)
+    res = torch.empty((3, r), dtype=torch.int64, device=dev)   # rank, sublist length, reduced successor
+    res[0] = srank
     ln_sorted = torch.empty_like(sr_sorted)
     ln_sorted[:-1] = sr_sorted[:-1] - sr_sorted[1:]
     ln_sorted[-1] = sr_sorted[-1] + 1
     nx_sorted = torch.empty_like(order)
     nx_sorted[:-1] = order[1:]
     nx_sorted[-1] = order[-1]
-    sub_len = torch.empty_like(ln_sorted)
-    sub_len[order] = ln_sorted
-    succ = torch.empty_like(order)
-    succ[order] = nx_sorted
+    res[1].index_copy_(0, order, ln_sorted)
+    res[2].index_copy_(0, order, nx_sorted)
+    host = res.cpu().numpy()
     out = SplitterSet(r, np.ascontiguousarray(spl_nodes, dtype=np.int64))
-    out.sublist_len = sub_len.cpu().numpy()
-    out.splitter_succ = succ.cpu().numpy()
-    out.splitter_rank = srank.cpu().numpy()
+    out.splitter_rank = host[0]
+    out.sublist_len = host[1]
+    out.splitter_succ = host[2]
     return out
 
 
@@ -273,7 +291,7 @@ def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_su
         spl_nodes = node_at[:: n // p].cpu().numpy()
     else:
         spl_nodes = _draw_splitters(n, p, seed)
-    splitters = _splitter_set(rank, spl_nodes, n)
+    splitters = _splitter_set(rank, spl_nodes, n, key=None if even else (n, p, int(seed)))
     stats.meta.update(n=n, p=p, packing=packing.value, splitter_set=splitters,
                       max_sublist=int(splitters.sublist_len.max()),
                       levels=int(st.levels), level_size=[int(st.level_size[k]) for k in range(st.levels + 1)],

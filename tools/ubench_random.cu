@@ -31,6 +31,32 @@ __global__ void chase(const unsigned long long* a, uint32_t mask, int iters, uns
     if (cur == 0xFFFFFFFF) *sink = cur;
 }
 
+// dependent chase through L2 only (ld.global.cg) / without L1 allocation
+__global__ void chase_cg(const unsigned long long* a, uint32_t mask, int iters, unsigned long long* sink) {
+    uint32_t cur = mix(blockIdx.x * blockDim.x + threadIdx.x) & mask;
+    for (int k = 0; k < iters; ++k) cur = (uint32_t)__ldcg(a + cur) & mask;
+    if (cur == 0xFFFFFFFF) *sink = cur;
+}
+__global__ void chase_na(const unsigned long long* a, uint32_t mask, int iters, unsigned long long* sink) {
+    uint32_t cur = mix(blockIdx.x * blockDim.x + threadIdx.x) & mask;
+    for (int k = 0; k < iters; ++k) {
+        unsigned long long v;
+        asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(a + cur));
+        cur = (uint32_t)v & mask;
+    }
+    if (cur == 0xFFFFFFFF) *sink = cur;
+}
+__global__ void chase32_cg(const uint32_t* a, uint32_t mask, int iters, unsigned long long* sink) {
+    uint32_t cur = mix(blockIdx.x * blockDim.x + threadIdx.x) & mask;
+    for (int k = 0; k < iters; ++k) cur = __ldcg(a + cur) & mask;
+    if (cur == 0xFFFFFFFF) *sink = cur;
+}
+__global__ void chase32(const uint32_t* a, uint32_t mask, int iters, unsigned long long* sink) {
+    uint32_t cur = mix(blockIdx.x * blockDim.x + threadIdx.x) & mask;
+    for (int k = 0; k < iters; ++k) cur = a[cur] & mask;
+    if (cur == 0xFFFFFFFF) *sink = cur;
+}
+
 // chase + write previous node's word (the in-place walk pattern)
 __global__ void chase_wr(unsigned long long* a, uint32_t mask, int iters, unsigned long long* sink) {
     uint32_t cur = mix(blockIdx.x * blockDim.x + threadIdx.x) & mask, prev = cur;
@@ -59,6 +85,11 @@ __global__ void wr(unsigned long long* a, uint32_t mask, int iters) {
     for (int k = 0; k < iters; ++k) a[mix(t * 7919u + k * 104729u) & mask] = k;
 }
 
+__global__ void init32(uint32_t* a, uint32_t mask) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= mask; i += gridDim.x * blockDim.x)
+        a[i] = mix(i * 2654435761u + 7) & mask;
+}
+
 __global__ void init(unsigned long long* a, uint32_t mask) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= mask; i += gridDim.x * blockDim.x)
         a[i] = mix(i * 2654435761u + 1) & mask;
@@ -72,6 +103,7 @@ int main() {
     cudaMalloc(&w, (size_t)n * 8);
     cudaMalloc(&sink, 8);
     init<<<148 * 8, 256>>>(a, mask);
+    init32<<<148 * 8, 256>>>((uint32_t*)w, mask);
     cudaDeviceSynchronize();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -93,6 +125,10 @@ int main() {
     run("read  MLP4", [&] { rd<4><<<grid, blk>>>(a, mask, it, sink); }, (double)T * it * 4);
     run("read  MLP8", [&] { rd<8><<<grid, blk>>>(a, mask, it / 2, sink); }, (double)T * it * 4);
     run("chase (dependent)", [&] { chase<<<grid, blk>>>(a, mask, it * 2, sink); }, (double)T * it * 2);
+    run("chase ld.cg", [&] { chase_cg<<<grid, blk>>>(a, mask, it * 2, sink); }, (double)T * it * 2);
+    run("chase ld.L1::no_allocate", [&] { chase_na<<<grid, blk>>>(a, mask, it * 2, sink); }, (double)T * it * 2);
+    run("chase u32 (1 GiB)", [&] { chase32<<<grid, blk>>>((const uint32_t*)w, mask, it * 2, sink); }, (double)T * it * 2);
+    run("chase u32 ld.cg (1 GiB)", [&] { chase32_cg<<<grid, blk>>>((const uint32_t*)w, mask, it * 2, sink); }, (double)T * it * 2);
     run("chase + write same word", [&] { chase_wr<<<grid, blk>>>(a, mask, it * 2, sink); }, (double)T * it * 2);
     run("chase + write other array", [&] { chase_wr2<<<grid, blk>>>(a, w, mask, it * 2, sink); }, (double)T * it * 2);
     run("write random 8B", [&] { wr<<<grid, blk>>>(w, mask, it * 4); }, (double)T * it * 4);
