@@ -131,22 +131,26 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned l
         i += rng[0];
         m = rng[1];
     }
-    // two edges per iteration: four independent parent loads in flight
-    for (; i + stride < m; i += 2 * stride) {
-        unsigned long long u0, v0, u1, v1;
-        edges.load(i, u0, v0);
-        edges.load(i + stride, u1, v1);
-        bool ok0 = true, ok1 = true;
-        if (kValidate) {
-            ok0 = edge_ok(u0, v0, n, row0 + i, flags);
-            ok1 = edge_ok(u1, v1, n, row0 + i + stride, flags);
+    // HU edges per iteration: 2*HU independent parent loads in flight
+    constexpr int HU = 4;
+    for (; i + (HU - 1) * stride < m; i += HU * stride) {
+        unsigned long long u[HU], v[HU];
+        bool ok[HU];
+#pragma unroll
+        for (int k = 0; k < HU; ++k) edges.load(i + k * stride, u[k], v[k]);
+#pragma unroll
+        for (int k = 0; k < HU; ++k) ok[k] = !kValidate || edge_ok(u[k], v[k], n, row0 + i + k * stride, flags);
+        uint32_t pu[HU], pv[HU];
+#pragma unroll
+        for (int k = 0; k < HU; ++k) {
+            pu[k] = ok[k] ? ld_parent(D + u[k]) : 0;
+            pv[k] = ok[k] ? ld_parent(D + v[k]) : 0;
         }
-        const uint32_t pu0 = ok0 ? ld_parent(D + u0) : 0, pv0 = ok0 ? ld_parent(D + v0) : 0;
-        const uint32_t pu1 = ok1 ? ld_parent(D + u1) : 0, pv1 = ok1 ? ld_parent(D + v1) : 0;
-        if (ok0 && pu0 != pv0) any |= unite(D, (uint32_t)u0, pu0, (uint32_t)v0, pv0);
-        if (ok1 && pu1 != pv1) any |= unite(D, (uint32_t)u1, pu1, (uint32_t)v1, pv1);
+#pragma unroll
+        for (int k = 0; k < HU; ++k)
+            if (ok[k] && pu[k] != pv[k]) any |= unite(D, (uint32_t)u[k], pu[k], (uint32_t)v[k], pv[k]);
     }
-    if (i < m) {
+    for (; i < m; i += stride) {
         unsigned long long u, v;
         edges.load(i, u, v);
         if (!kValidate || edge_ok(u, v, n, row0 + i, flags)) {
@@ -297,22 +301,19 @@ __global__ void k_cc_part_offsets(const unsigned long long* __restrict__ totals,
     }
 }
 
-// Scatter every valid edge into its partition (block multisplit by ballots,
+// Scatter every valid edge into its partition (block multisplit,
 // sg_msplit.cuh; one global atomic per partition per 4096-edge tile).
-constexpr int PS_ITEMS = 16;
-constexpr int PS_TILE = MS_THREADS * PS_ITEMS;
-
 template <class E>
-__global__ void __launch_bounds__(MS_THREADS) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
+__global__ void __launch_bounds__(MS_THREADS, 4) k_cc_part_scatter(E edges, unsigned long long m, unsigned long long n,
                                                                 uint32_t shift, int P,
                                                                 const unsigned long long* __restrict__ off_part,
                                                                 unsigned long long* __restrict__ cursor,
                                                                 uint2* __restrict__ out) {
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * PS_TILE;
-    if (e0 >= m) return;
+    extern __shared__ __align__(16) unsigned char ms_raw[];
+    MsSmem sm = MsSmem::carve(ms_raw, (uint32_t)P);
     int nbits = 0;
     while ((1 << nbits) < P) ++nbits;
-    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool) -> bool {
+    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b) -> bool {
         uint2 uv;
         const int p = part_of(edges, e, m, n, shift, nullptr, false, uv);
         if (p < 0) return false;
@@ -320,15 +321,21 @@ __global__ void __launch_bounds__(MS_THREADS) k_cc_part_scatter(E edges, unsigne
         b = (uint32_t)p;
         return true;
     };
+    auto bin_of = [&](unsigned long long pr) {
+        const uint32_t u = (uint32_t)pr, v = (uint32_t)(pr >> 32);
+        return (u > v ? u : v) >> shift;
+    };
     auto slot = [&](uint32_t b) { return make_ulonglong2(off_part[b], off_part[b + 1] - off_part[b]); };
-    ms_tile<PS_ITEMS>(get, slot, e0, min(e0 + PS_TILE, m), (uint32_t)P, nbits, cursor,
-                      reinterpret_cast<unsigned long long*>(out));
+    for (unsigned long long e0 = (unsigned long long)blockIdx.x * MS_TILE; e0 < m;
+         e0 += (unsigned long long)gridDim.x * MS_TILE)
+        ms_tile(get, bin_of, slot, e0, min(e0 + MS_TILE, m), (uint32_t)P, nbits, cursor,
+                reinterpret_cast<unsigned long long*>(out), sm);
 }
 
 // ---------------------------------------------------------------------------
 // host side
 
-static uint32_t hook_grid(unsigned long long m) { return grid_for(m, HOOK_THREADS, 2, kSMs * 8); }
+static uint32_t hook_grid(unsigned long long m) { return grid_for(m, HOOK_THREADS, 4, kSMs * 8); }
 static uint32_t vtx_grid(unsigned long long n) { return grid_for(n, COMP_THREADS, 1, kSMs * 8); }
 
 template <class E>
@@ -404,8 +411,11 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
     SG_LAUNCH_CHECK();
     k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
-    const uint32_t ns = (uint32_t)((m + PS_TILE - 1) / PS_TILE);
-    k_cc_part_scatter<E><<<ns, MS_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
+    const size_t smem = MsSmem::bytes((uint32_t)p.parts);
+    SG_CUDA(cudaFuncSetAttribute(k_cc_part_scatter<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned long long ntile = (m + MS_TILE - 1) / MS_TILE;
+    const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * 4 ? ntile : kSMs * 4);
+    k_cc_part_scatter<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
     SG_LAUNCH_CHECK();
     return SG_OK;
 }

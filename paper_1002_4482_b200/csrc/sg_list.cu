@@ -593,65 +593,69 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
 // Both bucketing passes are ballot multisplits (sg_msplit.cuh).  Invalid
 // inputs can overfill a window; such writes are dropped (the call reports
 // the list invalid anyway).
-constexpr int RP_ITEMS = 64;
-constexpr int RP_TILE = MS_THREADS * RP_ITEMS;
-
 __device__ __forceinline__ int ceil_log2(uint32_t x) {
     int b = 0;
     while ((1u << b) < x) ++b;
     return b;
 }
 
-__global__ void __launch_bounds__(MS_THREADS) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
+__global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
                                                                  const unsigned long long* __restrict__ rec_sl,
                                                                  const uint32_t* __restrict__ IS1,
                                                                  unsigned long long* __restrict__ cursor,
                                                                  unsigned long long* __restrict__ pairs,
                                                                  ListStatus* st, uint32_t cshift, uint32_t cbins) {
     if (layout_local(st) || st->overflow) return;
+    extern __shared__ __align__(16) unsigned char ms_raw[];
+    MsSmem sm = MsSmem::carve(ms_raw, cbins);
     const unsigned long long total = st->chunks * REC_CH;
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * RP_TILE;
-    if (e0 >= total) return;
     const unsigned long long R1 = st->R[1];
-    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool want) -> bool {
-        const uint32_t c = rec_cur[e];
+    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b) -> bool {
+        const uint32_t c = __ldcs(rec_cur + e);
+        const unsigned long long sl = __ldcs(rec_sl + e);
         if (c == NIL) return false;
         b = c >> cshift;
-        if (want) {  // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
-            const unsigned long long sl = rec_sl[e];
-            const unsigned long long o = sl >> 32;
-            const uint32_t rk = o < R1 ? __ldg(IS1 + o) - (uint32_t)sl - 1u : 0u;
-            pr = ((unsigned long long)c << 32) | rk;
-        }
+        const unsigned long long o = sl >> 32;  // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
+        const uint32_t rk = o < R1 ? __ldg(IS1 + o) - (uint32_t)sl - 1u : 0u;
+        pr = ((unsigned long long)c << 32) | rk;
         return true;
     };
+    auto bin_of = [&](unsigned long long pr) { return (uint32_t)((pr >> 32) >> cshift); };
     auto slot = [&](uint32_t b) { return make_ulonglong2((unsigned long long)b << cshift, 1ull << cshift); };
-    if (ms_tile<RP_ITEMS>(get, slot, e0, min(e0 + RP_TILE, total), cbins, ceil_log2(cbins), cursor, pairs))
-        st->bad = 1;
+    bool over = false;
+    const int nbits = ceil_log2(cbins);
+    for (unsigned long long e0 = (unsigned long long)blockIdx.x * MS_TILE; e0 < total;
+         e0 += (unsigned long long)gridDim.x * MS_TILE)
+        over |= ms_tile(get, bin_of, slot, e0, min(e0 + MS_TILE, total), cbins, nbits, cursor, pairs, sm);
+    if (over) st->bad = 1;
 }
 
-__global__ void __launch_bounds__(MS_THREADS) k_rs_rec_refine(const unsigned long long* __restrict__ in,
+__global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_refine(const unsigned long long* __restrict__ in,
                                                               unsigned long long* __restrict__ cursor,
                                                               unsigned long long* __restrict__ out, ListStatus* st,
                                                               unsigned long long n, uint32_t cshift, uint32_t fshift) {
     if (layout_local(st) || st->overflow) return;
-    // tiles never straddle a coarse window (2^cshift is a multiple of RP_TILE)
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * RP_TILE;
-    if (e0 >= n) return;
-    const unsigned long long c = e0 >> cshift;
     const uint32_t fb = 1u << (cshift - fshift);
-    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b, bool) -> bool {
-        pr = in[e];
-        const unsigned long long cur = pr >> 32;
-        if ((cur >> cshift) != c) return false;  // only for invalid inputs
-        b = (uint32_t)((cur >> fshift) & (fb - 1));
-        return true;
-    };
-    auto slot = [&](uint32_t b) {
-        return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift);
-    };
-    if (ms_tile<RP_ITEMS>(get, slot, e0, min(e0 + RP_TILE, n), fb, (int)(cshift - fshift), cursor + c * fb, out))
-        st->bad = 1;
+    extern __shared__ __align__(16) unsigned char ms_raw[];
+    MsSmem sm = MsSmem::carve(ms_raw, fb);
+    bool over = false;
+    // tiles never straddle a coarse window (2^cshift is a multiple of MS_TILE)
+    for (unsigned long long e0 = (unsigned long long)blockIdx.x * MS_TILE; e0 < n;
+         e0 += (unsigned long long)gridDim.x * MS_TILE) {
+        const unsigned long long c = e0 >> cshift;
+        auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b) -> bool {
+            pr = __ldcs(in + e);
+            const unsigned long long cur = pr >> 32;
+            if ((cur >> cshift) != c) return false;  // only for invalid inputs
+            b = (uint32_t)((cur >> fshift) & (fb - 1));
+            return true;
+        };
+        auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
+        auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
+        over |= ms_tile(get, bin_of, slot, e0, min(e0 + MS_TILE, n), fb, (int)(cshift - fshift), cursor + c * fb,
+                        out, sm);
+    }
+    if (over) st->bad = 1;
 }
 
 // one CTA per fine window: scatter its pairs into shared memory, then store
@@ -818,9 +822,9 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     // windows: few enough bins for one multisplit, >= 64 pairs per bin per tile
     p.fshift = out_bytes >= 8 ? 12 : 13;
     uint32_t cs = p.fshift + 1;
-    if (cs < 14) cs = 14;  // 2^cshift must be a multiple of RP_TILE
+    if (cs < 13) cs = 13;  // 2^cshift must be a multiple of MS_TILE
     while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
-    while (cs - p.fshift > 10) ++p.fshift;  // <= MS_MAXB fine windows per coarse window
+    while (cs - p.fshift > 8) ++p.fshift;  // <= 256 fine windows per coarse window
     p.cshift = cs;
     p.cbins = (uint32_t)((n + (1ull << cs) - 1) >> cs);
     p.nwin = (unsigned long long)p.cbins << (cs - p.fshift);
@@ -1036,15 +1040,18 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     SG_LAUNCH_CHECK();
     // scattered layouts: rank the records, bucket them by window, scatter
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
-    const uint32_t gpart = (uint32_t)((p.maxchunks * REC_CH + RP_TILE - 1) / RP_TILE);
-    rec.begin(K_RS5_PARTITION, 0, gpart, MS_THREADS, n);
-    k_rs_rec_partition<<<gpart, MS_THREADS, 0, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
-                                                     p.cshift, p.cbins);
+    const uint32_t persist = kSMs * 4;
+    const size_t sm_part = MsSmem::bytes(p.cbins), sm_ref = MsSmem::bytes(1u << (p.cshift - p.fshift));
+    SG_CUDA(cudaFuncSetAttribute(k_rs_rec_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part));
+    SG_CUDA(cudaFuncSetAttribute(k_rs_rec_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref));
+    rec.begin(K_RS5_PARTITION, 0, persist, MS_THREADS, n);
+    k_rs_rec_partition<<<persist, MS_THREADS, sm_part, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
+                                                            p.cshift, p.cbins);
     rec.end();
     SG_LAUNCH_CHECK();
-    const uint32_t gref = (uint32_t)((n + RP_TILE - 1) / RP_TILE);
-    rec.begin(K_RS5_REFINE, 0, gref, MS_THREADS, n);
-    k_rs_rec_refine<<<gref, MS_THREADS, 0, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
+    rec.begin(K_RS5_REFINE, 0, persist, MS_THREADS, n);
+    k_rs_rec_refine<<<persist, MS_THREADS, sm_ref, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
+                                                        p.fshift);
     rec.end();
     SG_LAUNCH_CHECK();
     rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);

@@ -48,3 +48,15 @@ print("rs_rank API      ms:", round(timed(lambda: g.rs_rank(sl, 16384)), 3))
 out = g.rs_rank(sl, 16384)[0]
 print("splitter meta    ms:", round(timed(lambda: listrank._splitter_set(out, listrank._draw_splitters(n, 16384, 0), n)), 3))
 print("per kernel:", {k: round(x.ms, 4) for k, x in g.rs_rank(sl, 16384)[1].per_kernel().items()})
+
+# PCIe: pinned H2D / D2H of the e2e payloads
+host = sl.succ.to(torch.int64).cpu().pin_memory()
+dst = torch.empty_like(host, device=dev)
+print("H2D 8n pinned    ms:", round(timed(lambda: dst.copy_(host, non_blocking=True)), 3), "for", host.numel() * 8 / 2**20, "MiB")
+hb = torch.empty(host.shape, dtype=torch.int64, pin_memory=True)
+print("D2H 8n pinned    ms:", round(timed(lambda: hb.copy_(dst, non_blocking=True)), 3))
+hs = g.SuccessorList(host)
+print("e2e API (pinned) ms:", round(timed(lambda: g.rs_rank(hs, 16384), reps=3), 3))
+import numpy as np
+hn = g.SuccessorList(host.numpy())
+print("e2e API (numpy)  ms:", round(timed(lambda: g.rs_rank(hn, 16384), reps=3), 3))
