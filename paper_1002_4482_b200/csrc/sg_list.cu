@@ -792,6 +792,7 @@ struct RsPlan {
     uint32_t cbins = 1;                          // number of coarse windows
     unsigned long long nwin = 1;                 // number of fine windows
     uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
+    bool rec_ok = true;                          // fine windows fit shared memory
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
@@ -825,6 +826,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     if (cs < 13) cs = 13;  // 2^cshift must be a multiple of MS_TILE
     while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
     while (cs - p.fshift > 8) ++p.fshift;  // <= 256 fine windows per coarse window
+    p.rec_ok = ((size_t)out_bytes << p.fshift) <= (200u << 10);  // false only for n > ~2^31
     p.cshift = cs;
     p.cbins = (uint32_t)((n + (1ull << cs) - 1) >> cs);
     p.nwin = (unsigned long long)p.cbins << (cs - p.fshift);
@@ -1128,6 +1130,18 @@ static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed,
         for (int k = 0; k < SG_MAX_LEVELS; ++k) stats->level_size[k] = 0;
     }
     Recorder rec(stats, s);
+    if (p.levels > 0 && !p.rec_ok) {
+        // output windows would not fit shared memory (n > ~2^31): pointer jumping
+        if (stats) stats->fallback = 1;
+        int rc = wyllie_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, SG_WY_MULTI_KERNEL, b.st, b.word0, s,
+                                         rec, stats);
+        if (rc != SG_OK) return rc;
+        SG_CUDA(rec.finish());
+        ListStatus h;
+        rc = read_status(b.st, h, s);
+        if (rc != SG_OK) return rc;
+        return classify(h, n, viol);
+    }
     int rc = rs_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, p, b, s, rec, stats);
     if (rc != SG_OK) return rc;
     SG_CUDA(rec.finish());

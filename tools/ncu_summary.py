@@ -27,7 +27,9 @@ KEYS = [
     "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
 ]
 STALL = "smsp__average_warp_latency_issue_stalled_"
-NAME_MAP = {"k_rs_walk0": "rs3_walk", "k_rs_walk<Level0": "rs3_walk", "k_rs_walk<LevelK": "rs4_walk",
+NAME_MAP = {"k_rs_walk_stage": "rs3_walk", "k_rs_walk_rec": "rs3_walk", "k_rs_walk<sg::Level0": "rs3_walk",
+            "k_rs_walk<Level0": "rs3_walk", "k_rs_walk<sg::LevelK": "rs4_walk", "k_rs_walk<LevelK": "rs4_walk",
+            "k_rs_rec_refine": "rs5_refine", "k_rs_rec_scatter": "rs5_scatter", "k_rs_rec_partition": "rs5_partition",
             "k_rs_expand0": "rs5_expand", "k_rs_count0": "rs1_validate", "k_cc_hook_uf": "cc_hook_uf",
             "k_cc_hook_sv": "cc_hook_sv", "k_cc_part_scatter": "cc_partition_scatter",
             "k_cc_part_count": "cc_partition_count", "k_wy_jump": "wy_jump", "k_cc_compress": "cc_shortcut"}
@@ -56,6 +58,7 @@ def main():
     out = [f"# ncu --set full summary: {os.path.basename(rep)} ({workload})", ""]
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    seen = set()
     for r in data:
         d = dict(zip(hdr, r))
         kname = d.get("Kernel Name", "?")
@@ -70,7 +73,12 @@ def main():
             out.append(f"  {'DRAM traffic (read+write)':62s} {rd + wr:16.0f} byte")
             if t:
                 out.append(f"  {'DRAM traffic / duration':62s} {(rd + wr) / t / 1e9:16.1f} GB/s")
-            traffic.setdefault(workload, {})[short(kname)] = int(rd + wr)
+            # several captured launches of one kernel (e.g. one hook launch per
+            # edge window) add up to one ExecStats launch record
+            w = traffic.setdefault(workload, {})
+            key = short(kname)
+            w[key] = int(rd + wr) + (w.get(key, 0) if key in seen else 0)
+            seen.add(key)
         stalls = []
         for k in hdr:
             if k.startswith(STALL) and k.endswith(".ratio"):
