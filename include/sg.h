@@ -100,7 +100,7 @@ typedef struct sg_stats {
     uint64_t vertex_sweeps;   /* CC: passes over the vertex array          */
     uint64_t level_size[SG_MAX_LEVELS];   /* nodes per ruling-set level    */
     uint32_t n_roots;         /* entries in roots_per_round               */
-    uint32_t pad;
+    uint32_t list_path;       /* rs: 0 ruling-set walk, 1 tile contraction */
     uint64_t roots_per_round[SG_MAX_ROUNDS];
     float total_ms;           /* event time of the whole device pipeline  */
     uint32_t pad2;

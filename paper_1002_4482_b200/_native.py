@@ -51,7 +51,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("n_launches", ctypes.c_uint32), ("rounds", ctypes.c_uint32), ("levels", ctypes.c_uint32),
                 ("fallback", ctypes.c_uint32), ("edge_sweeps", ctypes.c_uint64),
                 ("vertex_sweeps", ctypes.c_uint64), ("level_size", ctypes.c_uint64 * SG_MAX_LEVELS),
-                ("n_roots", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("n_roots", ctypes.c_uint32), ("list_path", ctypes.c_uint32),
                 ("roots_per_round", ctypes.c_uint64 * SG_MAX_ROUNDS), ("total_ms", ctypes.c_float),
                 ("pad2", ctypes.c_uint32), ("launch", Launch * SG_MAX_LAUNCHES)]
 

@@ -52,6 +52,8 @@ enum KernelId : int {
     K_RS5_PARTITION,  // rs5_partition: rank the walk records, split by output window
     K_RS5_SCATTER,    // rs5_scatter:   fine window -> shared memory -> coalesced ranks
     K_RS5_REFINE,     // rs5_refine:    coarse window -> fine windows
+    K_RS_CONTRACT,    // rs3_contract:  tile contraction of a local layout (segments in shared memory)
+    K_RS_CONTRACT_LINK,  // rs3_link:   contracted-list successors
     K_COUNT_
 };
 
@@ -64,7 +66,7 @@ struct ListStatus {
     unsigned long long head_sum;    // final inclusive suffix sum at the head
     unsigned long long head_ok;     // 1: the head's pointer reached the tail
     unsigned long long bad;         // walk saw an out-of-range successor
-    unsigned long long local;       // successors within 16 slots of their node (layout locality)
+    unsigned long long local;       // 1: local layout, ranked by tile contraction
     unsigned long long R[SG_MAX_LEVELS + 1];      // nodes per level (R[0] = n)
     unsigned long long qhead[SG_MAX_LEVELS + 1];  // walk work-queue heads
     unsigned long long chunks;      // record chunks handed out by the level-0 record walk

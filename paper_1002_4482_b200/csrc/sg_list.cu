@@ -24,10 +24,13 @@
 // core.validate_list (core.py:148-167).  A walk that exceeds the hop cap
 // (a cycle without rulers, or a pathological layout) makes the host re-run
 // the list with Wyllie, which terminates on any input.
+#include <cub/block/block_load.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_store.cuh>
 
 #include <stdlib.h>
+#include <type_traits>
 #include <string.h>
 
 #include "sg_internal.cuh"
@@ -273,69 +276,167 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count(const SuccT* __restri
 }
 
 // level 0: validate the successors (range, self-loops), count rulers per tile
-// and measure layout locality (successor within 16 slots)
-template <class SuccT>
+// and in-tile chain ends per tile (nodes whose successor leaves the tile, or
+// the tail): the segment count of the tile contraction below.  Full tiles
+// are read with 16-B vector loads; node ids are 32-bit (n < 2^32 - 1).
+template <class SuccT, bool kVec>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restrict__ succ,
-                                                            uint32_t* __restrict__ tile_cnt, ListStatus* st,
+                                                            uint32_t* __restrict__ tile_cnt,
+                                                            uint32_t* __restrict__ tile_end, ListStatus* st,
                                                             uint32_t kbits, uint32_t salt) {
+    constexpr int VEC = 16 / sizeof(SuccT);  // ids per 16-B load
+    constexpr int NLD = TILE_ITEMS / VEC;    // loads per thread per tile
+    typedef typename std::conditional<sizeof(SuccT) == 4, uint4, ulonglong2>::type V;
     typedef cub::BlockReduce<uint32_t, TILE_THREADS> BR;
     __shared__ typename BR::TempStorage tmp;
     const unsigned long long N = st->R[0];
     const unsigned long long ntiles = (N + TILE - 1) / TILE;
-    uint32_t loc = 0;
     // persistent blocks walk the tiles; all loads of a tile are issued before
     // the (rare) atomics of the self-loop / range census
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const unsigned long long base = tile * TILE;
-        SuccT v[TILE_ITEMS];
+        const bool full = kVec && base + TILE <= N;
+        SuccT e[TILE_ITEMS];
+        if (full) {
+            const V* src = reinterpret_cast<const V*>(succ + base);
 #pragma unroll
-        for (int j = 0; j < TILE_ITEMS; ++j) {
-            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
-            v[j] = i < N ? __ldcs(succ + i) : SuccT(0);
-        }
-        uint32_t cnt = 0;
+            for (int j = 0; j < NLD; ++j) {
+                const V v = __ldcs(src + j * TILE_THREADS + threadIdx.x);
 #pragma unroll
-        for (int j = 0; j < TILE_ITEMS; ++j) {
-            const unsigned long long i = base + (unsigned long long)j * TILE_THREADS + threadIdx.x;
-            if (i < N) {
-                const unsigned long long x = as_index<SuccT>(v[j]);
-                if (x >= N || x == i) note_succ(st, i, x, N);
-                cnt += is_ruler((uint32_t)i, kbits, salt) ? 1u : 0u;
-                loc += (x + 16 > i && x < i + 16) ? 1u : 0u;
+                for (int c = 0; c < VEC; ++c) e[j * VEC + c] = reinterpret_cast<const SuccT*>(&v)[c];
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NLD; ++j)
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) {
+                    const unsigned long long i = base + (unsigned long long)(j * TILE_THREADS + threadIdx.x) * VEC + c;
+                    e[j * VEC + c] = i < N ? __ldcs(succ + i) : SuccT(0);
+                }
         }
-        const uint32_t tot = BR(tmp).Sum(cnt);
-        if (threadIdx.x == 0) tile_cnt[tile] = tot;
+        uint32_t packed = 0;  // rulers << 16 | ends
+        const uint32_t b32 = (uint32_t)base;
+#pragma unroll
+        for (int j = 0; j < NLD; ++j)
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+                const uint32_t l = (j * TILE_THREADS + threadIdx.x) * VEC + c;
+                if (full || base + l < N) {
+                    const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
+                    const uint32_t i = b32 + l, x = (uint32_t)x64;
+                    const bool oor = x64 >= N, self = !oor && x == i;
+                    if (oor | self) note_succ(st, i, x64, N);
+                    packed += (is_ruler(i, kbits, salt) ? 0x10000u : 0u) + ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
+                }
+            }
+        const uint32_t tot = BR(tmp).Sum(packed);
+        if (threadIdx.x == 0) {
+            tile_cnt[tile] = tot >> 16;
+            tile_end[tile] = tot & 0xFFFFu;
+        }
         __syncthreads();
     }
-    const uint32_t ltot = BR(tmp).Sum(loc);
-    if (threadIdx.x == 0 && ltot) atomicAdd(&st->local, (unsigned long long)ltot);
 }
 
-// Lists laid out mostly in chain order (successor within 16 slots) walk
-// faster reading the input and writing the words separately: each lane
-// streams its own lines through L1.  Scattered lists use the in-place walk.
-__device__ __forceinline__ bool layout_local(const ListStatus* st) { return st->local * 2 > st->R[0]; }
+// Lists whose chains mostly stay inside their 4096-node tile (ordered or
+// locally shuffled layouts) are contracted tile by tile in shared memory
+// (k_rs_contract); scattered lists take the ruling-set record walk.
+__device__ __forceinline__ bool layout_local(const ListStatus* st) { return st->local != 0; }
+
+// Single-CTA exclusive scan of per-tile counts, in place, chunk by chunk
+// with coalesced (transposed) loads and stores.  Returns the total.
+constexpr int SCAN_THREADS = 512;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
+
+struct ScanSmem {
+    typedef cub::BlockLoad<uint32_t, SCAN_THREADS, SCAN_ITEMS, cub::BLOCK_LOAD_TRANSPOSE> BL;
+    typedef cub::BlockStore<uint32_t, SCAN_THREADS, SCAN_ITEMS, cub::BLOCK_STORE_TRANSPOSE> BSt;
+    typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BSc;
+    typedef cub::BlockReduce<unsigned long long, SCAN_THREADS> BR;
+    union {
+        typename BL::TempStorage load;
+        typename BSt::TempStorage store;
+        typename BSc::TempStorage scan;
+        typename BR::TempStorage red;
+    };
+};
+
+__device__ unsigned long long cta_sum(const uint32_t* __restrict__ a, unsigned long long cnt, ScanSmem& sm) {
+    unsigned long long acc = 0;
+    for (unsigned long long c0 = 0; c0 < cnt; c0 += SCAN_CHUNK) {
+        const int valid = (int)min((unsigned long long)SCAN_CHUNK, cnt - c0);
+        uint32_t v[SCAN_ITEMS];
+        ScanSmem::BL(sm.load).Load(a + c0, v, valid, 0u);
+        __syncthreads();
+        unsigned long long x = 0;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) x += v[j];
+        acc += ScanSmem::BR(sm.red).Sum(x);
+        __syncthreads();
+    }
+    return acc;  // valid in thread 0
+}
+
+__device__ unsigned long long cta_exclusive_scan(const uint32_t* src, uint32_t* dst, unsigned long long cnt,
+                                                 ScanSmem& sm) {
+    unsigned long long carry = 0;
+    for (unsigned long long c0 = 0; c0 < cnt; c0 += SCAN_CHUNK) {
+        const int valid = (int)min((unsigned long long)SCAN_CHUNK, cnt - c0);
+        uint32_t v[SCAN_ITEMS];
+        ScanSmem::BL(sm.load).Load(src + c0, v, valid, 0u);
+        __syncthreads();
+        unsigned long long x = 0;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) x += v[j];
+        unsigned long long pre, tot;
+        ScanSmem::BSc(sm.scan).ExclusiveSum(x, pre, tot);
+        __syncthreads();
+        pre += carry;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            const uint32_t c = v[j];
+            v[j] = (uint32_t)pre;
+            pre += c;
+        }
+        ScanSmem::BSt(sm.store).Store(dst + c0, v, valid);
+        __syncthreads();
+        carry += tot;
+    }
+    return carry;
+}
+
+// level 0: pick the path and scan its tile counts.  Contraction when the
+// in-tile segments are few (>= 16 nodes per segment on average) and fit the
+// level-1 buffers; otherwise the hashed ruling set.
+__global__ void __launch_bounds__(SCAN_THREADS) k_rs_scan0(uint32_t* tile_cnt, const uint32_t* __restrict__ tile_end,
+                                                           ListStatus* st, unsigned long long cap, int allow_contract) {
+    __shared__ ScanSmem sm;
+    __shared__ int s_contract;
+    const unsigned long long N = st->R[0];
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
+    const unsigned long long segs = cta_sum(tile_end, ntiles, sm);
+    if (threadIdx.x == 0) s_contract = allow_contract && segs <= cap && segs * 16 <= N;
+    __syncthreads();
+    const int contract = s_contract;
+    unsigned long long total = cta_exclusive_scan(contract ? tile_end : tile_cnt, tile_cnt, ntiles, sm);
+    if (threadIdx.x == 0) {
+        if (total > cap) {
+            st->overflow = 1;
+            total = cap;
+        }
+        st->R[1] = total;
+        st->local = contract ? 1ull : 0ull;
+    }
+}
 
 // single CTA exclusive scan of the tile counts of `level`
-__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* tile_cnt, ListStatus* st, int level,
-                                                  unsigned long long cap) {
+__global__ void __launch_bounds__(SCAN_THREADS) k_rs_scan(uint32_t* tile_cnt, ListStatus* st, int level,
+                                                          unsigned long long cap) {
+    __shared__ ScanSmem sm;
     const unsigned long long N = st->R[level];
     const unsigned long long ntiles = (N + TILE - 1) / TILE;
-    const unsigned long long per = (ntiles + 1023) / 1024;
-    const unsigned long long a = threadIdx.x * per;
-    const unsigned long long b = min(a + per, ntiles);
-    unsigned long long sum = 0;
-    for (unsigned long long t = a; t < b; ++t) sum += tile_cnt[t];
-    typedef cub::BlockScan<unsigned long long, 1024> BS;
-    __shared__ typename BS::TempStorage tmp;
-    unsigned long long off, total;
-    BS(tmp).ExclusiveSum(sum, off, total);
-    for (unsigned long long t = a; t < b; ++t) {
-        const uint32_t c = tile_cnt[t];
-        tile_cnt[t] = (uint32_t)off;
-        off += c;
-    }
+    unsigned long long total = cta_exclusive_scan(tile_cnt, tile_cnt, ntiles, sm);
     if (threadIdx.x == 0) {
         if (total > cap) {
             st->overflow = 1;
@@ -354,27 +455,25 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
                                                             const ListStatus* st, int level, uint32_t kbits,
                                                             uint32_t salt, unsigned long long cap,
                                                             uint32_t* __restrict__ rid) {
+    if (level == 0 && layout_local(st)) return;  // k_rs_contract takes this list
     const unsigned long long N = st->R[level];
-    const unsigned long long base = (unsigned long long)blockIdx.x * TILE;
-    if (base >= N) return;
-    const unsigned long long i0 = base + (unsigned long long)threadIdx.x * TILE_ITEMS;
-    uint32_t flags = 0, cnt = 0;
-#pragma unroll
-    for (int j = 0; j < TILE_ITEMS; ++j) {
-        const unsigned long long i = i0 + j;
-        if (i < N && is_ruler((uint32_t)i, kbits, salt)) {
-            flags |= 1u << j;
-            ++cnt;
-        }
-    }
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
     typedef cub::BlockScan<uint32_t, TILE_THREADS> BS;
     __shared__ typename BS::TempStorage tmp;
-    uint32_t pre;
-    BS(tmp).ExclusiveSum(cnt, pre);
-    unsigned long long id = (unsigned long long)tile_off[blockIdx.x] + pre;
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long base = tile * TILE;
+        const unsigned long long i0 = base + (unsigned long long)threadIdx.x * TILE_ITEMS;
+        uint32_t flags = 0;
 #pragma unroll
-    for (int j = 0; j < TILE_ITEMS; ++j) {
-        if (flags & (1u << j)) {
+        for (int j = 0; j < TILE_ITEMS; ++j) {
+            const unsigned long long i = i0 + j;
+            if (i < N && is_ruler((uint32_t)i, kbits, salt)) flags |= 1u << j;
+        }
+        uint32_t pre;
+        BS(tmp).ExclusiveSum((uint32_t)__popc(flags), pre);
+        unsigned long long id = (unsigned long long)tile_off[tile] + pre;
+        for (uint32_t rem = flags; rem != 0; rem &= rem - 1, ++id) {
+            const uint32_t j = __ffs(rem) - 1;
             if (id < cap) {
                 spl[id] = (uint32_t)(i0 + j);
                 if (rid != nullptr)
@@ -382,8 +481,8 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
                 else
                     word[i0 + j] = kPacked ? ((id << 32) | (word[i0 + j] & 0xFFFFFFFFull)) : (id << 32);
             }
-            ++id;
         }
+        __syncthreads();
     }
 }
 
@@ -434,8 +533,7 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
                                                           const uint32_t* __restrict__ spl,
                                                           uint2* __restrict__ up, ListStatus* st, int level,
                                                           uint32_t kbits, uint32_t salt, uint32_t cap_hops,
-                                                          bool only_local, const uint32_t* __restrict__ rid) {
-    if (only_local && !layout_local(st)) return;  // k_rs_walk0 takes this list
+                                                          const uint32_t* __restrict__ rid) {
     const unsigned long long N = st->R[level];
     const unsigned long long R = st->R[level + 1];
     unsigned long long* q = &st->qhead[level];
@@ -680,6 +778,43 @@ __global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long
     for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) rank[w0 + i] = win[i];
 }
 
+// Coarse windows straight to node order: the pairs of one coarse window are
+// contiguous, so a front-to-back sweep keeps the stores of the CTAs in
+// flight inside one or two windows (a few MiB of ranks) -- L2 merges the
+// random 4/8-B stores into whole lines before they are written back.
+template <class OutT>
+__global__ void __launch_bounds__(256) k_rs_rec_l2scatter(const unsigned long long* __restrict__ pairs,
+                                                          OutT* __restrict__ rank, unsigned long long n,
+                                                          uint32_t cshift, const ListStatus* st) {
+    if (layout_local(st) || st->overflow) return;
+    const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(pairs);
+    const unsigned long long np = n >> 1;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + stride < np; i += 2 * stride) {
+        const ulonglong2 a = __ldcs(p2 + i);
+        const ulonglong2 b = __ldcs(p2 + i + stride);
+        const unsigned long long s0 = 2 * i, s1 = 2 * (i + stride);
+        const unsigned long long c0 = a.x >> 32, c1 = a.y >> 32, c2 = b.x >> 32, c3 = b.y >> 32;
+        if (c0 < n && (c0 >> cshift) == (s0 >> cshift)) rank[c0] = (OutT)(uint32_t)a.x;
+        if (c1 < n && (c1 >> cshift) == (s0 >> cshift)) rank[c1] = (OutT)(uint32_t)a.y;
+        if (c2 < n && (c2 >> cshift) == (s1 >> cshift)) rank[c2] = (OutT)(uint32_t)b.x;
+        if (c3 < n && (c3 >> cshift) == (s1 >> cshift)) rank[c3] = (OutT)(uint32_t)b.y;
+    }
+    for (; i < np; i += stride) {
+        const ulonglong2 a = __ldcs(p2 + i);
+        const unsigned long long s0 = 2 * i;
+        const unsigned long long c0 = a.x >> 32, c1 = a.y >> 32;
+        if (c0 < n && (c0 >> cshift) == (s0 >> cshift)) rank[c0] = (OutT)(uint32_t)a.x;
+        if (c1 < n && (c1 >> cshift) == (s0 >> cshift)) rank[c1] = (OutT)(uint32_t)a.y;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long a = pairs[n - 1];
+        const unsigned long long c0 = a >> 32;
+        if (c0 < n && (c0 >> cshift) == ((n - 1) >> cshift)) rank[c0] = (OutT)(uint32_t)a;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // top level: one CTA of weighted pointer jumping (RS4 single block,
 // listrank.py:333-342) producing inclusive suffix sums IS[i].
@@ -748,36 +883,321 @@ __global__ void __launch_bounds__(256) k_rs_expand_k(const unsigned long long* _
 }
 
 template <class OutT>
-__global__ void __launch_bounds__(256) k_rs_expand0(const unsigned long long* __restrict__ word,
-                                                    const uint32_t* __restrict__ IS1, OutT* __restrict__ rank,
-                                                    unsigned long long n, const ListStatus* st) {
-    if (st->overflow || !layout_local(st)) return;  // overflow: Wyllie re-ranks; scattered: record path
-    const unsigned long long R1 = st->R[1];
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    const unsigned long long npair = n >> 1;
-    const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(word);
-    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < npair; k += stride) {
-        const ulonglong2 w = __ldcs(w2 + k);
-        const unsigned long long o0 = w.x >> 32, o1 = w.y >> 32;
-        const uint32_t r0 = o0 < R1 ? __ldg(IS1 + o0) - (uint32_t)w.x - 1u : 0u;
-        const uint32_t r1 = o1 < R1 ? __ldg(IS1 + o1) - (uint32_t)w.y - 1u : 0u;
-        rank[2 * k] = (OutT)r0;
-        rank[2 * k + 1] = (OutT)r1;
-    }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const unsigned long long w = word[n - 1];
-        const unsigned long long o = w >> 32;
-        rank[n - 1] = (OutT)(o < R1 ? IS1[o] - (uint32_t)w - 1u : 0u);
-    }
-}
-
-template <class OutT>
 __global__ void k_rs_expand_direct(const uint32_t* __restrict__ IS0, OutT* __restrict__ rank, unsigned long long n,
                                    const ListStatus* st) {
     if (st->overflow) return;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         rank[i] = (OutT)(IS0[i] - 1u);
+}
+
+// ---------------------------------------------------------------------------
+// Tile contraction (local layouts: ordered or locally shuffled lists).
+//
+// A tile is TILE consecutive node ids.  Inside a tile the successor links
+// that stay in the tile form disjoint chains ("segments"); a segment starts
+// at a node with no in-tile predecessor (its head) and ends at a node whose
+// successor leaves the tile (or the tail).  One CTA per tile loads the tile's
+// successors into shared memory (coalesced) and ranks every node inside its
+// segment with a small ruling set of its own: segment heads plus every
+// CT_STRIDE-th node walk to the next local ruler, then weighted pointer
+// jumping over the local rulers gives each node its distance to the segment
+// end.  The contracted list -- one node per segment, weight = segment length,
+// numbered by head index so node 0's segment is 0 -- is ranked by the
+// upper levels; the expand pass recomputes the same tile structure and writes
+// rank = (IS1[segment] - length) + distance to the end, coalesced.  Per node
+// this costs two streaming 4-B reads and one 4-B write; no walk touches HBM
+// at random.  Validation: no in-tile node with two in-tile predecessors, no
+// in-tile cycle, heads == ends per tile, every segment's successor is some
+// segment's head; the top level then checks that the head's segment reaches
+// the tail with weight n (listrank.py:297-298, core.py:148-167).
+constexpr uint32_t CT_STRIDE = 16;
+constexpr uint16_t CT_END = 0xFFFF;
+constexpr int CT_CTAS_PER_SM = 3;
+
+struct ContractSmem {
+    uint32_t own[TILE];      // node -> (local ruler << 16) | offset from the ruler          [sw32]
+    uint32_t link[TILE];     // ruler -> (next ruler << 16) | distance; next = CT_END: distance to the segment end
+    uint16_t nx[TILE];       // node -> in-tile successor, CT_END if it leaves the tile / is the tail [sw16]
+    uint16_t rid[TILE];      // node -> local ruler index (walk); end node -> tile-local segment     [sw16]
+    uint16_t term[TILE];     // ruler -> end node of its segment
+    uint8_t pred[TILE];      // node has an in-tile predecessor
+};
+
+// Bank swizzles for node-indexed arrays.  Walkers start 16 nodes apart (one
+// local ruler per 16 ids), so an unswizzled u32 array puts a warp's 32 walk
+// steps into 2 banks.  sw32 spreads them over all 32 banks; sw16 (2 ids per
+// bank word) leaves at most 2-way conflicts.  Both keep aligned groups of 4
+// ids together (sw16 also in order; sw32 permutes a group by XOR with
+// sw32(group base) & 3), so 16-B / 8-B vector accesses stay legal.
+__device__ __forceinline__ uint32_t sw32(uint32_t l) { return l ^ (((l >> 5) & 3u) << 2) ^ ((l >> 7) & 3u); }
+__device__ __forceinline__ uint32_t sw16(uint32_t l) { return l ^ (((l >> 6) & 7u) << 2); }
+
+template <class SuccT, class OutT, bool kExpand, bool kVec>
+__global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
+    const SuccT* __restrict__ succ, ListStatus* st, const uint32_t* __restrict__ tile_off,
+    uint32_t* __restrict__ headsid, uint32_t* __restrict__ seg_head, uint32_t* __restrict__ seg_succ,
+    uint2* __restrict__ lvl1, const uint32_t* __restrict__ IS1, OutT* __restrict__ rank) {
+    if (!layout_local(st)) return;
+    if (kExpand && (st->overflow || st->bad)) return;
+    constexpr int VEC = 4;  // ids per thread and vector access
+    constexpr int NV = TILE_ITEMS / VEC;
+    extern __shared__ __align__(16) unsigned char ct_raw[];
+    ContractSmem& S = *reinterpret_cast<ContractSmem*>(ct_raw);
+    typedef cub::BlockScan<unsigned long long, TILE_THREADS> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+    const unsigned long long N = st->R[0];
+    const unsigned long long R1 = st->R[1];
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
+    const uint32_t t = threadIdx.x;
+    static_assert(TILE == TILE_THREADS * 16, "one uint4 of predecessor flags per thread");
+    bool bad = false;
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long base = tile * TILE;
+        const uint32_t tn = (uint32_t)min((unsigned long long)TILE, N - base);
+        const bool full = kVec && tn == TILE;
+        // 1. successors -> in-tile links, predecessor flags (plain byte
+        //    stores: a node with two in-tile predecessors shows up as fewer
+        //    flags than links).  Thread t holds ids 4(j*256+t) .. +3.
+        SuccT v[TILE_ITEMS];
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const SuccT* p = succ + base + (size_t)(j * TILE_THREADS + t) * VEC;
+                if (sizeof(SuccT) == 4) {
+                    const uint4 w = kExpand ? __ldcs(reinterpret_cast<const uint4*>(p)) : *reinterpret_cast<const uint4*>(p);
+                    v[j * 4 + 0] = (SuccT)w.x, v[j * 4 + 1] = (SuccT)w.y, v[j * 4 + 2] = (SuccT)w.z, v[j * 4 + 3] = (SuccT)w.w;
+                } else {
+                    const ulonglong2 w0 = kExpand ? __ldcs(reinterpret_cast<const ulonglong2*>(p))
+                                                  : *reinterpret_cast<const ulonglong2*>(p);
+                    const ulonglong2 w1 = kExpand ? __ldcs(reinterpret_cast<const ulonglong2*>(p) + 1)
+                                                  : *(reinterpret_cast<const ulonglong2*>(p) + 1);
+                    v[j * 4 + 0] = (SuccT)w0.x, v[j * 4 + 1] = (SuccT)w0.y, v[j * 4 + 2] = (SuccT)w1.x, v[j * 4 + 3] = (SuccT)w1.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) {
+                    const uint32_t l = (j * TILE_THREADS + t) * VEC + c;
+                    v[j * 4 + c] = l < tn ? succ[base + l] : SuccT(0);
+                }
+        }
+        reinterpret_cast<uint4*>(S.pred)[t] = make_uint4(0u, 0u, 0u, 0u);  // 4096 flags
+        __syncthreads();
+        uint32_t links = 0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
+            uint16_t nx[VEC];
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+                const uint32_t l = l0 + c;
+                nx[c] = CT_END;
+                if (l < tn) {
+                    const unsigned long long dx = as_index<SuccT>(v[j * 4 + c]) - base;
+                    if (dx < tn && dx != l) {
+                        nx[c] = (uint16_t)dx;
+                        S.pred[dx] = 1;
+                        ++links;
+                    }
+                }
+            }
+            *reinterpret_cast<ushort4*>(&S.nx[sw16(l0)]) = make_ushort4(nx[0], nx[1], nx[2], nx[3]);
+            *reinterpret_cast<uint4*>(&S.own[sw32(l0) & ~3u]) = make_uint4(~0u, ~0u, ~0u, ~0u);
+        }
+        __syncthreads();
+        if (!kExpand && tile == 0 && S.pred[0]) bad = true;  // node 0 must start the list
+        // 2. local rulers (blocked: thread t owns nodes 16t .. 16t+15): heads
+        //    and every CT_STRIDE-th node; numbered in index order
+        uint32_t rflags = 0, hflags = 0;
+        const uint4 pf = reinterpret_cast<const uint4*>(S.pred)[t];
+        const uint32_t pw[4] = {pf.x, pf.y, pf.z, pf.w};
+#pragma unroll
+        for (int q = 0; q < TILE_ITEMS; ++q) {
+            const uint32_t l = t * TILE_ITEMS + q;
+            if (l < tn) {
+                const bool head = ((pw[q >> 2] >> (8 * (q & 3))) & 0xFFu) == 0u;
+                if (head) hflags |= 1u << q;
+                if (head || (l % CT_STRIDE) == 0) rflags |= 1u << q;
+            }
+        }
+        // one scan: rulers (bits 32..), heads (16..31), in-tile links (0..15)
+        unsigned long long packed = ((unsigned long long)__popc(rflags) << 32) |
+                                    ((unsigned long long)__popc(hflags) << 16) | links, pre, tot;
+        BS(scan_tmp).ExclusiveSum(packed, pre, tot);
+        const uint32_t rpre = (uint32_t)(pre >> 32), hpre = (uint32_t)(pre >> 16) & 0xFFFFu;
+        const uint32_t K = (uint32_t)(tot >> 32), H = (uint32_t)(tot >> 16) & 0xFFFFu;
+        if (!kExpand && H + (uint32_t)(tot & 0xFFFFu) != tn) bad = true;  // two in-tile predecessors
+#pragma unroll
+        for (int g = 0; g < TILE_ITEMS / 4; ++g) {
+            uint16_t r[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int q = g * 4 + c;
+                r[c] = (rflags & (1u << q)) ? (uint16_t)(rpre + __popc(rflags & ((1u << q) - 1u))) : CT_END;
+            }
+            *reinterpret_cast<ushort4*>(&S.rid[sw16(t * TILE_ITEMS + g * 4)]) = make_ushort4(r[0], r[1], r[2], r[3]);
+        }
+        __syncthreads();
+        // 3. each thread walks from its own local rulers to the next local
+        //    ruler / the segment end
+        for (uint32_t rem = rflags; rem != 0; rem &= rem - 1) {
+            const uint32_t q = __ffs(rem) - 1;
+            const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
+            uint32_t l = t * TILE_ITEMS + q, off = 0;
+            for (;;) {
+                S.own[sw32(l)] = (k << 16) | off;
+                const uint16_t nx = S.nx[sw16(l)];
+                if (nx == CT_END) {
+                    S.link[k] = ((uint32_t)CT_END << 16) | off;
+                    S.term[k] = (uint16_t)l;
+                    break;
+                }
+                const uint16_t r2 = S.rid[sw16(nx)];
+                if (r2 != CT_END || off + 1 >= TILE) {  // the cap only trips on invalid lists
+                    if (r2 == CT_END) bad = true;
+                    S.link[k] = ((uint32_t)(r2 == CT_END ? k : r2) << 16) | (off + 1);
+                    S.term[k] = CT_END;
+                    break;
+                }
+                l = nx;
+                ++off;
+            }
+        }
+        __syncthreads();
+        // 4. weighted pointer jumping over the local rulers, in place (one
+        //    32-bit {next, distance} word per ruler keeps every read
+        //    consistent), until each ruler points at the last ruler of its
+        //    segment -- whose word holds the distance to the end
+        for (int round = 0; round < 16; ++round) {
+            int active = 0;
+            for (uint32_t k = t; k < K; k += TILE_THREADS) {
+                const uint32_t a = S.link[k];
+                const uint32_t p = a >> 16;
+                if (p != CT_END) {
+                    const uint32_t b = S.link[p];
+                    if ((b >> 16) != CT_END) {
+                        S.link[k] = (b & 0xFFFF0000u) | ((a + b) & 0xFFFFu);
+                        active = 1;
+                    }
+                }
+            }
+            if (!__syncthreads_or(active)) break;
+        }
+        // distance from ruler k to its segment end, and the end node
+        auto seg_end = [&](uint32_t k, uint32_t& d, uint16_t& e) {
+            const uint32_t a = S.link[k];
+            const uint32_t p = a >> 16;
+            if (p == CT_END) {
+                d = a & 0xFFFFu;
+                e = S.term[k];
+            } else {
+                const uint32_t b = S.link[p];
+                d = (a + b) & 0xFFFFu;
+                e = (b >> 16) == CT_END ? S.term[p] : CT_END;
+            }
+        };
+        if (!kExpand) {
+            for (uint32_t k = t; k < K; k += TILE_THREADS) {
+                uint32_t d;
+                uint16_t e;
+                seg_end(k, d, e);
+                if (e == CT_END) bad = true;  // a cycle through local rulers
+            }
+            for (uint32_t l = t; l < tn; l += TILE_THREADS)
+                if (S.own[sw32(l)] == 0xFFFFFFFFu) bad = true;  // a cycle without local rulers
+        }
+        // 5. segments: numbered by head index; end node -> tile-local segment
+        const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
+                                                : (uint32_t)(R1 - tile_off[tile]);
+        if (!kExpand && segs != H) bad = true;
+        __syncthreads();  // rid[] is rewritten below
+        for (uint32_t rem = hflags; rem != 0; rem &= rem - 1) {
+            const uint32_t q = __ffs(rem) - 1;
+            const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
+            const uint32_t h = hpre + __popc(hflags & ((1u << q) - 1u));
+            uint32_t d;
+            uint16_t e;
+            seg_end(k, d, e);
+            if (e != CT_END) S.rid[sw16(e)] = (uint16_t)h;
+            if (!kExpand && h < segs && e != CT_END) {
+                const unsigned long long sid = (unsigned long long)tile_off[tile] + h;
+                const uint32_t l = t * TILE_ITEMS + q;
+                seg_head[sid] = (uint32_t)(base + l);
+                headsid[base + l] = (uint32_t)sid;
+                lvl1[sid] = make_uint2(0u, d + 1u);
+                const unsigned long long x = as_index<SuccT>(succ[base + e]);
+                seg_succ[sid] = (x >= N || x == base + e) ? NIL : (uint32_t)x;
+            }
+        }
+        if (kExpand) {
+            __syncthreads();
+            const unsigned long long t0 = tile_off[tile];
+            auto rank_of = [&](uint32_t o) -> uint32_t {
+                uint32_t r = 0;
+                if (o != 0xFFFFFFFFu) {  // always, for lists that passed the contraction checks
+                    uint32_t d;
+                    uint16_t e;
+                    seg_end(o >> 16, d, e);
+                    const unsigned long long sid = t0 + (e != CT_END ? S.rid[sw16(e)] : 0xFFFFu);
+                    if (sid < R1) r = __ldg(IS1 + sid) - __ldg(&lvl1[sid].y) + (d - (o & 0xFFFFu));
+                }
+                return r;
+            };
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
+                const uint32_t g = sw32(l0);
+                const uint4 ow4 = *reinterpret_cast<const uint4*>(&S.own[g & ~3u]);
+                const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
+                OutT r[VEC];
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) r[c] = (OutT)rank_of(ow[c ^ (g & 3u)]);
+                if (full) {
+                    if (sizeof(OutT) == 4) {
+                        __stcs(reinterpret_cast<uint4*>(rank + base + l0),
+                               make_uint4((uint32_t)r[0], (uint32_t)r[1], (uint32_t)r[2], (uint32_t)r[3]));
+                    } else {
+                        ulonglong2* q = reinterpret_cast<ulonglong2*>(rank + base + l0);
+                        __stcs(q, make_ulonglong2((unsigned long long)r[0], (unsigned long long)r[1]));
+                        __stcs(q + 1, make_ulonglong2((unsigned long long)r[2], (unsigned long long)r[3]));
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c)
+                        if (l0 + c < tn) rank[base + l0 + c] = r[c];
+                }
+            }
+        }
+        __syncthreads();  // shared memory is reused by the next tile
+    }
+    if (bad) st->bad = 1;
+}
+
+// contracted list links: segment s -> the segment whose head is succ(end(s))
+__global__ void k_rs_contract_link(const uint32_t* __restrict__ headsid, const uint32_t* __restrict__ seg_head,
+                                   const uint32_t* __restrict__ seg_succ, uint2* __restrict__ lvl1, ListStatus* st) {
+    if (!layout_local(st)) return;
+    const unsigned long long S = st->R[1];
+    const unsigned long long N = st->R[0];
+    bool bad = false;
+    for (unsigned long long s = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+         s += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint32_t x = seg_succ[s];
+        uint32_t nxt = (uint32_t)s;  // the tail's segment points at itself
+        if (x != NIL) {
+            const uint32_t y = x < N ? headsid[x] : NIL;
+            if (y < S && seg_head[y] == x) {
+                nxt = y;
+            } else {
+                bad = true;  // succ(end) is not a segment head: a node with two predecessors
+            }
+        }
+        lvl1[s].x = nxt;
+    }
+    if (bad) st->bad = 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -793,6 +1213,8 @@ struct RsPlan {
     unsigned long long nwin = 1;                 // number of fine windows
     uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
     bool rec_ok = true;                          // fine windows fit shared memory
+    int scatter_mode = 0;                        // 0: refine + smem scatter, 1: L2 window scatter
+    int contract = 1;                            // allow the tile contraction for local layouts
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
@@ -825,6 +1247,11 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     uint32_t cs = p.fshift + 1;
     if (cs < 13) cs = 13;  // 2^cshift must be a multiple of MS_TILE
     while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
+    p.scatter_mode = (int)env_u32("SG_RS_SCATTER", 0, 0, 1);
+    if (p.scatter_mode == 1) {
+        const uint32_t mcs = env_u32("SG_RS_CSHIFT", 20, 13, 30);
+        if (cs < mcs) cs = mcs;
+    }
     while (cs - p.fshift > 8) ++p.fshift;  // <= 256 fine windows per coarse window
     p.rec_ok = ((size_t)out_bytes << p.fshift) <= (200u << 10);  // false only for n > ~2^31
     p.cshift = cs;
@@ -842,6 +1269,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     const uint32_t fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
+    p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
     p.cap[0] = n;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
@@ -867,6 +1295,8 @@ struct RsBufs {
     unsigned long long* pairs = nullptr;
     unsigned long long* cursor = nullptr;  // coarse cursors, then fine cursors
     uint32_t* tiles = nullptr;
+    uint32_t* tiles_end = nullptr;
+    uint32_t* tiles_up = nullptr;   // levels >= 1 (level 0's offsets stay for the contraction expand)
     uint32_t* spl[SG_MAX_LEVELS] = {};
     uint2* lvl[SG_MAX_LEVELS + 1] = {};
     unsigned long long* word[SG_MAX_LEVELS + 1] = {};
@@ -889,6 +1319,8 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     }
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     b.tiles = c.take<uint32_t>(ntiles + 1);
+    b.tiles_end = c.take<uint32_t>(ntiles + 1);
+    b.tiles_up = c.take<uint32_t>((p.levels > 0 ? (p.cap[1] + TILE - 1) / TILE : 0) + 1);
     for (int k = 0; k < p.levels; ++k) {
         const unsigned long long cap = p.cap[k + 1];
         b.spl[k] = c.take<uint32_t>(cap);
@@ -952,6 +1384,19 @@ static int wyllie_run(const SuccT* succ, OutT* rank, uint64_t n, int variant, Li
     return SG_OK;
 }
 
+template <class SuccT, class OutT, bool kExpand>
+static int launch_contract(uint32_t grid, cudaStream_t s, const SuccT* succ, OutT* rank, ListStatus* st,
+                           const uint32_t* tile_off, uint32_t* headsid, uint32_t* seg_head, uint32_t* seg_succ,
+                           uint2* lvl1, const uint32_t* IS1) {
+    const bool vec = ((uintptr_t)succ & 15) == 0 && ((uintptr_t)rank & 15) == 0;
+    auto kv = k_rs_contract<SuccT, OutT, kExpand, true>;
+    auto ks = k_rs_contract<SuccT, OutT, kExpand, false>;
+    auto k = vec ? kv : ks;
+    SG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ContractSmem)));
+    k<<<grid, TILE_THREADS, sizeof(ContractSmem), s>>>(succ, st, tile_off, headsid, seg_head, seg_succ, lvl1, IS1, rank);
+    return SG_OK;
+}
+
 // ---- ruling-set host driver ----------------------------------------------------
 
 template <class SuccT, class OutT>
@@ -985,38 +1430,56 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         const uint32_t nt = (uint32_t)((capN + TILE - 1) / TILE);
         const unsigned long long capR = p.cap[k + 1];
         unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
+        uint32_t* tk = k == 0 ? b.tiles : b.tiles_up;
         if (k == 0) {
             rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, capN);
-            k_rs_count0<SuccT><<<nt < kSMs * 8 ? nt : kSMs * 8, TILE_THREADS, 0, s>>>(succ, b.tiles, b.st, p.kbits[0],
-                                                                                   p.salt[0]);
+            const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
+            if (((uintptr_t)succ & 15) == 0)
+                k_rs_count0<SuccT, true><<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0],
+                                                                      p.salt[0]);
+            else
+                k_rs_count0<SuccT, false><<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0],
+                                                                       p.salt[0]);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
-            k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, b.tiles, b.st, k, p.kbits[k], p.salt[k], 1);
+            k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, tk, b.st, k, p.kbits[k], p.salt[k], 1);
         }
         rec.end();
         SG_LAUNCH_CHECK();
-        rec.begin(k == 0 ? K_RS_SCAN : K_RS4_SCAN, k, 1, 1024, nt);
-        k_rs_scan<<<1, 1024, 0, s>>>(b.tiles, b.st, k, capR);
+        rec.begin(k == 0 ? K_RS_SCAN : K_RS4_SCAN, k, 1, SCAN_THREADS, nt);
+        if (k == 0)
+            k_rs_scan0<<<1, SCAN_THREADS, 0, s>>>(b.tiles, b.tiles_end, b.st, capR, p.contract);
+        else
+            k_rs_scan<<<1, SCAN_THREADS, 0, s>>>(tk, b.st, k, capR);
         rec.end();
         SG_LAUNCH_CHECK();
         rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
-        k_rs_select<false><<<nt, TILE_THREADS, 0, s>>>(b.tiles, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
+        k_rs_select<false><<<nt < kSMs * 8 ? nt : kSMs * 8, TILE_THREADS, 0, s>>>(tk, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
                                                         k == 0 ? b.rid : nullptr);
         rec.end();
         SG_LAUNCH_CHECK();
         if (k == 0) {
+            // scattered layouts: record walk; local layouts: tile contraction
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
             k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rid, b.spl[0], b.lvl[1], b.rec_cur,
                                                                     b.rec_sl, b.st, p.kbits[0], p.salt[0],
                                                                     p.walk_cap, p.maxchunks, p.load_mode);
+            rec.end();
             SG_LAUNCH_CHECK();
-            k_rs_walk<Level0<SuccT>><<<walk_grid, WALK_THREADS, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.word0,
-                                                                        b.spl[0], b.lvl[1], b.st, 0, p.kbits[0],
-                                                                        p.salt[0], p.walk_cap, true, b.rid);
+            const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
+            rec.begin(K_RS_CONTRACT, 0, cg, TILE_THREADS, capN);
+            const int rc = launch_contract<SuccT, OutT, false>(cg, s, succ, (OutT*)nullptr, b.st, b.tiles, b.rid,
+                                                               b.spl[0], b.IS[1], b.lvl[1], nullptr);
+            if (rc != SG_OK) return rc;
+            rec.end();
+            SG_LAUNCH_CHECK();
+            const uint32_t lg = grid_for(capR, 256, 1, kSMs * 8);
+            rec.begin(K_RS_CONTRACT_LINK, 0, lg, 256, capR);
+            k_rs_contract_link<<<lg, 256, 0, s>>>(b.rid, b.spl[0], b.IS[1], b.lvl[1], b.st);
         } else {
             rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
             k_rs_walk<LevelK><<<walk_grid, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
-                                                                 k, p.kbits[k], p.salt[k], p.walk_cap, false, nullptr);
+                                                                 k, p.kbits[k], p.salt[k], p.walk_cap, nullptr);
         }
         rec.end();
         SG_LAUNCH_CHECK();
@@ -1035,11 +1498,16 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
     }
-    const uint32_t g = grid_for(n / 2 + 1, 256, 1, kSMs * 8);
-    rec.begin(K_RS5_EXPAND, 0, g, 256, n);
-    k_rs_expand0<OutT><<<g, 256, 0, s>>>(b.word0, b.IS[1], rank, n, b.st);  // local layouts
-    rec.end();
-    SG_LAUNCH_CHECK();
+    {  // local layouts: expand the contraction
+        const uint32_t nt = (uint32_t)((n + TILE - 1) / TILE);
+        const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
+        rec.begin(K_RS5_EXPAND, 0, cg, TILE_THREADS, n);
+        int rc = launch_contract<SuccT, OutT, true>(cg, s, succ, rank, b.st, b.tiles, nullptr, nullptr, nullptr,
+                                                    b.lvl[1], b.IS[1]);
+        if (rc != SG_OK) return rc;
+        rec.end();
+        SG_LAUNCH_CHECK();
+    }
     // scattered layouts: rank the records, bucket them by window, scatter
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
     const uint32_t persist = kSMs * 4;
@@ -1051,6 +1519,15 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
                                                             p.cshift, p.cbins);
     rec.end();
     SG_LAUNCH_CHECK();
+    if (p.scatter_mode == 1) {
+        const uint32_t g2 = kSMs * 8;
+        rec.begin(K_RS5_SCATTER, 0, g2, 256, n);
+        k_rs_rec_l2scatter<OutT><<<g2, 256, 0, s>>>(b.pairs, rank, n, p.cshift, b.st);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        if (stats) stats->levels = (uint32_t)L;
+        return SG_OK;
+    }
     rec.begin(K_RS5_REFINE, 0, persist, MS_THREADS, n);
     k_rs_rec_refine<<<persist, MS_THREADS, sm_ref, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
                                                         p.fshift);
@@ -1127,6 +1604,7 @@ static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed,
     if (stats) {
         stats->levels = (uint32_t)p.levels;
         stats->fallback = 0;
+        stats->list_path = 0;
         for (int k = 0; k < SG_MAX_LEVELS; ++k) stats->level_size[k] = 0;
     }
     Recorder rec(stats, s);
@@ -1148,8 +1626,10 @@ static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed,
     ListStatus h;
     rc = read_status(b.st, h, s);
     if (rc != SG_OK) return rc;
-    if (stats)
+    if (stats) {
         for (int k = 0; k <= p.levels && k < SG_MAX_LEVELS; ++k) stats->level_size[k] = h.R[k];
+        stats->list_path = h.local ? 1u : 0u;
+    }
     if (h.oor_first == NONE64 && h.loop_count == 1 && h.overflow) {
         // a walk hit the hop cap or a level overflowed its capacity: rank the
         // list by pointer jumping instead (terminates on every input)

@@ -137,7 +137,7 @@ const char* sg_kernel_name(int id) {
         "rs4_scan",    "rs4_select",  "rs4_walk",    "rs4_rank",    "rs4_expand",
         "rs5_expand",  "sv0",         "cc_hook_uf",  "cc_hook_sv",  "cc_shortcut",
         "cc_labels",   "gather",      "kiss",        "list_from_order", "edge_keys",
-        "edges_from_keys", "cc_partition", "rs5_partition", "rs5_scatter", "rs5_refine",
+        "edges_from_keys", "cc_partition", "rs5_partition", "rs5_scatter", "rs5_refine", "rs3_contract", "rs3_link",
     };
     if (id < 0 || id >= sg::K_COUNT_) return "unknown";
     return names[id];

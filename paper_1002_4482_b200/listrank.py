@@ -295,7 +295,9 @@ def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_su
     stats.meta.update(n=n, p=p, packing=packing.value, splitter_set=splitters,
                       max_sublist=int(splitters.sublist_len.max()),
                       levels=int(st.levels), level_size=[int(st.level_size[k]) for k in range(st.levels + 1)],
-                      fallback=bool(st.fallback), backend=backend, accounting=accounting,
+                      fallback=bool(st.fallback),
+                      path="wyllie" if st.fallback else ("contract" if st.list_path == 1 else "ruling_set"),
+                      backend=backend, accounting=accounting,
                       block_size=block_size, seed=seed, workers=workers)
     return _finish_rank(rank, host_input), stats
 
