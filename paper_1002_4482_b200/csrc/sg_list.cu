@@ -756,6 +756,133 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_refine(const unsigned 
     if (over) st->bad = 1;
 }
 
+// TMA-staged versions (persistent, 2 CTAs per SM): the next 4096-element
+// tile streams into shared memory while the current one is split.
+constexpr int MS2_CTAS_PER_SM = 2;
+
+__global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_partition2(
+    const uint32_t* __restrict__ rec_cur, const unsigned long long* __restrict__ rec_sl,
+    const uint32_t* __restrict__ IS1, unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ pairs,
+    ListStatus* st, uint32_t cshift, uint32_t cbins) {
+    if (layout_local(st) || st->overflow) return;
+    extern __shared__ __align__(128) unsigned char ms_raw[];
+    uint32_t* s_cur = reinterpret_cast<uint32_t*>(ms_raw);
+    unsigned long long* s_sl = reinterpret_cast<unsigned long long*>(ms_raw + MS2_TILE * 4);
+    MsSmem sm = MsSmem::carve(ms_raw + MS2_TILE * 12, cbins, MS2_TILE);
+    __shared__ unsigned long long bar;
+    const unsigned long long total = st->chunks * REC_CH;  // a multiple of REC_CH
+    const unsigned long long ntiles = (total + MS2_TILE - 1) / MS2_TILE;
+    const unsigned long long R1 = st->R[1];
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    auto issue = [&](unsigned long long tile) {
+        if (threadIdx.x == 0 && tile < ntiles) {
+            const unsigned long long e0 = tile * MS2_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, total - e0);
+            mbar_expect_tx(&bar, cnt * 12u);
+            bulk_g2s(s_cur, rec_cur + e0, cnt * 4u, &bar);
+            bulk_g2s(s_sl, rec_sl + e0, cnt * 8u, &bar);
+        }
+    };
+    auto bin_of = [&](unsigned long long pr) { return (uint32_t)((pr >> 32) >> cshift); };
+    auto slot = [&](uint32_t b) { return make_ulonglong2((unsigned long long)b << cshift, 1ull << cshift); };
+    bool over = false;
+    uint32_t phase = 0;
+    issue(blockIdx.x);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, total - tile * MS2_TILE);
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        unsigned long long pr[MS2_ITEMS];
+        uint32_t bn[MS2_ITEMS];
+#pragma unroll
+        for (int g = 0; g < MS2_ITEMS / 4; ++g) {
+            const uint32_t e = (g * MS_THREADS + threadIdx.x) * 4;  // 4 records per vector access
+            const uint4 c4 = e < cnt ? reinterpret_cast<const uint4*>(s_cur)[e >> 2] : make_uint4(NIL, NIL, NIL, NIL);
+            const ulonglong2 s01 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[e >> 1] : make_ulonglong2(0, 0);
+            const ulonglong2 s23 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[(e >> 1) + 1] : make_ulonglong2(0, 0);
+            const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+            const unsigned long long sl[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = g * 4 + q;
+                const unsigned long long o = sl[q] >> 32;
+                pr[j] = ((unsigned long long)cc[q] << 32) | (uint32_t)sl[q];
+                bn[j] = __ldg(IS1 + (o < R1 ? o : 0));  // gathers first, all in flight together
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < MS2_ITEMS; ++j) {
+            const uint32_t c = (uint32_t)(pr[j] >> 32);
+            const uint32_t local = (uint32_t)pr[j];
+            // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
+            pr[j] = ((unsigned long long)c << 32) | (bn[j] - local - 1u);
+            const uint32_t b = c >> cshift;
+            bn[j] = (c != NIL && b < cbins) ? b : (uint32_t)MS_MAXB;
+        }
+        __syncthreads();  // staging consumed: refill it behind the split
+        issue(tile + gridDim.x);
+        over |= ms_split<MS2_ITEMS>(pr, bn, bin_of, slot, cbins, cursor, pairs, sm);
+    }
+    if (over) st->bad = 1;
+}
+
+__global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_refine2(
+    const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
+    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift) {
+    if (layout_local(st) || st->overflow) return;
+    const uint32_t fb = 1u << (cshift - fshift);
+    extern __shared__ __align__(128) unsigned char ms_raw[];
+    unsigned long long* s_in = reinterpret_cast<unsigned long long*>(ms_raw);
+    MsSmem sm = MsSmem::carve(ms_raw + MS2_TILE * 8, fb, MS2_TILE);
+    __shared__ unsigned long long bar;
+    // tiles never straddle a coarse window (2^cshift is a multiple of MS2_TILE)
+    const unsigned long long ntiles = (n + MS2_TILE - 1) / MS2_TILE;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    auto issue = [&](unsigned long long tile) {
+        if (threadIdx.x == 0 && tile < ntiles) {
+            const unsigned long long e0 = tile * MS2_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, n - e0);
+            const uint32_t bytes = (cnt * 8u + 15u) & ~15u;  // the buffer is padded to whole windows
+            mbar_expect_tx(&bar, bytes);
+            bulk_g2s(s_in, in + e0, bytes, &bar);
+        }
+    };
+    bool over = false;
+    uint32_t phase = 0;
+    issue(blockIdx.x);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long e0 = tile * MS2_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, n - e0);
+        const unsigned long long c = e0 >> cshift;
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        unsigned long long pr[MS2_ITEMS];
+        uint32_t bn[MS2_ITEMS];
+#pragma unroll
+        for (int g = 0; g < MS2_ITEMS / 2; ++g) {
+            const uint32_t e = (g * MS_THREADS + threadIdx.x) * 2;
+            const ulonglong2 v = e < cnt ? reinterpret_cast<const ulonglong2*>(s_in)[e >> 1] : make_ulonglong2(0, 0);
+            const unsigned long long vv[2] = {v.x, v.y};
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int j = g * 2 + q;
+                pr[j] = vv[q];
+                const unsigned long long cur = pr[j] >> 32;
+                bn[j] = (e + q < cnt && (cur >> cshift) == c) ? (uint32_t)((cur >> fshift) & (fb - 1))
+                                                             : (uint32_t)MS_MAXB;
+            }
+        }
+        __syncthreads();
+        issue(tile + gridDim.x);
+        auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
+        auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
+        over |= ms_split<MS2_ITEMS>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
+    }
+    if (over) st->bad = 1;
+}
+
 // one CTA per fine window: scatter its pairs into shared memory, then store
 // the window coalesced
 template <class OutT>
@@ -776,43 +903,6 @@ __global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) rank[w0 + i] = win[i];
-}
-
-// Coarse windows straight to node order: the pairs of one coarse window are
-// contiguous, so a front-to-back sweep keeps the stores of the CTAs in
-// flight inside one or two windows (a few MiB of ranks) -- L2 merges the
-// random 4/8-B stores into whole lines before they are written back.
-template <class OutT>
-__global__ void __launch_bounds__(256) k_rs_rec_l2scatter(const unsigned long long* __restrict__ pairs,
-                                                          OutT* __restrict__ rank, unsigned long long n,
-                                                          uint32_t cshift, const ListStatus* st) {
-    if (layout_local(st) || st->overflow) return;
-    const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(pairs);
-    const unsigned long long np = n >> 1;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + stride < np; i += 2 * stride) {
-        const ulonglong2 a = __ldcs(p2 + i);
-        const ulonglong2 b = __ldcs(p2 + i + stride);
-        const unsigned long long s0 = 2 * i, s1 = 2 * (i + stride);
-        const unsigned long long c0 = a.x >> 32, c1 = a.y >> 32, c2 = b.x >> 32, c3 = b.y >> 32;
-        if (c0 < n && (c0 >> cshift) == (s0 >> cshift)) rank[c0] = (OutT)(uint32_t)a.x;
-        if (c1 < n && (c1 >> cshift) == (s0 >> cshift)) rank[c1] = (OutT)(uint32_t)a.y;
-        if (c2 < n && (c2 >> cshift) == (s1 >> cshift)) rank[c2] = (OutT)(uint32_t)b.x;
-        if (c3 < n && (c3 >> cshift) == (s1 >> cshift)) rank[c3] = (OutT)(uint32_t)b.y;
-    }
-    for (; i < np; i += stride) {
-        const ulonglong2 a = __ldcs(p2 + i);
-        const unsigned long long s0 = 2 * i;
-        const unsigned long long c0 = a.x >> 32, c1 = a.y >> 32;
-        if (c0 < n && (c0 >> cshift) == (s0 >> cshift)) rank[c0] = (OutT)(uint32_t)a.x;
-        if (c1 < n && (c1 >> cshift) == (s0 >> cshift)) rank[c1] = (OutT)(uint32_t)a.y;
-    }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const unsigned long long a = pairs[n - 1];
-        const unsigned long long c0 = a >> 32;
-        if (c0 < n && (c0 >> cshift) == ((n - 1) >> cshift)) rank[c0] = (OutT)(uint32_t)a;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1213,8 +1303,8 @@ struct RsPlan {
     unsigned long long nwin = 1;                 // number of fine windows
     uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
     bool rec_ok = true;                          // fine windows fit shared memory
-    int scatter_mode = 0;                        // 0: refine + smem scatter, 1: L2 window scatter
     int contract = 1;                            // allow the tile contraction for local layouts
+    int ms_version = 2;                          // 2: TMA-staged window passes, 1: register tiles
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
@@ -1247,11 +1337,6 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     uint32_t cs = p.fshift + 1;
     if (cs < 13) cs = 13;  // 2^cshift must be a multiple of MS_TILE
     while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
-    p.scatter_mode = (int)env_u32("SG_RS_SCATTER", 0, 0, 1);
-    if (p.scatter_mode == 1) {
-        const uint32_t mcs = env_u32("SG_RS_CSHIFT", 20, 13, 30);
-        if (cs < mcs) cs = mcs;
-    }
     while (cs - p.fshift > 8) ++p.fshift;  // <= 256 fine windows per coarse window
     p.rec_ok = ((size_t)out_bytes << p.fshift) <= (200u << 10);  // false only for n > ~2^31
     p.cshift = cs;
@@ -1270,6 +1355,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
     p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
+    p.ms_version = (int)env_u32("SG_RS_MS", 2, 1, 2);
     p.cap[0] = n;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
@@ -1511,26 +1597,34 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // scattered layouts: rank the records, bucket them by window, scatter
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
     const uint32_t persist = kSMs * 4;
+    const uint32_t persist2 = kSMs * MS2_CTAS_PER_SM;
     const size_t sm_part = MsSmem::bytes(p.cbins), sm_ref = MsSmem::bytes(1u << (p.cshift - p.fshift));
-    SG_CUDA(cudaFuncSetAttribute(k_rs_rec_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part));
-    SG_CUDA(cudaFuncSetAttribute(k_rs_rec_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref));
-    rec.begin(K_RS5_PARTITION, 0, persist, MS_THREADS, n);
-    k_rs_rec_partition<<<persist, MS_THREADS, sm_part, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
-                                                            p.cshift, p.cbins);
-    rec.end();
-    SG_LAUNCH_CHECK();
-    if (p.scatter_mode == 1) {
-        const uint32_t g2 = kSMs * 8;
-        rec.begin(K_RS5_SCATTER, 0, g2, 256, n);
-        k_rs_rec_l2scatter<OutT><<<g2, 256, 0, s>>>(b.pairs, rank, n, p.cshift, b.st);
+    const size_t sm_part2 = (size_t)MS2_TILE * 12 + MsSmem::bytes(p.cbins, MS2_TILE);
+    const size_t sm_ref2 = (size_t)MS2_TILE * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), MS2_TILE);
+    if (p.ms_version == 2) {
+        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_partition2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part2));
+        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_refine2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref2));
+        rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
+        k_rs_rec_partition2<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs,
+                                                                   b.st, p.cshift, p.cbins);
         rec.end();
         SG_LAUNCH_CHECK();
-        if (stats) stats->levels = (uint32_t)L;
-        return SG_OK;
+    } else {
+        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part));
+        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref));
+        rec.begin(K_RS5_PARTITION, 0, persist, MS_THREADS, n);
+        k_rs_rec_partition<<<persist, MS_THREADS, sm_part, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
+                                                                p.cshift, p.cbins);
+        rec.end();
+        SG_LAUNCH_CHECK();
     }
-    rec.begin(K_RS5_REFINE, 0, persist, MS_THREADS, n);
-    k_rs_rec_refine<<<persist, MS_THREADS, sm_ref, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
-                                                        p.fshift);
+    rec.begin(K_RS5_REFINE, 0, p.ms_version == 2 ? persist2 : persist, MS_THREADS, n);
+    if (p.ms_version == 2)
+        k_rs_rec_refine2<<<persist2, MS_THREADS, sm_ref2, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n,
+                                                               p.cshift, p.fshift);
+    else
+        k_rs_rec_refine<<<persist, MS_THREADS, sm_ref, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
+                                                            p.fshift);
     rec.end();
     SG_LAUNCH_CHECK();
     rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);

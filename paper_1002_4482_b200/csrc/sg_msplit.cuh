@@ -26,54 +26,62 @@ constexpr int MS_MAXB = 1024;
 // dynamic shared memory layout for nb bins
 struct MsSmem {
     unsigned long long* buf;    // [MS_TILE] the tile, sorted by bin
-    unsigned long long* base;   // [nb] first global slot claimed for the bin
+    unsigned long long* base;   // [nb] first global slot claimed for the bin, then the tile -> global delta
+    unsigned long long* endp;   // [nb] end of the bin's global slots
     uint32_t* w;                // [MS_WARPS][nb] per-warp counts, then per-warp offsets
     uint32_t* start;            // [nb] first buffer slot of each bin in the tile
 
-    static size_t bytes(uint32_t nb) { return (size_t)MS_TILE * 8 + (size_t)nb * 8 + (size_t)nb * 4 * (MS_WARPS + 1); }
-    __device__ static MsSmem carve(unsigned char* p, uint32_t nb) {
+    static size_t bytes(uint32_t nb, uint32_t tile = MS_TILE) {
+        return (size_t)tile * 8 + (size_t)nb * 16 + (size_t)nb * 4 * (MS_WARPS + 1);
+    }
+    __device__ static MsSmem carve(unsigned char* p, uint32_t nb, uint32_t tile = MS_TILE) {
         MsSmem s;
         s.buf = reinterpret_cast<unsigned long long*>(p);
-        s.base = s.buf + MS_TILE;
-        s.w = reinterpret_cast<uint32_t*>(s.base + nb);
+        s.base = s.buf + tile;
+        s.endp = s.base + nb;
+        s.w = reinterpret_cast<uint32_t*>(s.endp + nb);
         s.start = s.w + (size_t)MS_WARPS * nb;
         return s;
     }
 };
 
-// One tile: elements [e0, e1), element (j, t) = e0 + j*MS_THREADS + t.
-// get(e, pair, bin) -> false to skip; bins < nb <= MS_MAXB, nbits =
-// ceil(log2 nb).  slot(bin) = {first slot, capacity}; cursor[bin] (global
-// u64) counts the bin's slots already claimed.  bin_of(pair) recovers the bin
-// when writing out.  Returns true if a bin overflowed (only for inputs that
-// break the caller's size contract).  Needs MsSmem::bytes(nb) of dynamic smem.
-template <class Get, class BinOf, class Slot>
-__device__ __forceinline__ bool ms_tile(Get get, BinOf bin_of, Slot slot, unsigned long long e0,
-                                        unsigned long long e1, uint32_t nb, int nbits,
-                                        unsigned long long* __restrict__ cursor,
-                                        unsigned long long* __restrict__ out, MsSmem& sm) {
+// The split of one tile already in registers: element j of thread t is
+// pr[j] with bin bn[j] (>= nb: skip).  slot(bin) = {first slot, capacity};
+// cursor[bin] (global u64) counts the bin's slots already claimed.
+// bin_of(pair) recovers the bin when writing out.  Returns true if a bin
+// overflowed (only for inputs that break the caller's size contract).
+template <int ITEMS, class BinOf, class Slot>
+__device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], const uint32_t (&bn)[ITEMS],
+                                         BinOf bin_of, Slot slot, uint32_t nb,
+                                         unsigned long long* __restrict__ cursor,
+                                         unsigned long long* __restrict__ out, MsSmem& sm) {
     const uint32_t lane = lane_id();
     const int w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    unsigned long long pr[MS_ITEMS];
-    uint32_t bn[MS_ITEMS];  // bin, or MS_MAXB for a skipped element
-    unsigned peers[MS_ITEMS];
-#pragma unroll
-    for (int j = 0; j < MS_ITEMS; ++j) {
-        const unsigned long long e = e0 + (unsigned long long)j * MS_THREADS + threadIdx.x;
-        uint32_t b = 0;
-        pr[j] = 0;
-        const bool ok = e < e1 && get(e, pr[j], b) && b < nb;
-        bn[j] = ok ? b : (uint32_t)MS_MAXB;
-    }
+    uint32_t rk[ITEMS];  // rank among the warp's elements of the same bin
     for (uint32_t b = lane; b < nb; b += 32) sm.w[w * nb + b] = 0;
     __syncwarp();
-    // per-warp counts
+    // per-warp counts; the leader of each peer group (lanes with equal bins)
+    // bumps the warp's counter and hands the old value to its peers
+    const int nbits = 32 - __clz(nb > 1 ? nb - 1 : 1);
 #pragma unroll
-    for (int j = 0; j < MS_ITEMS; ++j) {
-        peers[j] = __match_any_sync(0xffffffffu, bn[j]);
-        if (bn[j] < nb && (peers[j] & lt) == 0) sm.w[w * nb + bn[j]] += __popc(peers[j]);
-        __syncwarp();
+    for (int j = 0; j < ITEMS; ++j) {
+        // peers: lanes with the same bin (bit-by-bit ballots; the VOTE unit
+        // is much faster than match.any on this part)
+        const bool valid = bn[j] < nb;
+        const unsigned vb = __ballot_sync(0xffffffffu, valid);
+        unsigned peers = valid ? vb : ~vb;
+        for (int k = 0; k < nbits; ++k) {
+            const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
+            peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+        }
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (bn[j] < nb && (int)lane == leader) {
+            old = sm.w[w * nb + bn[j]];
+            sm.w[w * nb + bn[j]] = old + __popc(peers);
+        }
+        rk[j] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
     }
     __syncthreads();
     // bin totals -> tile-local bin starts, warp offsets, global slots
@@ -106,19 +114,18 @@ __device__ __forceinline__ bool ms_tile(Get get, BinOf bin_of, Slot slot, unsign
     uint32_t run = wpre + incl - tot;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint32_t c = sm.start[b];
+        const ulonglong2 sc = slot(b);
+        // global slot of tile position i in bin b: delta + i; valid while < end
+        sm.base[b] = sc.x + sm.base[b] - run;
+        sm.endp[b] = sc.x + sc.y;
         sm.start[b] = run;
         run += c;
     }
     __syncthreads();
-    // rank and place into the sorted tile
+    // place into the sorted tile
 #pragma unroll
-    for (int j = 0; j < MS_ITEMS; ++j) {
-        const bool ok = bn[j] < nb;
-        if (ok) sm.buf[sm.start[bn[j]] + sm.w[w * nb + bn[j]] + __popc(peers[j] & lt)] = pr[j];
-        __syncwarp();
-        if (ok && (peers[j] & lt) == 0) sm.w[w * nb + bn[j]] += __popc(peers[j]);
-        __syncwarp();
-    }
+    for (int j = 0; j < ITEMS; ++j)
+        if (bn[j] < nb) sm.buf[sm.start[bn[j]] + sm.w[w * nb + bn[j]] + rk[j]] = pr[j];
     __syncthreads();
     // write out, run by run
     uint32_t total = 0;
@@ -127,15 +134,68 @@ __device__ __forceinline__ bool ms_tile(Get get, BinOf bin_of, Slot slot, unsign
     for (uint32_t i = threadIdx.x; i < total; i += MS_THREADS) {
         const unsigned long long p = sm.buf[i];
         const uint32_t b = bin_of(p);
-        const unsigned long long pos = sm.base[b] + (i - sm.start[b]);
-        const ulonglong2 sc = slot(b);
-        if (pos < sc.y)
-            out[sc.x + pos] = p;
+        const unsigned long long pos = sm.base[b] + i;
+        if (pos < sm.endp[b])
+            out[pos] = p;
         else
             over = true;
     }
     __syncthreads();  // the smem is reused by the next tile
     return over;
+}
+
+// One tile: elements [e0, e1), element (j, t) = e0 + j*MS_THREADS + t.
+// get(e, pair, bin) -> false to skip; bins < nb <= MS_MAXB.  Needs
+// MsSmem::bytes(nb) of dynamic smem.
+template <class Get, class BinOf, class Slot>
+__device__ __forceinline__ bool ms_tile(Get get, BinOf bin_of, Slot slot, unsigned long long e0,
+                                        unsigned long long e1, uint32_t nb, int nbits,
+                                        unsigned long long* __restrict__ cursor,
+                                        unsigned long long* __restrict__ out, MsSmem& sm) {
+    (void)nbits;
+    unsigned long long pr[MS_ITEMS];
+    uint32_t bn[MS_ITEMS];
+#pragma unroll
+    for (int j = 0; j < MS_ITEMS; ++j) {
+        const unsigned long long e = e0 + (unsigned long long)j * MS_THREADS + threadIdx.x;
+        uint32_t b = 0;
+        pr[j] = 0;
+        const bool ok = e < e1 && get(e, pr[j], b) && b < nb;
+        bn[j] = ok ? b : (uint32_t)MS_MAXB;
+    }
+    return ms_split<MS_ITEMS>(pr, bn, bin_of, slot, nb, cursor, out, sm);
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk staging: a persistent CTA streams its next input tile into shared
+// memory (cp.async.bulk, completion on an mbarrier) while it splits the
+// current one, so the loads never stall the sort.
+constexpr int MS2_ITEMS = 16;
+constexpr int MS2_TILE = MS_THREADS * MS2_ITEMS;  // 4096 elements
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// bytes: multiple of 16, src/dst 16-B aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "SG_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra SG_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
 }  // namespace sg
