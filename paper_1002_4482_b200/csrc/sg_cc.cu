@@ -41,7 +41,13 @@ constexpr int COMP_THREADS = 256;
 // the range check
 
 struct EdgesU32 {
+    static constexpr uint32_t kBytes = 8;
     const uint2* e;
+    __device__ static void decode(const void* p, uint32_t i, unsigned long long& u, unsigned long long& v) {
+        const uint2 x = reinterpret_cast<const uint2*>(p)[i];
+        u = x.x;
+        v = x.y;
+    }
     __device__ __forceinline__ void load(unsigned long long i, unsigned long long& u, unsigned long long& v) const {
         const uint2 x = __ldcs(e + i);
         u = x.x;
@@ -49,7 +55,13 @@ struct EdgesU32 {
     }
 };
 struct EdgesI32 {
+    static constexpr uint32_t kBytes = 8;
     const int2* e;
+    __device__ static void decode(const void* p, uint32_t i, unsigned long long& u, unsigned long long& v) {
+        const int2 x = reinterpret_cast<const int2*>(p)[i];
+        u = (unsigned long long)(long long)x.x;
+        v = (unsigned long long)(long long)x.y;
+    }
     __device__ __forceinline__ void load(unsigned long long i, unsigned long long& u, unsigned long long& v) const {
         const int2 x = __ldcs(e + i);
         u = (unsigned long long)(long long)x.x;
@@ -57,7 +69,13 @@ struct EdgesI32 {
     }
 };
 struct EdgesI64 {
+    static constexpr uint32_t kBytes = 16;
     const longlong2* e;
+    __device__ static void decode(const void* p, uint32_t i, unsigned long long& u, unsigned long long& v) {
+        const longlong2 x = reinterpret_cast<const longlong2*>(p)[i];
+        u = (unsigned long long)x.x;
+        v = (unsigned long long)x.y;
+    }
     __device__ __forceinline__ void load(unsigned long long i, unsigned long long& u, unsigned long long& v) const {
         const longlong2 x = __ldcs(e + i);
         u = (unsigned long long)x.x;
@@ -264,28 +282,59 @@ __device__ __forceinline__ int part_of(E edges, unsigned long long e, unsigned l
     return (int)((u > v ? u : v) >> shift);
 }
 
-// partition sizes: per-tile counts (warp-aggregated in shared memory), one
-// atomic per partition per tile into the global totals; validates rows
+// partition sizes: persistent CTAs; per 32 edges a warp takes five ballots
+// (valid + 4 partition bits) and lane p keeps partition p's count in a
+// register; one atomic per partition per CTA at the end.  Validates rows.
 template <class E>
 __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigned long long m, unsigned long long n,
                                                                 uint32_t shift, int P,
                                                                 unsigned long long* __restrict__ totals,
                                                                 unsigned long long* flags) {
-    __shared__ uint32_t s_cnt[MAX_PARTS + 1];
-    if (threadIdx.x <= MAX_PARTS) s_cnt[threadIdx.x] = 0;
+    __shared__ unsigned long long s_cnt[MAX_PARTS];
+    if (threadIdx.x < MAX_PARTS) s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    const unsigned long long e0 = (unsigned long long)blockIdx.x * PART_TILE + threadIdx.x;
     const uint32_t lane = lane_id();
-#pragma unroll 4
-    for (int j = 0; j < PART_ITEMS; ++j) {
-        uint2 uv;
-        int p = part_of(edges, e0 + (unsigned long long)j * PART_THREADS, m, n, shift, flags, true, uv);
-        if (p < 0) p = MAX_PARTS;
-        const unsigned mm = __match_any_sync(0xffffffffu, p);
-        if (lane == (uint32_t)(__ffs(mm) - 1) && p < MAX_PARTS) atomicAdd(&s_cnt[p], (uint32_t)__popc(mm));
+    unsigned long long mine = 0;  // edges of partition `lane` seen by this warp
+    const unsigned long long ntiles = (m + PART_TILE - 1) / PART_TILE;
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long e0 = tile * PART_TILE + threadIdx.x;
+        unsigned long long uu[PART_ITEMS], vv[PART_ITEMS];
+#pragma unroll
+        for (int j = 0; j < PART_ITEMS; ++j) {  // all loads in flight before any validation atomic
+            const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
+            uu[j] = n;
+            vv[j] = n;
+            if (e < m) edges.load(e, uu[j], vv[j]);
+        }
+        int pp[PART_ITEMS];
+#pragma unroll
+        for (int j = 0; j < PART_ITEMS; ++j) {
+            const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
+            pp[j] = -1;
+            if (e < m) {
+                if (uu[j] >= n || vv[j] >= n)
+                    atomicMax(flags + 1, ~e);
+                else if (uu[j] == vv[j])
+                    atomicMax(flags + 2, ~e);
+                else
+                    pp[j] = (int)((uu[j] > vv[j] ? uu[j] : vv[j]) >> shift);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < PART_ITEMS; ++j) {
+            const int p = pp[j];
+            unsigned msk = __ballot_sync(0xffffffffu, p >= 0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const unsigned b = __ballot_sync(0xffffffffu, p >= 0 && ((p >> k) & 1));
+                msk &= ((lane >> k) & 1u) ? b : ~b;
+            }
+            mine += __popc(msk);
+        }
     }
+    if (lane < (uint32_t)P && mine) atomicAdd(&s_cnt[lane], mine);
     __syncthreads();
-    if (threadIdx.x < P && s_cnt[threadIdx.x]) atomicAdd(totals + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
+    if (threadIdx.x < (uint32_t)P && s_cnt[threadIdx.x]) atomicAdd(totals + threadIdx.x, s_cnt[threadIdx.x]);
 }
 
 // off_part = exclusive prefix of the P totals (off_part[P] = valid edges)
@@ -330,6 +379,67 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_cc_part_scatter(E edges, unsi
          e0 += (unsigned long long)gridDim.x * MS_TILE)
         ms_tile(get, bin_of, slot, e0, min(e0 + MS_TILE, m), (uint32_t)P, nbits, cursor,
                 reinterpret_cast<unsigned long long*>(out), sm);
+}
+
+// TMA-staged scatter (persistent, 2 CTAs per SM): the next 4096-edge tile
+// streams into shared memory while the current one is split.
+constexpr int PART2_CTAS_PER_SM = 2;
+
+template <class E>
+__global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatter2(
+    E edges, unsigned long long m, unsigned long long n, uint32_t shift, int P,
+    const unsigned long long* __restrict__ off_part, unsigned long long* __restrict__ cursor, uint2* __restrict__ out) {
+    extern __shared__ __align__(128) unsigned char ms_raw[];
+    unsigned char* stage = ms_raw;
+    MsSmem sm = MsSmem::carve(ms_raw + MS2_TILE * E::kBytes, (uint32_t)P, MS2_TILE);
+    __shared__ unsigned long long bar;
+    const unsigned long long ntiles = (m + MS2_TILE - 1) / MS2_TILE;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    auto issue = [&](unsigned long long tile) {
+        if (threadIdx.x == 0 && tile < ntiles) {
+            const unsigned long long e0 = tile * MS2_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, m - e0);
+            const uint32_t full = cnt * E::kBytes & ~15u;  // whole 16-B units by bulk copy, the rest below
+            if (full) {
+                mbar_expect_tx(&bar, full);
+                bulk_g2s(stage, reinterpret_cast<const unsigned char*>(edges.e) + e0 * E::kBytes, full, &bar);
+            } else {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
+            }
+        }
+    };
+    auto bin_of = [&](unsigned long long pr) {
+        const uint32_t u = (uint32_t)pr, v = (uint32_t)(pr >> 32);
+        return (u > v ? u : v) >> shift;
+    };
+    auto slot = [&](uint32_t b) { return make_ulonglong2(off_part[b], off_part[b + 1] - off_part[b]); };
+    uint32_t phase = 0;
+    issue(blockIdx.x);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long e0 = tile * MS2_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, m - e0);
+        const uint32_t staged = (cnt * E::kBytes & ~15u) / E::kBytes;
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        unsigned long long pr[MS2_ITEMS];
+        uint32_t bn[MS2_ITEMS];
+#pragma unroll
+        for (int j = 0; j < MS2_ITEMS; ++j) {
+            const uint32_t e = j * MS_THREADS + threadIdx.x;
+            unsigned long long u = n, v = n;
+            if (e < staged)
+                E::decode(stage, e, u, v);
+            else if (e < cnt)
+                edges.load(e0 + e, u, v);  // the odd tail element of the last tile
+            const bool ok = u < n && v < n && u != v;
+            pr[j] = ((unsigned long long)(uint32_t)v << 32) | (uint32_t)u;
+            bn[j] = ok ? (uint32_t)((u > v ? u : v) >> shift) : (uint32_t)MS_MAXB;
+        }
+        __syncthreads();  // staging consumed: refill it behind the split
+        issue(tile + gridDim.x);
+        ms_split<MS2_ITEMS>(pr, bn, bin_of, slot, (uint32_t)P, cursor, reinterpret_cast<unsigned long long*>(out), sm);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -407,15 +517,26 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
     const uint32_t nt = (uint32_t)p.ntiles;
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * MAX_PARTS, s));
-    k_cc_part_count<E><<<nt, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.totals, flags);
+    const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
+    k_cc_part_count<E><<<cg, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.totals, flags);
     SG_LAUNCH_CHECK();
     k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
-    const size_t smem = MsSmem::bytes((uint32_t)p.parts);
-    SG_CUDA(cudaFuncSetAttribute(k_cc_part_scatter<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned long long ntile = (m + MS_TILE - 1) / MS_TILE;
-    const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * 4 ? ntile : kSMs * 4);
-    k_cc_part_scatter<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
+    if (((uintptr_t)view.e & 15) == 0) {
+        const size_t smem = (size_t)MS2_TILE * E::kBytes + MsSmem::bytes((uint32_t)p.parts, MS2_TILE);
+        SG_CUDA(cudaFuncSetAttribute(k_cc_part_scatter2<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const unsigned long long ntile = (m + MS2_TILE - 1) / MS2_TILE;
+        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * PART2_CTAS_PER_SM ? ntile
+                                                                                            : kSMs * PART2_CTAS_PER_SM);
+        k_cc_part_scatter2<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor,
+                                                           b.edges);
+    } else {
+        const size_t smem = MsSmem::bytes((uint32_t)p.parts);
+        SG_CUDA(cudaFuncSetAttribute(k_cc_part_scatter<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const unsigned long long ntile = (m + MS_TILE - 1) / MS_TILE;
+        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * 4 ? ntile : kSMs * 4);
+        k_cc_part_scatter<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
+    }
     SG_LAUNCH_CHECK();
     return SG_OK;
 }
@@ -531,6 +652,7 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
         viol->pad = 0;
     }
     const CcPlan plan = plan_cc(n, m);
+    ms_configure();
     Carver c(ws, ws_bytes);
     unsigned long long* flags;
     uint32_t* Dws;

@@ -1692,6 +1692,7 @@ template <class SuccT, class OutT>
 static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
                     cudaStream_t s, sg_stats* stats, sg_violation* viol) {
     const RsPlan p = plan_rs(n, seed, (int)sizeof(OutT));
+    ms_configure();
     Carver c(ws, ws_bytes);
     RsBufs b;
     if (!carve_rs(c, n, p, b)) return SG_ERR_WORKSPACE;

@@ -13,6 +13,8 @@
 // One global atomic per (tile, bin) claims the tile's slots of a bin.
 #pragma once
 
+#include <stdlib.h>
+
 #include "sg_internal.cuh"
 
 namespace sg {
@@ -22,6 +24,17 @@ constexpr int MS_WARPS = MS_THREADS / 32;
 constexpr int MS_ITEMS = 8;
 constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
 constexpr int MS_MAXB = 1024;
+
+// peer ranking: 0 match.any, 1 ballots (SG_MS_PEERS, for measurement)
+static __constant__ int g_ms_peers = 1;
+
+static inline void ms_configure() {
+    const char* e = getenv("SG_MS_PEERS");
+    if (e && *e) {
+        const int v = atoi(e) ? 1 : 0;
+        cudaMemcpyToSymbol(g_ms_peers, &v, sizeof(int));
+    }
+}
 
 // dynamic shared memory layout for nb bins
 struct MsSmem {
@@ -66,14 +79,19 @@ __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], 
     const int nbits = 32 - __clz(nb > 1 ? nb - 1 : 1);
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
-        // peers: lanes with the same bin (bit-by-bit ballots; the VOTE unit
-        // is much faster than match.any on this part)
-        const bool valid = bn[j] < nb;
-        const unsigned vb = __ballot_sync(0xffffffffu, valid);
-        unsigned peers = valid ? vb : ~vb;
-        for (int k = 0; k < nbits; ++k) {
-            const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
-            peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+        // peers: lanes with the same bin
+        unsigned peers;
+        if (g_ms_peers == 0) {
+            peers = __match_any_sync(0xffffffffu, bn[j]);
+        } else {
+            // bit-by-bit ballots (VOTE is an ALU op; match.any queues on MIO)
+            const bool valid = bn[j] < nb;
+            const unsigned vb = __ballot_sync(0xffffffffu, valid);
+            peers = valid ? vb : ~vb;
+            for (int k = 0; k < nbits; ++k) {
+                const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
+                peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+            }
         }
         const int leader = __ffs(peers) - 1;
         uint32_t old = 0;
