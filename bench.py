@@ -42,10 +42,28 @@ WORKLOADS = {
 
 # SURVEY §8(d) algorithmic bytes
 LR_BYTES_PER_NODE = {"random": 116, "ordered": 40}       # whole ranking
-LR_WALK_BYTES_PER_NODE = {"random": 96, "ordered": 20}   # RS3 walk alone (3 x 32 B sectors / 20 B payload)
-WY_BYTES_PER_NODE_ROUND = 48                              # own word 8 + gather 32 + write 8
 CC_EDGE_SWEEP_BYTES = 72                                  # 8 B edge + 2 x 32 B parent gathers
 CC_VERTEX_SWEEP_BYTES = 40                                # 4 B + 32 B gather + 4 B write
+
+# Algorithmic bytes per unit (node / edge) for each kernel of the step, used
+# for the dominant kernel's roofline.  rs3_walk and the CC hooks use SURVEY
+# §8(d)'s per-access figures (every data-dependent access to an array >> L2
+# charged one 32-B sector); the streaming passes are charged the bytes they
+# must move.  out = bytes per output rank (4 device-resident, 8 int64).
+def kernel_bytes(kernel, order, out):
+    return {
+        "rs3_walk": 96 if order == "random" else 20,   # RS3: packed write + succ[cur] + packed read (listrank.py:279-283)
+        "rs5_partition": 12 + 8,                       # record {cur, sid|local} in, {cur, rank} pair out
+        "rs5_refine": 8 + 8,
+        "rs5_scatter": 8 + out,
+        "rs3_contract": 4,                             # succ in (segments out are O(n / 4096))
+        "rs5_expand": 4 + out,                         # succ in, rank out
+        "rs1_validate": 4,
+        "cc_hook_uf": CC_EDGE_SWEEP_BYTES,
+        "cc_hook_sv": CC_EDGE_SWEEP_BYTES,
+        "cc_partition": 8 + 8 + 8,                     # count pass reads the pairs; scatter reads + writes them
+        "wy_jump": 48,
+    }.get(kernel)
 
 
 def parse():
@@ -74,13 +92,16 @@ def load_peaks():
 
 
 def load_traffic(workload, kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    """DRAM bytes per step of `kernel` from the committed ncu capture
     (profiles/traffic.json, written by tools/ncu_summary.py), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(workload, {}).get(kernel)
+            w = json.load(f).get(workload, {})
     except Exception:
         return None
+    if kernel == "cc_partition" and "cc_partition_scatter" in w:
+        return w.get("cc_partition_count", 0) + w["cc_partition_scatter"]
+    return w.get(kernel)
 
 
 class ClockSampler:
@@ -177,7 +198,9 @@ def main():
     unit = "M nodes/s" if kind == "list" else "M edges/s"
     config = {"workload": a.workload, "n": n}
     if kind == "list":
-        config.update(order=order, p=a.p, algorithm="rs_rank (recursive sparse ruling set)",
+        config.update(order=order, p=a.p,
+                      algorithm="rs_rank: recursive sparse ruling set (scattered layouts) / tile contraction "
+                                "(local layouts)",
                       inputs="device-resident u32 successors",
                       l2="inputs (4n B) > 126 MB L2, no flush" if n >= (1 << 26) else "L2 flushed between steps")
     else:
@@ -273,29 +296,32 @@ def main():
 
     # ---- dominant kernel roofline --------------------------------------------------
     peak, peak_src = load_peaks()
+    units = n if kind == "list" else m
+    step_kern = {k: sum(v) / a.steps for k, v in kern_ms.items()}        # ms per step, per kernel
+    launches_per_step = {k: len(v) / a.steps for k, v in kern_ms.items()}
+    kname = max(step_kern, key=step_kern.get)
+    out_bytes = 4
+    bpu = kernel_bytes(kname, order, out_bytes)
+    k_units = units // world if (kind == "cc" and world > 1 and kname.startswith("cc_")) else units
+    k_ms = step_kern[kname]
+    algo_bytes = bpu * k_units if bpu is not None else None
+    achieved = (algo_bytes / (k_ms / 1e3) / 1e9) if (algo_bytes and k_ms) else None
     if kind == "list":
-        kname = "rs3_walk"
-        algo_bytes = LR_WALK_BYTES_PER_NODE[order] * n
         pipe_bytes = LR_BYTES_PER_NODE[order] * n
     else:
-        kname = "cc_hook_uf" if a.variant == "uf" else "cc_hook_sv"
-        sweeps = st.meta["edge_sweeps"]
-        algo_bytes = CC_EDGE_SWEEP_BYTES * (m // world if world > 1 else m)
-        pipe_bytes = sweeps * CC_EDGE_SWEEP_BYTES * m + st.meta["vertex_sweeps"] * CC_VERTEX_SWEEP_BYTES * n
-    kt = kern_ms.get(kname, [])
-    k_ms = (sum(kt) / len(kt)) if kt else None
-    if kind == "cc" and k_ms and st.meta.get("edge_sweeps", 1) > 1 and a.variant == "sv":
-        pass  # per-launch average already is one sweep
-    achieved = (algo_bytes / (k_ms / 1e3) / 1e9) if k_ms else None
+        pipe_bytes = st.meta["edge_sweeps"] * CC_EDGE_SWEEP_BYTES * m + st.meta["vertex_sweeps"] * CC_VERTEX_SWEEP_BYTES * n
     traffic = load_traffic(a.workload, kname)
     roofline = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1) if achieved else None,
                 "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
-                "traffic": traffic, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
-                "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": round(k_ms, 4) if k_ms else None,
-                "kernel_share_of_step": round(sum(kt) / sum(step_ms), 3) if kt else None,
+                "traffic": traffic, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)",
+                "algorithmic_bytes_per_unit": bpu, "units_per_step": k_units,
+                "algorithmic_bytes_per_step": algo_bytes, "kernel_ms_per_step": round(k_ms, 4),
+                "launches_per_step": launches_per_step[kname],
+                "kernel_share_of_step": round(k_ms / ms_per_step, 3),
+                "traffic_note": "dram__bytes_read+write per step from the committed ncu capture (profiles/)",
                 "pipeline": {"algorithmic_bytes": pipe_bytes,
-                             "achieved": round(pipe_bytes * (1 if kind == "cc" or world == 1 else 1)
-                                               / (ms_per_step / 1e3) / 1e9, 1),
+                             "bytes_per_unit": (LR_BYTES_PER_NODE[order] if kind == "list" else None),
+                             "achieved": round(pipe_bytes / (ms_per_step / 1e3) / 1e9, 1),
                              "frac": round(pipe_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4)}}
     kernels = {k: round(sum(v) / len(v), 4) for k, v in sorted(kern_ms.items())}
 
@@ -343,8 +369,8 @@ def main():
                           "vertex_sweeps": st.meta["vertex_sweeps"],
                           "components": st.meta["roots_per_round"][-1]}
         else:
-            line["ruling_set"] = {"levels": st.meta["levels"], "level_size": st.meta["level_size"],
-                                  "fallback": st.meta["fallback"]}
+            line["ruling_set"] = {"path": st.meta["path"], "levels": st.meta["levels"],
+                                  "level_size": st.meta["level_size"], "fallback": st.meta["fallback"]}
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.barrier()

@@ -1012,6 +1012,7 @@ struct ContractSmem {
     uint16_t rid[TILE];      // node -> local ruler index (walk); end node -> tile-local segment     [sw16]
     uint16_t term[TILE];     // ruler -> end node of its segment
     uint8_t pred[TILE];      // node has an in-tile predecessor
+    uint16_t brk[TILE / 16]; // per 16-id block: bit q = id q's successor is not id q + 1
 };
 
 // Bank swizzles for node-indexed arrays.  Walkers start 16 nodes apart (one
@@ -1023,13 +1024,12 @@ struct ContractSmem {
 __device__ __forceinline__ uint32_t sw32(uint32_t l) { return l ^ (((l >> 5) & 3u) << 2) ^ ((l >> 7) & 3u); }
 __device__ __forceinline__ uint32_t sw16(uint32_t l) { return l ^ (((l >> 6) & 7u) << 2); }
 
-template <class SuccT, class OutT, bool kExpand, bool kVec>
+template <class SuccT, bool kVec>
 __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
     const SuccT* __restrict__ succ, ListStatus* st, const uint32_t* __restrict__ tile_off,
     uint32_t* __restrict__ headsid, uint32_t* __restrict__ seg_head, uint32_t* __restrict__ seg_succ,
-    uint2* __restrict__ lvl1, const uint32_t* __restrict__ IS1, OutT* __restrict__ rank) {
+    uint2* __restrict__ lvl1, uint32_t* __restrict__ node_word) {
     if (!layout_local(st)) return;
-    if (kExpand && (st->overflow || st->bad)) return;
     constexpr int VEC = 4;  // ids per thread and vector access
     constexpr int NV = TILE_ITEMS / VEC;
     extern __shared__ __align__(16) unsigned char ct_raw[];
@@ -1040,6 +1040,7 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
     const unsigned long long R1 = st->R[1];
     const unsigned long long ntiles = (N + TILE - 1) / TILE;
     const uint32_t t = threadIdx.x;
+    const uint32_t lane = lane_id();
     static_assert(TILE == TILE_THREADS * 16, "one uint4 of predecessor flags per thread");
     bool bad = false;
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1048,20 +1049,19 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
         const bool full = kVec && tn == TILE;
         // 1. successors -> in-tile links, predecessor flags (plain byte
         //    stores: a node with two in-tile predecessors shows up as fewer
-        //    flags than links).  Thread t holds ids 4(j*256+t) .. +3.
+        //    flags than links), run-break masks.  Thread t holds ids
+        //    4(j*256+t) .. +3.
         SuccT v[TILE_ITEMS];
         if (full) {
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
                 const SuccT* p = succ + base + (size_t)(j * TILE_THREADS + t) * VEC;
                 if (sizeof(SuccT) == 4) {
-                    const uint4 w = kExpand ? __ldcs(reinterpret_cast<const uint4*>(p)) : *reinterpret_cast<const uint4*>(p);
+                    const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p));
                     v[j * 4 + 0] = (SuccT)w.x, v[j * 4 + 1] = (SuccT)w.y, v[j * 4 + 2] = (SuccT)w.z, v[j * 4 + 3] = (SuccT)w.w;
                 } else {
-                    const ulonglong2 w0 = kExpand ? __ldcs(reinterpret_cast<const ulonglong2*>(p))
-                                                  : *reinterpret_cast<const ulonglong2*>(p);
-                    const ulonglong2 w1 = kExpand ? __ldcs(reinterpret_cast<const ulonglong2*>(p) + 1)
-                                                  : *(reinterpret_cast<const ulonglong2*>(p) + 1);
+                    const ulonglong2 w0 = __ldcs(reinterpret_cast<const ulonglong2*>(p));
+                    const ulonglong2 w1 = __ldcs(reinterpret_cast<const ulonglong2*>(p) + 1);
                     v[j * 4 + 0] = (SuccT)w0.x, v[j * 4 + 1] = (SuccT)w0.y, v[j * 4 + 2] = (SuccT)w1.x, v[j * 4 + 3] = (SuccT)w1.y;
                 }
             }
@@ -1081,6 +1081,7 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
         for (int j = 0; j < NV; ++j) {
             const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
             uint16_t nx[VEC];
+            uint32_t nib = 0;  // run breaks: nx[l] != l + 1
 #pragma unroll
             for (int c = 0; c < VEC; ++c) {
                 const uint32_t l = l0 + c;
@@ -1093,12 +1094,18 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                         ++links;
                     }
                 }
+                if (nx[c] != l + 1) nib |= 1u << c;
             }
             *reinterpret_cast<ushort4*>(&S.nx[sw16(l0)]) = make_ushort4(nx[0], nx[1], nx[2], nx[3]);
             *reinterpret_cast<uint4*>(&S.own[sw32(l0) & ~3u]) = make_uint4(~0u, ~0u, ~0u, ~0u);
+            // the 4 nibbles of a 16-id block sit in 4 consecutive lanes
+            uint32_t m16 = nib << (4 * (lane & 3));
+            m16 |= __shfl_xor_sync(0xffffffffu, m16, 1);
+            m16 |= __shfl_xor_sync(0xffffffffu, m16, 2);
+            if ((lane & 3) == 0) S.brk[l0 >> 4] = (uint16_t)m16;
         }
         __syncthreads();
-        if (!kExpand && tile == 0 && S.pred[0]) bad = true;  // node 0 must start the list
+        if (tile == 0 && S.pred[0]) bad = true;  // node 0 must start the list
         // 2. local rulers (blocked: thread t owns nodes 16t .. 16t+15): heads
         //    and every CT_STRIDE-th node; numbered in index order
         uint32_t rflags = 0, hflags = 0;
@@ -1119,7 +1126,7 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
         BS(scan_tmp).ExclusiveSum(packed, pre, tot);
         const uint32_t rpre = (uint32_t)(pre >> 32), hpre = (uint32_t)(pre >> 16) & 0xFFFFu;
         const uint32_t K = (uint32_t)(tot >> 32), H = (uint32_t)(tot >> 16) & 0xFFFFu;
-        if (!kExpand && H + (uint32_t)(tot & 0xFFFFu) != tn) bad = true;  // two in-tile predecessors
+        if (H + (uint32_t)(tot & 0xFFFFu) != tn) bad = true;  // two in-tile predecessors
 #pragma unroll
         for (int g = 0; g < TILE_ITEMS / 4; ++g) {
             uint16_t r[4];
@@ -1132,12 +1139,27 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
         }
         __syncthreads();
         // 3. each thread walks from its own local rulers to the next local
-        //    ruler / the segment end
+        //    ruler / the segment end.  A run of +1 successors inside a 16-id
+        //    block is crossed in one step (no ruler can sit inside it: its
+        //    nodes have in-tile predecessors and are not 16-aligned); the
+        //    block start after a full run is a ruler.
         for (uint32_t rem = rflags; rem != 0; rem &= rem - 1) {
             const uint32_t q = __ffs(rem) - 1;
             const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
             uint32_t l = t * TILE_ITEMS + q, off = 0;
             for (;;) {
+                const uint32_t m = (uint32_t)S.brk[l >> 4] >> (l & 15u);
+                const uint32_t r = m ? (uint32_t)(__ffs(m) - 1) : 16u - (l & 15u);
+                if (r) {
+                    for (uint32_t j = 0; j < r; ++j) S.own[sw32(l + j)] = (k << 16) | (off + j);
+                    l += r;
+                    off += r;
+                    if (m == 0) {  // l: the next block's first id, a ruler
+                        S.link[k] = ((uint32_t)S.rid[sw16(l)] << 16) | off;
+                        S.term[k] = CT_END;
+                        break;
+                    }
+                }
                 S.own[sw32(l)] = (k << 16) | off;
                 const uint16_t nx = S.nx[sw16(l)];
                 if (nx == CT_END) {
@@ -1148,7 +1170,7 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                 const uint16_t r2 = S.rid[sw16(nx)];
                 if (r2 != CT_END || off + 1 >= TILE) {  // the cap only trips on invalid lists
                     if (r2 == CT_END) bad = true;
-                    S.link[k] = ((uint32_t)(r2 == CT_END ? k : r2) << 16) | (off + 1);
+                    S.link[k] = ((uint32_t)(r2 == CT_END ? k : r2) << 16) | ((off + 1) & 0xFFFFu);
                     S.term[k] = CT_END;
                     break;
                 }
@@ -1189,20 +1211,16 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                 e = (b >> 16) == CT_END ? S.term[p] : CT_END;
             }
         };
-        if (!kExpand) {
-            for (uint32_t k = t; k < K; k += TILE_THREADS) {
-                uint32_t d;
-                uint16_t e;
-                seg_end(k, d, e);
-                if (e == CT_END) bad = true;  // a cycle through local rulers
-            }
-            for (uint32_t l = t; l < tn; l += TILE_THREADS)
-                if (S.own[sw32(l)] == 0xFFFFFFFFu) bad = true;  // a cycle without local rulers
+        for (uint32_t k = t; k < K; k += TILE_THREADS) {
+            uint32_t d;
+            uint16_t e;
+            seg_end(k, d, e);
+            if (e == CT_END) bad = true;  // a cycle through local rulers
         }
         // 5. segments: numbered by head index; end node -> tile-local segment
         const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
                                                 : (uint32_t)(R1 - tile_off[tile]);
-        if (!kExpand && segs != H) bad = true;
+        if (segs != H) bad = true;
         __syncthreads();  // rid[] is rewritten below
         for (uint32_t rem = hflags; rem != 0; rem &= rem - 1) {
             const uint32_t q = __ffs(rem) - 1;
@@ -1212,7 +1230,7 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
             uint16_t e;
             seg_end(k, d, e);
             if (e != CT_END) S.rid[sw16(e)] = (uint16_t)h;
-            if (!kExpand && h < segs && e != CT_END) {
+            if (h < segs && e != CT_END) {
                 const unsigned long long sid = (unsigned long long)tile_off[tile] + h;
                 const uint32_t l = t * TILE_ITEMS + q;
                 seg_head[sid] = (uint32_t)(base + l);
@@ -1222,48 +1240,76 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                 seg_succ[sid] = (x >= N || x == base + e) ? NIL : (uint32_t)x;
             }
         }
-        if (kExpand) {
-            __syncthreads();
-            const unsigned long long t0 = tile_off[tile];
-            auto rank_of = [&](uint32_t o) -> uint32_t {
-                uint32_t r = 0;
-                if (o != 0xFFFFFFFFu) {  // always, for lists that passed the contraction checks
-                    uint32_t d;
-                    uint16_t e;
-                    seg_end(o >> 16, d, e);
-                    const unsigned long long sid = t0 + (e != CT_END ? S.rid[sw16(e)] : 0xFFFFu);
-                    if (sid < R1) r = __ldg(IS1 + sid) - __ldg(&lvl1[sid].y) + (d - (o & 0xFFFFu));
-                }
-                return r;
-            };
+        __syncthreads();
+        // 6. per node: {tile-local segment : 16 | distance to the segment end : 16}
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
-                const uint32_t g = sw32(l0);
-                const uint4 ow4 = *reinterpret_cast<const uint4*>(&S.own[g & ~3u]);
-                const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
-                OutT r[VEC];
+        for (int j = 0; j < NV; ++j) {
+            const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
+            const uint32_t g = sw32(l0);
+            const uint4 ow4 = *reinterpret_cast<const uint4*>(&S.own[g & ~3u]);
+            const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
+            uint32_t wd[VEC];
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) r[c] = (OutT)rank_of(ow[c ^ (g & 3u)]);
-                if (full) {
-                    if (sizeof(OutT) == 4) {
-                        __stcs(reinterpret_cast<uint4*>(rank + base + l0),
-                               make_uint4((uint32_t)r[0], (uint32_t)r[1], (uint32_t)r[2], (uint32_t)r[3]));
+            for (int c = 0; c < VEC; ++c) {
+                const uint32_t o = ow[c ^ (g & 3u)];
+                wd[c] = 0xFFFFFFFFu;
+                if (l0 + c < tn) {
+                    if (o == 0xFFFFFFFFu) {
+                        bad = true;  // a cycle without local rulers
                     } else {
-                        ulonglong2* q = reinterpret_cast<ulonglong2*>(rank + base + l0);
-                        __stcs(q, make_ulonglong2((unsigned long long)r[0], (unsigned long long)r[1]));
-                        __stcs(q + 1, make_ulonglong2((unsigned long long)r[2], (unsigned long long)r[3]));
+                        uint32_t d;
+                        uint16_t e;
+                        seg_end(o >> 16, d, e);
+                        if (e != CT_END) wd[c] = ((uint32_t)S.rid[sw16(e)] << 16) | ((d - (o & 0xFFFFu)) & 0xFFFFu);
                     }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < VEC; ++c)
-                        if (l0 + c < tn) rank[base + l0 + c] = r[c];
                 }
+            }
+            if (full) {
+                *reinterpret_cast<uint4*>(node_word + base + l0) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < VEC; ++c)
+                    if (l0 + c < tn) node_word[base + l0 + c] = wd[c];
             }
         }
         __syncthreads();  // shared memory is reused by the next tile
     }
     if (bad) st->bad = 1;
+}
+
+// expand the contraction: rank = (IS1[segment] - length) + distance to the
+// segment end; two streaming 4-B accesses per node plus L1-resident gathers
+template <class OutT, bool kVec>
+__global__ void __launch_bounds__(256) k_rs_contract_expand(const uint32_t* __restrict__ node_word,
+                                                            const uint32_t* __restrict__ tile_off,
+                                                            const uint2* __restrict__ lvl1,
+                                                            const uint32_t* __restrict__ IS1, OutT* __restrict__ rank,
+                                                            const ListStatus* st) {
+    if (!layout_local(st) || st->overflow || st->bad) return;
+    const unsigned long long N = st->R[0];
+    const unsigned long long R1 = st->R[1];
+    auto rank_of = [&](unsigned long long i, uint32_t w) -> uint32_t {
+        const unsigned long long sid = (unsigned long long)__ldg(tile_off + (i / TILE)) + (w >> 16);
+        return sid < R1 ? __ldg(IS1 + sid) - __ldg(&lvl1[sid].y) + (w & 0xFFFFu) : 0u;
+    };
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long nq = kVec ? N / 4 : 0;
+    for (unsigned long long qd = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; qd < nq; qd += stride) {
+        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(node_word) + qd);
+        const unsigned long long i = qd * 4;
+        const uint32_t r0 = rank_of(i, w.x), r1 = rank_of(i + 1, w.y), r2 = rank_of(i + 2, w.z),
+                       r3 = rank_of(i + 3, w.w);
+        if (sizeof(OutT) == 4) {
+            __stcs(reinterpret_cast<uint4*>(rank) + qd, make_uint4(r0, r1, r2, r3));
+        } else {
+            ulonglong2* q = reinterpret_cast<ulonglong2*>(rank) + 2 * qd;
+            __stcs(q, make_ulonglong2(r0, r1));
+            __stcs(q + 1, make_ulonglong2(r2, r3));
+        }
+    }
+    for (unsigned long long i = nq * 4 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += stride)
+        rank[i] = (OutT)rank_of(i, node_word[i]);
 }
 
 // contracted list links: segment s -> the segment whose head is succ(end(s))
@@ -1470,16 +1516,15 @@ static int wyllie_run(const SuccT* succ, OutT* rank, uint64_t n, int variant, Li
     return SG_OK;
 }
 
-template <class SuccT, class OutT, bool kExpand>
-static int launch_contract(uint32_t grid, cudaStream_t s, const SuccT* succ, OutT* rank, ListStatus* st,
-                           const uint32_t* tile_off, uint32_t* headsid, uint32_t* seg_head, uint32_t* seg_succ,
-                           uint2* lvl1, const uint32_t* IS1) {
-    const bool vec = ((uintptr_t)succ & 15) == 0 && ((uintptr_t)rank & 15) == 0;
-    auto kv = k_rs_contract<SuccT, OutT, kExpand, true>;
-    auto ks = k_rs_contract<SuccT, OutT, kExpand, false>;
-    auto k = vec ? kv : ks;
+template <class SuccT>
+static int launch_contract(uint32_t grid, cudaStream_t s, const SuccT* succ, ListStatus* st, const uint32_t* tile_off,
+                           uint32_t* headsid, uint32_t* seg_head, uint32_t* seg_succ, uint2* lvl1,
+                           uint32_t* node_word) {
+    const bool vec = ((uintptr_t)succ & 15) == 0;
+    auto k = vec ? k_rs_contract<SuccT, true> : k_rs_contract<SuccT, false>;
     SG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ContractSmem)));
-    k<<<grid, TILE_THREADS, sizeof(ContractSmem), s>>>(succ, st, tile_off, headsid, seg_head, seg_succ, lvl1, IS1, rank);
+    k<<<grid, TILE_THREADS, sizeof(ContractSmem), s>>>(succ, st, tile_off, headsid, seg_head, seg_succ, lvl1,
+                                                       node_word);
     return SG_OK;
 }
 
@@ -1554,8 +1599,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             SG_LAUNCH_CHECK();
             const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
             rec.begin(K_RS_CONTRACT, 0, cg, TILE_THREADS, capN);
-            const int rc = launch_contract<SuccT, OutT, false>(cg, s, succ, (OutT*)nullptr, b.st, b.tiles, b.rid,
-                                                               b.spl[0], b.IS[1], b.lvl[1], nullptr);
+            const int rc = launch_contract<SuccT>(cg, s, succ, b.st, b.tiles, b.rid, b.spl[0], b.IS[1], b.lvl[1],
+                                                  reinterpret_cast<uint32_t*>(b.word0));
             if (rc != SG_OK) return rc;
             rec.end();
             SG_LAUNCH_CHECK();
@@ -1586,11 +1631,14 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     {  // local layouts: expand the contraction
         const uint32_t nt = (uint32_t)((n + TILE - 1) / TILE);
-        const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
-        rec.begin(K_RS5_EXPAND, 0, cg, TILE_THREADS, n);
-        int rc = launch_contract<SuccT, OutT, true>(cg, s, succ, rank, b.st, b.tiles, nullptr, nullptr, nullptr,
-                                                    b.lvl[1], b.IS[1]);
-        if (rc != SG_OK) return rc;
+        const uint32_t eg = grid_for(n / 4 + 1, 256, 1, kSMs * 8);
+        rec.begin(K_RS5_EXPAND, 0, eg, 256, n);
+        if (((uintptr_t)rank & 15) == 0)
+            k_rs_contract_expand<OutT, true><<<eg, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(b.word0), b.tiles,
+                                                                b.lvl[1], b.IS[1], rank, b.st);
+        else
+            k_rs_contract_expand<OutT, false><<<eg, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(b.word0), b.tiles,
+                                                                 b.lvl[1], b.IS[1], rank, b.st);
         rec.end();
         SG_LAUNCH_CHECK();
     }

@@ -44,6 +44,9 @@ def value(d, units, hdr, k):
 
 
 def short(kname):
+    if "k_rs_contract<" in kname:  # <SuccT, OutT, kExpand, kVec>
+        args = kname[kname.index("k_rs_contract<") + 14:].split(">")[0].split(", ")
+        return "rs5_expand" if len(args) > 2 and args[2] in ("(bool)1", "true") else "rs3_contract"
     for pat, nm in NAME_MAP.items():
         if pat in kname:
             return nm

@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Random-access ceilings of this B200 (development aid, not product code).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ubench_random tools/ubench_random.cu
 // Each test touches a 2 GiB array at hashed addresses; prints accesses/s.
@@ -96,6 +97,13 @@ __global__ void init(unsigned long long* a, uint32_t mask) {
 }
 
 int main() {
+    if (const char* f = getenv("UB_FETCH")) {  // cudaLimitMaxL2FetchGranularity experiment
+        size_t before = 0, after = 0;
+        cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(f));
+        cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
+        printf("L2 fetch granularity %zu -> %zu\n", before, after);
+    }
     const uint32_t n = 1u << 28;  // 2 GiB of u64
     const uint32_t mask = n - 1;
     unsigned long long *a, *w, *sink;
