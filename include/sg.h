@@ -158,6 +158,15 @@ int sg_rs_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype,
 int sg_gather_i64(const int64_t* src, const int64_t* idx, uint64_t k,
                   int64_t* out, void* stream);
 
+/* meta["splitter_set"] from the device ranks (listrank.py:252-357): for the
+ * r splitter nodes spl (int64, device), out (int64, device, 3 x r) receives
+ * the splitter ranks, the sublist lengths (to the next splitter in list
+ * order; the last to the tail) and the reduced successors (the last splitter
+ * points at itself).  One radix sort of the r ranks; n < 2^32. */
+size_t sg_splitter_meta_workspace_bytes(uint32_t r);
+int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t* spl,
+                     uint32_t r, int64_t* out, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- connected components ---------------------------------------------- */
 
 size_t sg_cc_workspace_bytes(uint64_t n, uint64_t m);
@@ -183,6 +192,14 @@ int sg_cc_init(uint32_t* D, uint64_t n, void* stream);
 int sg_cc_hook(const void* edges, int edge_dtype, uint64_t m, uint64_t row0,
                uint64_t n, uint32_t* D, int variant, int validate,
                uint64_t* flags, void* stream);
+/* As sg_cc_hook, for large n: the block is first split by 2^23-vertex window
+ * of the larger endpoint into `ws` (validating rows; reuse != 0 skips the
+ * split and hooks the copy a previous call left in `ws`), then hooked window
+ * by window so the parent gathers stay L2-resident. */
+size_t sg_cc_hook_workspace_bytes(uint64_t n, uint64_t m);
+int sg_cc_hook_part(const void* edges, int edge_dtype, uint64_t m, uint64_t row0,
+                    uint64_t n, uint32_t* D, int variant, int validate, uint64_t* flags,
+                    void* ws, size_t ws_bytes, int reuse, void* stream);
 /* D[i] = root(i) for lo <= i < hi; adds the number of roots in [lo,hi)
  * to *roots (device u64). */
 int sg_cc_compress(uint32_t* D, uint64_t lo, uint64_t hi, uint64_t* roots,

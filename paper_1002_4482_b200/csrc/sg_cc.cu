@@ -287,6 +287,7 @@ __device__ __forceinline__ int part_of(E edges, unsigned long long e, unsigned l
 // register; one atomic per partition per CTA at the end.  Validates rows.
 template <class E>
 __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigned long long m, unsigned long long n,
+                                                                unsigned long long row0,
                                                                 uint32_t shift, int P,
                                                                 unsigned long long* __restrict__ totals,
                                                                 unsigned long long* flags) {
@@ -313,9 +314,9 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
             pp[j] = -1;
             if (e < m) {
                 if (uu[j] >= n || vv[j] >= n)
-                    atomicMax(flags + 1, ~e);
+                    atomicMax(flags + 1, ~(row0 + e));
                 else if (uu[j] == vv[j])
-                    atomicMax(flags + 2, ~e);
+                    atomicMax(flags + 2, ~(row0 + e));
                 else
                     pp[j] = (int)((uu[j] > vv[j] ? uu[j] : vv[j]) >> shift);
             }
@@ -513,12 +514,12 @@ struct CcPartBufs {
 
 template <class E>
 static int partition_edges(E view, unsigned long long m, unsigned long long n, const CcPlan& p, CcPartBufs& b,
-                           unsigned long long* flags, cudaStream_t s) {
+                           unsigned long long* flags, cudaStream_t s, unsigned long long row0 = 0) {
     const uint32_t nt = (uint32_t)p.ntiles;
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
-    k_cc_part_count<E><<<cg, PART_THREADS, 0, s>>>(view, m, n, p.shift, p.parts, b.totals, flags);
+    k_cc_part_count<E><<<cg, PART_THREADS, 0, s>>>(view, m, n, row0, p.shift, p.parts, b.totals, flags);
     SG_LAUNCH_CHECK();
     k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
@@ -542,11 +543,11 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
 }
 
 static int partition_dispatch(const void* edges, int dt, unsigned long long m, unsigned long long n, const CcPlan& p,
-                              CcPartBufs& b, unsigned long long* flags, cudaStream_t s) {
+                              CcPartBufs& b, unsigned long long* flags, cudaStream_t s, unsigned long long row0 = 0) {
     switch (dt) {
-        case SG_U32: return partition_edges(EdgesU32{(const uint2*)edges}, m, n, p, b, flags, s);
-        case SG_I32: return partition_edges(EdgesI32{(const int2*)edges}, m, n, p, b, flags, s);
-        case SG_I64: return partition_edges(EdgesI64{(const longlong2*)edges}, m, n, p, b, flags, s);
+        case SG_U32: return partition_edges(EdgesU32{(const uint2*)edges}, m, n, p, b, flags, s, row0);
+        case SG_I32: return partition_edges(EdgesI32{(const int2*)edges}, m, n, p, b, flags, s, row0);
+        case SG_I64: return partition_edges(EdgesI64{(const longlong2*)edges}, m, n, p, b, flags, s, row0);
         default: return SG_ERR_VALUE;
     }
 }
@@ -761,6 +762,40 @@ int sg_cc_hook(const void* edges, int edge_dtype, uint64_t m, uint64_t row0, uin
     if (variant != SG_CC_UF && variant != SG_CC_SV) return SG_ERR_VALUE;
     return hook_dispatch(edges, edge_dtype, m, row0, n, D, variant, validate != 0, (unsigned long long*)flags,
                          (cudaStream_t)stream);
+}
+
+size_t sg_cc_hook_workspace_bytes(uint64_t n, uint64_t m) {
+    const CcPlan p = plan_cc(n, m);
+    if (p.parts <= 1) return 256;
+    Carver c(nullptr, 0);
+    CcPartBufs b;
+    b.totals = c.take<unsigned long long>(MAX_PARTS);
+    b.cursor = c.take<unsigned long long>(MAX_PARTS);
+    b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+    b.edges = c.take<uint2>(m);
+    return c.off + 256;
+}
+
+int sg_cc_hook_part(const void* edges, int edge_dtype, uint64_t m, uint64_t row0, uint64_t n, uint32_t* D,
+                    int variant, int validate, uint64_t* flags, void* ws, size_t ws_bytes, int reuse, void* stream) {
+    if (variant != SG_CC_UF && variant != SG_CC_SV) return SG_ERR_VALUE;
+    const CcPlan p = plan_cc(n, m);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p.parts <= 1)
+        return hook_dispatch(edges, edge_dtype, m, row0, n, D, variant, validate != 0, (unsigned long long*)flags, s);
+    ms_configure();
+    Carver c(ws, ws_bytes);
+    CcPartBufs b;
+    b.totals = c.take<unsigned long long>(MAX_PARTS);
+    b.cursor = c.take<unsigned long long>(MAX_PARTS);
+    b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+    b.edges = c.take<uint2>(m);
+    if (!c.ok) return SG_ERR_WORKSPACE;
+    if (!reuse) {  // rows are validated while they are counted (flags hold ~global row)
+        int rc = partition_dispatch(edges, edge_dtype, m, n, p, b, (unsigned long long*)flags, s, row0);
+        if (rc != SG_OK) return rc;
+    }
+    return hook_partitions(p, b, m, n, D, variant, (unsigned long long*)flags, s);
 }
 
 int sg_cc_compress(uint32_t* D, uint64_t lo, uint64_t hi, uint64_t* roots, void* stream) {

@@ -5,9 +5,38 @@
 // the jump-ahead state of every chunk on the host (paper_1002_4482_b200/gen.py)
 // and each thread then runs the exact scalar recurrence over its chunk, so
 // draw j of the device stream equals draw j of kiss_batch().
+#include <cub/device/device_radix_sort.cuh>
+
 #include "sg_internal.cuh"
 
 namespace sg {
+
+// ---- splitter meta (listrank.py:252-357 outputs, derived from the ranks) ----
+// key = n-1-rank (ascending = list order), value = splitter index
+template <class RankT>
+__global__ void k_spl_keys(const RankT* __restrict__ rank, const long long* __restrict__ spl, uint32_t r,
+                           unsigned long long n, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= r) return;
+    const unsigned long long rk = (unsigned long long)rank[spl[i]];
+    keys[i] = (uint32_t)(n - 1 - rk);
+    vals[i] = i;
+}
+
+// out[0][i] = splitter rank, out[1][i] = sublist length (to the next
+// splitter in list order, the last one to the tail), out[2][i] = reduced
+// successor (the last splitter points at itself)
+__global__ void k_spl_meta(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ order, uint32_t r,
+                           unsigned long long n, long long* __restrict__ out) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= r) return;
+    const uint32_t i = order[j];
+    const long long sr = (long long)(n - 1 - keys[j]);
+    const bool last = j + 1 == r;
+    out[i] = sr;
+    out[(size_t)r + i] = last ? sr + 1 : sr - (long long)(n - 1 - keys[j + 1]);
+    out[2 * (size_t)r + i] = last ? (long long)i : (long long)order[j + 1];
+}
 
 __global__ void __launch_bounds__(128) k_kiss(const unsigned long long* __restrict__ states, unsigned long long chunks,
                                               unsigned long long chunk_len, unsigned long long n,
@@ -117,6 +146,43 @@ int sg_edges_from_keys(const int64_t* keys, uint64_t m, uint64_t n, int64_t* edg
     if (n == 0) return SG_ERR_VALUE;
     k_edges_from_keys<<<grid_for(m, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
         (const long long*)keys, m, n, (long long*)edges);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+size_t sg_splitter_meta_workspace_bytes(uint32_t r) {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)r);
+    return tmp + 4 * ((size_t)r * 4 + 256) + 256;
+}
+
+int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t* spl, uint32_t r, int64_t* out,
+                     void* ws, size_t ws_bytes, void* stream) {
+    if (r == 0) return SG_OK;
+    if (n == 0 || n > 0xFFFFFFFFull) return SG_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    Carver c(ws, ws_bytes);
+    uint32_t* k0 = c.take<uint32_t>(r);
+    uint32_t* k1 = c.take<uint32_t>(r);
+    uint32_t* v0 = c.take<uint32_t>(r);
+    uint32_t* v1 = c.take<uint32_t>(r);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, (int)r);
+    void* t = c.take<unsigned char>(tmp);
+    if (!c.ok) return SG_ERR_WORKSPACE;
+    const uint32_t g = (r + 255) / 256;
+    switch (rank_dtype) {
+        case SG_U32: k_spl_keys<uint32_t><<<g, 256, 0, s>>>((const uint32_t*)rank, (const long long*)spl, r, n, k0, v0); break;
+        case SG_I32: k_spl_keys<int32_t><<<g, 256, 0, s>>>((const int32_t*)rank, (const long long*)spl, r, n, k0, v0); break;
+        case SG_I64: k_spl_keys<int64_t><<<g, 256, 0, s>>>((const int64_t*)rank, (const long long*)spl, r, n, k0, v0); break;
+        default: return SG_ERR_VALUE;
+    }
+    SG_LAUNCH_CHECK();
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < n) ++bits;
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, k0, k1, v0, v1, (int)r, 0, bits, s));
+    k_spl_meta<<<g, 256, 0, s>>>(k1, v1, r, n, (long long*)out);
     SG_LAUNCH_CHECK();
     return SG_OK;
 }

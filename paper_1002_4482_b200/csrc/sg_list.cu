@@ -448,18 +448,29 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_rs_scan(uint32_t* tile_cnt, Li
 
 // install ruler ids in index order: spl[id] = node, word[node] = id << 32
 // (level 0: the packed array keeps the successor in the low half)
+// Level 0 keeps no per-node id array: rgrp[g] = {ruler mask of the 32 ids
+// 32g..32g+31, id of the first ruler at or after 32g}, so a walk that hits
+// ruler x reads one 8-B word (an L2-resident n/4-byte table) instead of a
+// random 4-B id -- and this pass writes the table coalesced instead of
+// scattering n/32 ids.
+__device__ __forceinline__ uint32_t ruler_id(const uint2* __restrict__ rgrp, uint32_t x) {
+    const uint2 g = __ldg(rgrp + (x >> 5));
+    return g.y + __popc(g.x & ((1u << (x & 31u)) - 1u));
+}
+
 template <bool kPacked>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __restrict__ tile_off,
                                                             uint32_t* __restrict__ spl,
                                                             unsigned long long* __restrict__ word,
                                                             const ListStatus* st, int level, uint32_t kbits,
                                                             uint32_t salt, unsigned long long cap,
-                                                            uint32_t* __restrict__ rid) {
+                                                            uint2* __restrict__ rgrp) {
     if (level == 0 && layout_local(st)) return;  // k_rs_contract takes this list
     const unsigned long long N = st->R[level];
     const unsigned long long ntiles = (N + TILE - 1) / TILE;
     typedef cub::BlockScan<uint32_t, TILE_THREADS> BS;
     __shared__ typename BS::TempStorage tmp;
+    static_assert(TILE_ITEMS == 16, "two threads per 32-id group");
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const unsigned long long base = tile * TILE;
         const unsigned long long i0 = base + (unsigned long long)threadIdx.x * TILE_ITEMS;
@@ -472,13 +483,15 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
         uint32_t pre;
         BS(tmp).ExclusiveSum((uint32_t)__popc(flags), pre);
         unsigned long long id = (unsigned long long)tile_off[tile] + pre;
+        if (rgrp != nullptr) {
+            const uint32_t hi = __shfl_down_sync(0xffffffffu, flags, 1);
+            if ((threadIdx.x & 1) == 0 && i0 < N) rgrp[i0 >> 5] = make_uint2(flags | (hi << 16), (uint32_t)id);
+        }
         for (uint32_t rem = flags; rem != 0; rem &= rem - 1, ++id) {
             const uint32_t j = __ffs(rem) - 1;
             if (id < cap) {
                 spl[id] = (uint32_t)(i0 + j);
-                if (rid != nullptr)
-                    rid[i0 + j] = (uint32_t)id;  // level 0: ids live in rid[]
-                else
+                if (rgrp == nullptr)
                     word[i0 + j] = kPacked ? ((id << 32) | (word[i0 + j] & 0xFFFFFFFFull)) : (id << 32);
             }
         }
@@ -532,8 +545,7 @@ template <class View>
 __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned long long* __restrict__ word,
                                                           const uint32_t* __restrict__ spl,
                                                           uint2* __restrict__ up, ListStatus* st, int level,
-                                                          uint32_t kbits, uint32_t salt, uint32_t cap_hops,
-                                                          const uint32_t* __restrict__ rid) {
+                                                          uint32_t kbits, uint32_t salt, uint32_t cap_hops) {
     const unsigned long long N = st->R[level];
     const unsigned long long R = st->R[level + 1];
     unsigned long long* q = &st->qhead[level];
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
             up[sid] = make_uint2(sid, pre);
             sid = NIL;
         } else if (is_ruler((uint32_t)nx, kbits, salt)) {
-            up[sid] = make_uint2(rid != nullptr ? __ldg(rid + nx) : (uint32_t)(word[nx] >> 32), pre);
+            up[sid] = make_uint2((uint32_t)(word[nx] >> 32), pre);
             sid = NIL;
         } else if (hops >= cap_hops) {
             st->overflow = 1;
@@ -599,7 +611,7 @@ constexpr int REC_CH = 1024;
 
 template <class SuccT>
 __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_rec(const SuccT* __restrict__ succ,
-                                                              const uint32_t* __restrict__ rid,
+                                                              const uint2* __restrict__ rgrp,
                                                               const uint32_t* __restrict__ spl,
                                                               uint2* __restrict__ up, uint32_t* __restrict__ rec_cur,
                                                               unsigned long long* __restrict__ rec_sl,
@@ -665,7 +677,7 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
             } else if (nxl >= N) {  // out-of-range successor (invalid input)
                 st->bad = 1;
             } else if (is_ruler((uint32_t)nxl, kbits, salt)) {
-                upv.x = __ldg(rid + nxl);
+                upv.x = ruler_id(rgrp, (uint32_t)nxl);
             } else if (pre >= cap_hops) {
                 st->overflow = 1;
             } else {
@@ -1013,6 +1025,7 @@ struct ContractSmem {
     uint16_t term[TILE];     // ruler -> end node of its segment
     uint8_t pred[TILE];      // node has an in-tile predecessor
     uint16_t brk[TILE / 16]; // per 16-id block: bit q = id q's successor is not id q + 1
+    uint16_t rd[TILE];       // ruler -> distance to its segment end (after jumping)
 };
 
 // Bank swizzles for node-indexed arrays.  Walkers start 16 nodes apart (one
@@ -1241,6 +1254,16 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
             }
         }
         __syncthreads();
+        // per ruler: its segment (tile-local) and distance to the segment end;
+        // nx[] is dead after the walk and holds the segment from here on
+        for (uint32_t k = t; k < K; k += TILE_THREADS) {
+            uint32_t d;
+            uint16_t e;
+            seg_end(k, d, e);
+            S.nx[k] = e != CT_END ? S.rid[sw16(e)] : CT_END;
+            S.rd[k] = (uint16_t)d;
+        }
+        __syncthreads();
         // 6. per node: {tile-local segment : 16 | distance to the segment end : 16}
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
@@ -1257,10 +1280,8 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                     if (o == 0xFFFFFFFFu) {
                         bad = true;  // a cycle without local rulers
                     } else {
-                        uint32_t d;
-                        uint16_t e;
-                        seg_end(o >> 16, d, e);
-                        if (e != CT_END) wd[c] = ((uint32_t)S.rid[sw16(e)] << 16) | ((d - (o & 0xFFFFu)) & 0xFFFFu);
+                        const uint32_t k = o >> 16;
+                        wd[c] = ((uint32_t)S.nx[k] << 16) | (((uint32_t)S.rd[k] - (o & 0xFFFFu)) & 0xFFFFu);
                     }
                 }
             }
@@ -1396,7 +1417,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     const unsigned long long warps = wg * (WALK_THREADS / 32);
     p.maxchunks = n / (REC_CH - 32) + warps + 2;
     const uint32_t kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);
-    const uint32_t kb1 = env_u32("SG_RS_KBITS", 5, 1, 16);
+    const uint32_t kb1 = env_u32("SG_RS_KBITS", 3, 1, 16);  // upper levels: short chains, the walk tail is latency-bound
     const uint32_t fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
@@ -1421,7 +1442,8 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
 struct RsBufs {
     ListStatus* st = nullptr;
     unsigned long long* word0 = nullptr;
-    uint32_t* rid = nullptr;
+    uint32_t* rid = nullptr;        // contraction: segment id at each head
+    uint2* rgrp = nullptr;          // ruling set: {ruler mask, first id} per 32 nodes
     uint32_t* rec_cur = nullptr;
     unsigned long long* rec_sl = nullptr;
     unsigned long long* pairs = nullptr;
@@ -1443,6 +1465,7 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     if (p.levels > 0) {
         const unsigned long long nrec = p.maxchunks * REC_CH;
         b.rid = c.take<uint32_t>(n);
+        b.rgrp = c.take<uint2>(n / 32 + 2);
         b.rec_cur = c.take<uint32_t>(nrec);
         const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
         b.rec_sl = c.take<unsigned long long>(nrec > npad ? nrec : npad);  // reused by rs5_refine
@@ -1586,13 +1609,13 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         SG_LAUNCH_CHECK();
         rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
         k_rs_select<false><<<nt < kSMs * 8 ? nt : kSMs * 8, TILE_THREADS, 0, s>>>(tk, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
-                                                        k == 0 ? b.rid : nullptr);
+                                                        k == 0 ? b.rgrp : nullptr);
         rec.end();
         SG_LAUNCH_CHECK();
         if (k == 0) {
             // scattered layouts: record walk; local layouts: tile contraction
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
-            k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rid, b.spl[0], b.lvl[1], b.rec_cur,
+            k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.rec_cur,
                                                                     b.rec_sl, b.st, p.kbits[0], p.salt[0],
                                                                     p.walk_cap, p.maxchunks, p.load_mode);
             rec.end();
@@ -1610,7 +1633,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         } else {
             rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
             k_rs_walk<LevelK><<<walk_grid, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
-                                                                 k, p.kbits[k], p.salt[k], p.walk_cap, nullptr);
+                                                                 k, p.kbits[k], p.salt[k], p.walk_cap);
         }
         rec.end();
         SG_LAUNCH_CHECK();

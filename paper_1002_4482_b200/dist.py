@@ -24,6 +24,7 @@ orchestration is tested with the gloo backend on CPU (tests/test_dist.py);
 the product path uses ``CudaOps`` + NCCL.
 """
 
+import contextlib
 import ctypes
 import time
 
@@ -33,7 +34,7 @@ import torch.distributed as dist
 
 from . import _device, _native
 from .concomp import _graph_error_message, sv_round_bound
-from .core import EdgeGraph, ExecStats, InvalidGraphError
+from .core import EdgeGraph, ExecStats, InvalidGraphError, KernelCounters, LaunchRecord
 
 _NO_ROW = 1 << 62
 
@@ -60,11 +61,17 @@ class TorchDistComm:
 
 
 class CudaOps:
-    """Device kernels of one rank (libsg C ABI on the current CUDA stream)."""
+    """Device kernels of one rank (libsg C ABI on the current CUDA stream).
+
+    The rank's edge block is split once by vertex window (``sg_cc_hook_part``,
+    validating rows on the way) into a workspace that later rounds re-hook
+    from, so every round's parent gathers stay L2-resident."""
 
     def __init__(self, device):
         self.device = device
         self.lib = _native.lib()
+        self.ws = None
+        self.parted = None  # (data_ptr, m) of the block held in ws
 
     def stream(self):
         return _device.stream_ptr(self.device)
@@ -78,9 +85,15 @@ class CudaOps:
     def hook(self, edges, row0, n, D, variant, validate, flags):
         code = _native.SG_CC_UF if variant == "uf" else _native.SG_CC_SV
         m = edges.shape[0]
-        rc = self.lib.sg_cc_hook(_device.ptr(edges), _device.dtype_code(edges), m, row0, n, _device.ptr(D), code,
-                                 int(validate), _device.ptr(flags), self.stream())
-        _native.check(rc, "sg_cc_hook")
+        if self.ws is None:
+            self.ws = _device.workspace(self.lib.sg_cc_hook_workspace_bytes(n, m), self.device)
+        key = (edges.data_ptr(), m)
+        reuse = int(self.parted == key and not validate)
+        rc = self.lib.sg_cc_hook_part(_device.ptr(edges), _device.dtype_code(edges), m, row0, n, _device.ptr(D),
+                                      code, int(validate), _device.ptr(flags), _device.ptr(self.ws), self.ws.numel(),
+                                      reuse, self.stream())
+        _native.check(rc, "sg_cc_hook_part")
+        self.parted = key
 
     def compress(self, D, lo, hi, roots):
         _native.check(self.lib.sg_cc_compress(_device.ptr(D), lo, hi, _device.ptr(roots), self.stream()),
@@ -90,10 +103,33 @@ class CudaOps:
         torch.cuda.synchronize(self.device)
 
 
-def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None):
+class _NoTrace:
+    @contextlib.contextmanager
+    def span(self, name):
+        yield
+
+
+class CudaTrace:
+    """CUDA events around every kernel / collective of the sharded rounds ->
+    ExecStats launch records."""
+
+    def __init__(self):
+        self.spans = []
+
+    @contextlib.contextmanager
+    def span(self, name):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        yield
+        b.record()
+        self.spans.append((name, a, b))
+
+
+def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None, trace=None):
     """Run the sharded rounds.  `edges` is this rank's (m_g, 2) block whose
     first row is global row `row0`.  Returns (D replica as int32 tensor of
     size >= n, info dict)."""
+    trace = trace or _NoTrace()
     if variant not in ("uf", "sv"):
         raise ValueError(f"unknown variant {variant!r}")
     G = comm.world
@@ -114,7 +150,8 @@ def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None
         if r > bound:
             raise RuntimeError(f"no convergence after {r - 1} rounds (bound {bound})")
         flags.zero_()
-        ops.hook(edges, row0, n, D, variant, r == 1, flags)
+        with trace.span("cc_hook_uf" if variant == "uf" else "cc_hook_sv"):
+            ops.hook(edges, row0, n, D, variant, r == 1, flags)
         info["edge_sweeps"] += 1
         if r == 1:
             # kernel flags hold ~row (0 = none); reduce the first bad global row
@@ -125,20 +162,25 @@ def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None
             if b[0] != _NO_ROW or b[1] != _NO_ROW:
                 kind, row = (1, b[0]) if b[0] != _NO_ROW else (2, b[1])
                 raise InvalidGraphError(_graph_error_message(kind, row))
-        changed = int(flags[0].item())
+        # one UF sweep unites every edge of the block, so a single rank is
+        # done after round 1 (the single-GPU path's one-sweep argument)
+        changed = int(flags[0].item()) and not (variant == "uf" and G == 1)
         D[n] = 0 if changed else 1
         t0 = time.perf_counter()
-        comm.allreduce_min_(D)
+        with trace.span("nccl_allreduce_min"):
+            comm.allreduce_min_(D)
         info["comm_s"] += time.perf_counter() - t0
         info["allreduce_bytes"] += D.numel() * D.element_size()
         converged = int(D[n].item()) == 1
         if variant == "sv" or converged:
             roots.zero_()
-            ops.compress(D, lo, hi, roots)
+            with trace.span("cc_shortcut"):
+                ops.compress(D, lo, hi, roots)
             info["vertex_sweeps"] += 1
             t0 = time.perf_counter()
-            comm.allgather_(D, D[comm.rank * S:(comm.rank + 1) * S].clone())
-            comm.allreduce_sum_(roots)
+            with trace.span("nccl_allgather"):
+                comm.allgather_(D, D[comm.rank * S:(comm.rank + 1) * S].clone())
+                comm.allreduce_sum_(roots)
             info["comm_s"] += time.perf_counter() - t0
             info["allgather_bytes"] += D.numel() * D.element_size()
             if variant == "sv" or converged:
@@ -174,14 +216,19 @@ def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", 
     if int(p) > n:
         raise ValueError(f"more threads ({p}) than vertices ({n})")
     ops = CudaOps(dev)
+    trace = CudaTrace()
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record()
-    D, info = sharded_components(n, edges, int(row0), comm, ops, variant=variant)
+    D, info = sharded_components(n, edges, int(row0), comm, ops, variant=variant, trace=trace)
     stop.record()
     stop.synchronize()
     labels = D[:n].to(torch.int64)
     stats = ExecStats(backend="sm_100a")
+    for k, (name, a, b) in enumerate(trace.spans):
+        ms = a.elapsed_time(b)
+        stats.launch_log.append(LaunchRecord(kernel=name, counters=KernelCounters(launches=1, ms=ms), round=k, ms=ms))
+    stats.barriers = max(0, len(stats.launch_log) - 1)
     stats.rounds = info["rounds"]
     stats.wall_time = start.elapsed_time(stop) / 1e3
     stats.meta.update(n=n, p=int(p), m_stored=graph.m, oriented_m=2 * graph.m, rounds=info["rounds"],

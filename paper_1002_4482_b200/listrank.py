@@ -249,18 +249,12 @@ def _splitter_set(rank, spl_nodes, n, key=None):
     dev = rank.device
     r = len(spl_nodes)
     idx = _device_index(spl_nodes, dev, key)
-    srank = rank.index_select(0, idx).to(torch.int64)
-    sr_sorted, order = torch.sort(srank, descending=True)
+    L = _native.lib()
     res = torch.empty((3, r), dtype=torch.int64, device=dev)   # rank, sublist length, reduced successor
-    res[0] = srank
-    ln_sorted = torch.empty_like(sr_sorted)
-    ln_sorted[:-1] = sr_sorted[:-1] - sr_sorted[1:]
-    ln_sorted[-1] = sr_sorted[-1] + 1
-    nx_sorted = torch.empty_like(order)
-    nx_sorted[:-1] = order[1:]
-    nx_sorted[-1] = order[-1]
-    res[1].index_copy_(0, order, ln_sorted)
-    res[2].index_copy_(0, order, nx_sorted)
+    ws = _device.workspace(L.sg_splitter_meta_workspace_bytes(r), dev)
+    _native.check(L.sg_splitter_meta(_device.ptr(rank), _device.dtype_code(rank), n, _device.ptr(idx), r,
+                                     _device.ptr(res), _device.ptr(ws), ws.numel(), _device.stream_ptr(dev)),
+                  "sg_splitter_meta")
     host = res.cpu().numpy()
     out = SplitterSet(r, np.ascontiguousarray(spl_nodes, dtype=np.int64))
     out.splitter_rank = host[0]

@@ -6,6 +6,7 @@ TAG=${TAG:-r01}
 O=gpurun_out/$TAG
 mkdir -p $O
 python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
+if [ -z "$ONLY_NCU" ]; then
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
 python -c "import __graft_entry__ as e; e.smoke()" > $O/smoke.log 2>&1
 timeout 600 python bench.py > $O/bench_lr26.json 2> $O/bench_lr26.err
@@ -18,11 +19,15 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
     python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-secondary > $O/ncu_launch_bench.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cc26.csv \
     python bench.py --workload cc26 --steps 3 --warmup 3 --no-e2e --no-cpu > $O/ncu_launch_cc.log 2>&1
-for spec in "lr26:k_rs_walk_rec|k_rs_rec|k_rs_count0:lr26:6" "lr28:k_rs_walk_rec|k_rs_rec:lr28:4" \
-            "lr28o:k_rs_contract|k_rs_count0:lr28o:3" "cc26:k_cc_hook_uf|k_cc_part:cc26:11" "cc22:k_cc_hook_uf:cc22:1" \
-            "wy26:k_wy_jump:wy26:1"; do
-  IFS=: read -r wl kern name cnt <<< "$spec"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kern" -c $cnt -o $O/prof_$name \
-      python tools/prof_target.py $wl > $O/ncu_$name.log 2>&1
-done
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_lr28o.csv \
+    python bench.py --workload lr28o --steps 3 --warmup 3 --no-e2e --no-cpu > $O/ncu_launch_lr28o.log 2>&1
+fi
+# ncu captures: a separate call per batch (gpurun_out is capped at 64 MiB)
+if [ -n "$NCU_BATCH" ]; then
+  for spec in $NCU_BATCH; do
+    IFS=: read -r wl kern name cnt <<< "$spec"
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kern" -c $cnt -o $O/prof_$name \
+        python tools/prof_target.py $wl > $O/ncu_$name.log 2>&1
+  done
+fi
 ls $O
