@@ -297,40 +297,40 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
     const uint32_t lane = lane_id();
     unsigned long long mine = 0;  // edges of partition `lane` seen by this warp
     const unsigned long long ntiles = (m + PART_TILE - 1) / PART_TILE;
+    int nbits = 0;
+    while ((1 << nbits) < P) ++nbits;
+    constexpr int H = PART_ITEMS / 2;  // half a tile in flight: fewer registers, more resident warps
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const unsigned long long e0 = tile * PART_TILE + threadIdx.x;
-        unsigned long long uu[PART_ITEMS], vv[PART_ITEMS];
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            const unsigned long long e0 = tile * PART_TILE + (unsigned long long)half * H * PART_THREADS + threadIdx.x;
+            unsigned long long uu[H], vv[H];
 #pragma unroll
-        for (int j = 0; j < PART_ITEMS; ++j) {  // all loads in flight before any validation atomic
-            const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
-            uu[j] = n;
-            vv[j] = n;
-            if (e < m) edges.load(e, uu[j], vv[j]);
-        }
-        int pp[PART_ITEMS];
-#pragma unroll
-        for (int j = 0; j < PART_ITEMS; ++j) {
-            const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
-            pp[j] = -1;
-            if (e < m) {
-                if (uu[j] >= n || vv[j] >= n)
-                    atomicMax(flags + 1, ~(row0 + e));
-                else if (uu[j] == vv[j])
-                    atomicMax(flags + 2, ~(row0 + e));
-                else
-                    pp[j] = (int)((uu[j] > vv[j] ? uu[j] : vv[j]) >> shift);
+            for (int j = 0; j < H; ++j) {  // all loads in flight before any validation atomic
+                const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
+                uu[j] = n;
+                vv[j] = n;
+                if (e < m) edges.load(e, uu[j], vv[j]);
             }
-        }
 #pragma unroll
-        for (int j = 0; j < PART_ITEMS; ++j) {
-            const int p = pp[j];
-            unsigned msk = __ballot_sync(0xffffffffu, p >= 0);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const unsigned b = __ballot_sync(0xffffffffu, p >= 0 && ((p >> k) & 1));
-                msk &= ((lane >> k) & 1u) ? b : ~b;
+            for (int j = 0; j < H; ++j) {
+                const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
+                int p = -1;
+                if (e < m) {
+                    if (uu[j] >= n || vv[j] >= n)
+                        atomicMax(flags + 1, ~(row0 + e));
+                    else if (uu[j] == vv[j])
+                        atomicMax(flags + 2, ~(row0 + e));
+                    else
+                        p = (int)((uu[j] > vv[j] ? uu[j] : vv[j]) >> shift);
+                }
+                unsigned msk = __ballot_sync(0xffffffffu, p >= 0);
+                for (int k = 0; k < nbits; ++k) {
+                    const unsigned b = __ballot_sync(0xffffffffu, p >= 0 && ((p >> k) & 1));
+                    msk &= ((lane >> k) & 1u) ? b : ~b;
+                }
+                mine += __popc(msk);
             }
-            mine += __popc(msk);
         }
     }
     if (lane < (uint32_t)P && mine) atomicAdd(&s_cnt[lane], mine);

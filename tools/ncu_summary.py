@@ -27,7 +27,8 @@ KEYS = [
     "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
 ]
 STALL = "smsp__average_warp_latency_issue_stalled_"
-NAME_MAP = {"k_rs_walk_stage": "rs3_walk", "k_rs_walk_rec": "rs3_walk", "k_rs_walk<sg::Level0": "rs3_walk",
+NAME_MAP = {"k_rs_contract_expand": "rs5_expand", "k_rs_contract_link": "rs3_link", "k_rs_select": "rs2_select",
+            "k_cc_part_scatter2": "cc_partition_scatter","k_rs_walk_stage": "rs3_walk", "k_rs_walk_rec": "rs3_walk", "k_rs_walk<sg::Level0": "rs3_walk",
             "k_rs_walk<Level0": "rs3_walk", "k_rs_walk<sg::LevelK": "rs4_walk", "k_rs_walk<LevelK": "rs4_walk",
             "k_rs_rec_refine": "rs5_refine", "k_rs_rec_scatter": "rs5_scatter", "k_rs_rec_partition": "rs5_partition",
             "k_rs_expand0": "rs5_expand", "k_rs_count0": "rs1_validate", "k_cc_hook_uf": "cc_hook_uf",
@@ -44,9 +45,8 @@ def value(d, units, hdr, k):
 
 
 def short(kname):
-    if "k_rs_contract<" in kname:  # <SuccT, OutT, kExpand, kVec>
-        args = kname[kname.index("k_rs_contract<") + 14:].split(">")[0].split(", ")
-        return "rs5_expand" if len(args) > 2 and args[2] in ("(bool)1", "true") else "rs3_contract"
+    if "k_rs_contract<" in kname:  # <SuccT, kVec>
+        return "rs3_contract"
     for pat, nm in NAME_MAP.items():
         if pat in kname:
             return nm
