@@ -220,3 +220,30 @@ def test_partitioned_path_small_windows(cuda, orc, monkeypatch, variant):
         g.sv_components(g.EdgeGraph(60_000, e[:70_000]), p=8, variant=variant)
     with pytest.raises(g.InvalidGraphError, match="out of range at row 80000"):
         g.sv_components(g.EdgeGraph(60_000, e), p=8, variant=variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_sharded_path_on_nccl_single_rank(cuda, orc, monkeypatch, tmp_path, variant):
+    """The edge-sharded product path (dist.sv_components_dist: partitioned
+    per-rank hook via sg_cc_hook_part, NCCL min all-reduce, sharded
+    shortcut + all-gather) on a one-rank NCCL group, windows forced small so
+    the block is split; plus the launch trace and global-row validation."""
+    import torch.distributed as dist
+
+    from paper_1002_4482_b200 import dist as sgdist
+
+    monkeypatch.setenv("SG_CC_WBITS", "12")
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=cuda)
+    try:
+        for gr in (g.gen_random_graph(60_000, 5e-5, seed=4), g.gen_tree_graph(70_000, 3, seed=2)):
+            labels, stats = sgdist.sv_components_dist(gr, 64, variant=variant)
+            assert np.array_equal(labels, orc.seq_components(gr.n, gr.edges))
+            names = {r.kernel for r in stats.launch_log}
+            assert {"nccl_allreduce_min", "cc_shortcut"} <= names and any(k.startswith("cc_hook") for k in names)
+        e = g.gen_random_graph(60_000, 5e-5, seed=4).edges.copy()
+        e[50_000] = [9, 9]
+        with pytest.raises(g.InvalidGraphError, match="self-loop at edge 50000"):
+            sgdist.sv_components_dist(g.EdgeGraph(60_000, e), 8, variant=variant)
+    finally:
+        dist.destroy_process_group()
