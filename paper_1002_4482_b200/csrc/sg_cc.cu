@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
         }
         __syncthreads();  // staging consumed: refill it behind the split
         issue(tile + gridDim.x);
-        ms_split<MS2_ITEMS>(pr, bn, bin_of, slot, (uint32_t)P, cursor, reinterpret_cast<unsigned long long*>(out), sm);
+        ms_split<MS2_ITEMS, 4>(pr, bn, bin_of, slot, (uint32_t)P, cursor, reinterpret_cast<unsigned long long*>(out), sm);
     }
 }
 

@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_partitio
         }
         __syncthreads();  // staging consumed: refill it behind the split
         issue(tile + gridDim.x);
-        over |= ms_split<MS2_ITEMS>(pr, bn, bin_of, slot, cbins, cursor, pairs, sm);
+        over |= ms_split<MS2_ITEMS, 8>(pr, bn, bin_of, slot, cbins, cursor, pairs, sm);
     }
     if (over) st->bad = 1;
 }
@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_refine2(
         issue(tile + gridDim.x);
         auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
         auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
-        over |= ms_split<MS2_ITEMS>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
+        over |= ms_split<MS2_ITEMS, 8>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
     }
     if (over) st->bad = 1;
 }
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_refine2(
 template <class OutT>
 __global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
                                                                OutT* __restrict__ rank, unsigned long long n,
-                                                               uint32_t fshift, const ListStatus* st) {
+                                                               uint32_t fshift, const ListStatus* st, int vec) {
     if (layout_local(st) || st->overflow) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     OutT* win = reinterpret_cast<OutT*>(smem_raw);
@@ -908,11 +908,26 @@ __global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long
     if (w0 >= n) return;
     const uint32_t size = (uint32_t)min((unsigned long long)1 << fshift, n - w0);
     const uint32_t mask = (1u << fshift) - 1u;
-    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) {
-        const unsigned long long pr = __ldcs(pairs + w0 + i);
+    const unsigned long long wid = w0 >> fshift;
+    auto put = [&](unsigned long long pr) {
         const unsigned long long cur = pr >> 32;
-        if ((cur >> fshift) == (w0 >> fshift)) win[cur & mask] = (OutT)(uint32_t)pr;
+        if ((cur >> fshift) == wid) win[cur & mask] = (OutT)(uint32_t)pr;
+    };
+    if (vec && size == (1u << fshift)) {  // full window, aligned output: 16-B loads and stores
+        const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(pairs + w0);
+        for (uint32_t i = threadIdx.x; i < size / 2; i += blockDim.x) {
+            const ulonglong2 v = __ldcs(p2 + i);
+            put(v.x);
+            put(v.y);
+        }
+        __syncthreads();
+        constexpr uint32_t V = 16 / sizeof(OutT);
+        const uint4* src = reinterpret_cast<const uint4*>(win);
+        uint4* dst = reinterpret_cast<uint4*>(rank + w0);
+        for (uint32_t i = threadIdx.x; i < size / V; i += blockDim.x) __stcs(dst + i, src[i]);
+        return;
     }
+    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) put(__ldcs(pairs + w0 + i));
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) rank[w0 + i] = win[i];
 }
@@ -1699,8 +1714,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     rec.end();
     SG_LAUNCH_CHECK();
     rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);
-    k_rs_rec_scatter<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(b.rec_sl, rank, n, p.fshift,
-                                                                                  b.st);
+    k_rs_rec_scatter<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(
+        b.rec_sl, rank, n, p.fshift, b.st, ((uintptr_t)rank & 15) == 0 ? 1 : 0);
     rec.end();
     SG_LAUNCH_CHECK();
     if (stats) {

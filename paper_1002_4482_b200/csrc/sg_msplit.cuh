@@ -63,7 +63,7 @@ struct MsSmem {
 // cursor[bin] (global u64) counts the bin's slots already claimed.
 // bin_of(pair) recovers the bin when writing out.  Returns true if a bin
 // overflowed (only for inputs that break the caller's size contract).
-template <int ITEMS, class BinOf, class Slot>
+template <int ITEMS, int NBITS, class BinOf, class Slot>
 __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], const uint32_t (&bn)[ITEMS],
                                          BinOf bin_of, Slot slot, uint32_t nb,
                                          unsigned long long* __restrict__ cursor,
@@ -76,7 +76,6 @@ __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], 
     __syncwarp();
     // per-warp counts; the leader of each peer group (lanes with equal bins)
     // bumps the warp's counter and hands the old value to its peers
-    const int nbits = 32 - __clz(nb > 1 ? nb - 1 : 1);
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         // peers: lanes with the same bin
@@ -84,13 +83,17 @@ __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], 
         if (g_ms_peers == 0) {
             peers = __match_any_sync(0xffffffffu, bn[j]);
         } else {
-            // bit-by-bit ballots (VOTE is an ALU op; match.any queues on MIO)
+            // bit-by-bit ballots over the NBITS bin bits (VOTE is an ALU op;
+            // match.any queues on MIO).  Bits above nb's width are 0 in every
+            // lane and leave the mask unchanged.
             const bool valid = bn[j] < nb;
             const unsigned vb = __ballot_sync(0xffffffffu, valid);
             peers = valid ? vb : ~vb;
-            for (int k = 0; k < nbits; ++k) {
+#pragma unroll
+            for (int k = 0; k < NBITS; ++k) {
                 const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
-                peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+                const unsigned m = 0u - ((bn[j] >> k) & 1u);
+                peers &= ~(b ^ m);
             }
         }
         const int leader = __ffs(peers) - 1;
@@ -181,7 +184,7 @@ __device__ __forceinline__ bool ms_tile(Get get, BinOf bin_of, Slot slot, unsign
         const bool ok = e < e1 && get(e, pr[j], b) && b < nb;
         bn[j] = ok ? b : (uint32_t)MS_MAXB;
     }
-    return ms_split<MS_ITEMS>(pr, bn, bin_of, slot, nb, cursor, out, sm);
+    return ms_split<MS_ITEMS, 10>(pr, bn, bin_of, slot, nb, cursor, out, sm);
 }
 
 // ---------------------------------------------------------------------------
