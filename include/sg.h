@@ -153,6 +153,17 @@ int sg_rs_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype,
                uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
                void* stream, sg_stats* st, sg_violation* viol);
 
+/* sg_rs_rank plus meta["splitter_set"] (see sg_splitter_meta) for the r
+ * splitter nodes spl, computed on the same stream before the call's single
+ * synchronisation: meta_dev (device, 3 x r int64) and, if meta_host is not
+ * NULL, a copy in meta_host (host, pinned for best speed).  meta_ws holds
+ * sg_splitter_meta_workspace_bytes(r) bytes. */
+int sg_rs_rank_meta(const void* succ, int succ_dtype, void* rank, int rank_dtype,
+                    uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
+                    const int64_t* spl, uint32_t r, int64_t* meta_dev, int64_t* meta_host,
+                    void* meta_ws, size_t meta_ws_bytes,
+                    void* stream, sg_stats* st, sg_violation* viol);
+
 /* out[i] = src[idx[i]] for i < k (int64 ranks at the official splitters;
  * listrank.py:355-356 splitter_rank is the global rank of the splitter). */
 int sg_gather_i64(const int64_t* src, const int64_t* idx, uint64_t k,

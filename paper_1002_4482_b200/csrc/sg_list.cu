@@ -770,27 +770,27 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_refine(const unsigned 
 
 // TMA-staged versions (persistent, 2 CTAs per SM): the next 4096-element
 // tile streams into shared memory while the current one is split.
-constexpr int MS2_CTAS_PER_SM = 2;
 
-__global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_partition2(
+template <int IT>
+__global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_partition2(
     const uint32_t* __restrict__ rec_cur, const unsigned long long* __restrict__ rec_sl,
     const uint32_t* __restrict__ IS1, unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ pairs,
     ListStatus* st, uint32_t cshift, uint32_t cbins) {
     if (layout_local(st) || st->overflow) return;
     extern __shared__ __align__(128) unsigned char ms_raw[];
     uint32_t* s_cur = reinterpret_cast<uint32_t*>(ms_raw);
-    unsigned long long* s_sl = reinterpret_cast<unsigned long long*>(ms_raw + MS2_TILE * 4);
-    MsSmem sm = MsSmem::carve(ms_raw + MS2_TILE * 12, cbins, MS2_TILE);
+    unsigned long long* s_sl = reinterpret_cast<unsigned long long*>(ms_raw + (MS_THREADS * IT) * 4);
+    MsSmem sm = MsSmem::carve(ms_raw + (MS_THREADS * IT) * 12, cbins, (MS_THREADS * IT));
     __shared__ unsigned long long bar;
     const unsigned long long total = st->chunks * REC_CH;  // a multiple of REC_CH
-    const unsigned long long ntiles = (total + MS2_TILE - 1) / MS2_TILE;
+    const unsigned long long ntiles = (total + (MS_THREADS * IT) - 1) / (MS_THREADS * IT);
     const unsigned long long R1 = st->R[1];
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     auto issue = [&](unsigned long long tile) {
         if (threadIdx.x == 0 && tile < ntiles) {
-            const unsigned long long e0 = tile * MS2_TILE;
-            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, total - e0);
+            const unsigned long long e0 = tile * (MS_THREADS * IT);
+            const uint32_t cnt = (uint32_t)min((unsigned long long)(MS_THREADS * IT), total - e0);
             mbar_expect_tx(&bar, cnt * 12u);
             bulk_g2s(s_cur, rec_cur + e0, cnt * 4u, &bar);
             bulk_g2s(s_sl, rec_sl + e0, cnt * 8u, &bar);
@@ -802,13 +802,13 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_partitio
     uint32_t phase = 0;
     issue(blockIdx.x);
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, total - tile * MS2_TILE);
+        const uint32_t cnt = (uint32_t)min((unsigned long long)(MS_THREADS * IT), total - tile * (MS_THREADS * IT));
         mbar_wait(&bar, phase);
         phase ^= 1u;
-        unsigned long long pr[MS2_ITEMS];
-        uint32_t bn[MS2_ITEMS];
+        unsigned long long pr[IT];
+        uint32_t bn[IT];
 #pragma unroll
-        for (int g = 0; g < MS2_ITEMS / 4; ++g) {
+        for (int g = 0; g < IT / 4; ++g) {
             const uint32_t e = (g * MS_THREADS + threadIdx.x) * 4;  // 4 records per vector access
             const uint4 c4 = e < cnt ? reinterpret_cast<const uint4*>(s_cur)[e >> 2] : make_uint4(NIL, NIL, NIL, NIL);
             const ulonglong2 s01 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[e >> 1] : make_ulonglong2(0, 0);
@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_partitio
             }
         }
 #pragma unroll
-        for (int j = 0; j < MS2_ITEMS; ++j) {
+        for (int j = 0; j < IT; ++j) {
             const uint32_t c = (uint32_t)(pr[j] >> 32);
             const uint32_t local = (uint32_t)pr[j];
             // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
@@ -834,28 +834,29 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_partitio
         }
         __syncthreads();  // staging consumed: refill it behind the split
         issue(tile + gridDim.x);
-        over |= ms_split<MS2_ITEMS, 8>(pr, bn, bin_of, slot, cbins, cursor, pairs, sm);
+        over |= ms_split<IT, 8>(pr, bn, bin_of, slot, cbins, cursor, pairs, sm);
     }
     if (over) st->bad = 1;
 }
 
-__global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_refine2(
+template <int IT>
+__global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
     unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift) {
     if (layout_local(st) || st->overflow) return;
     const uint32_t fb = 1u << (cshift - fshift);
     extern __shared__ __align__(128) unsigned char ms_raw[];
     unsigned long long* s_in = reinterpret_cast<unsigned long long*>(ms_raw);
-    MsSmem sm = MsSmem::carve(ms_raw + MS2_TILE * 8, fb, MS2_TILE);
+    MsSmem sm = MsSmem::carve(ms_raw + (MS_THREADS * IT) * 8, fb, (MS_THREADS * IT));
     __shared__ unsigned long long bar;
-    // tiles never straddle a coarse window (2^cshift is a multiple of MS2_TILE)
-    const unsigned long long ntiles = (n + MS2_TILE - 1) / MS2_TILE;
+    // tiles never straddle a coarse window (2^cshift is a multiple of (MS_THREADS * IT))
+    const unsigned long long ntiles = (n + (MS_THREADS * IT) - 1) / (MS_THREADS * IT);
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     auto issue = [&](unsigned long long tile) {
         if (threadIdx.x == 0 && tile < ntiles) {
-            const unsigned long long e0 = tile * MS2_TILE;
-            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, n - e0);
+            const unsigned long long e0 = tile * (MS_THREADS * IT);
+            const uint32_t cnt = (uint32_t)min((unsigned long long)(MS_THREADS * IT), n - e0);
             const uint32_t bytes = (cnt * 8u + 15u) & ~15u;  // the buffer is padded to whole windows
             mbar_expect_tx(&bar, bytes);
             bulk_g2s(s_in, in + e0, bytes, &bar);
@@ -865,15 +866,15 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_refine2(
     uint32_t phase = 0;
     issue(blockIdx.x);
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const unsigned long long e0 = tile * MS2_TILE;
-        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, n - e0);
+        const unsigned long long e0 = tile * (MS_THREADS * IT);
+        const uint32_t cnt = (uint32_t)min((unsigned long long)(MS_THREADS * IT), n - e0);
         const unsigned long long c = e0 >> cshift;
         mbar_wait(&bar, phase);
         phase ^= 1u;
-        unsigned long long pr[MS2_ITEMS];
-        uint32_t bn[MS2_ITEMS];
+        unsigned long long pr[IT];
+        uint32_t bn[IT];
 #pragma unroll
-        for (int g = 0; g < MS2_ITEMS / 2; ++g) {
+        for (int g = 0; g < IT / 2; ++g) {
             const uint32_t e = (g * MS_THREADS + threadIdx.x) * 2;
             const ulonglong2 v = e < cnt ? reinterpret_cast<const ulonglong2*>(s_in)[e >> 1] : make_ulonglong2(0, 0);
             const unsigned long long vv[2] = {v.x, v.y};
@@ -890,7 +891,7 @@ __global__ void __launch_bounds__(MS_THREADS, MS2_CTAS_PER_SM) k_rs_rec_refine2(
         issue(tile + gridDim.x);
         auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
         auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
-        over |= ms_split<MS2_ITEMS, 8>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
+        over |= ms_split<IT, 8>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
     }
     if (over) st->bad = 1;
 }
@@ -1387,6 +1388,7 @@ struct RsPlan {
     bool rec_ok = true;                          // fine windows fit shared memory
     int contract = 1;                            // allow the tile contraction for local layouts
     int ms_version = 2;                          // 2: TMA-staged window passes, 1: register tiles
+    uint32_t ms_items = 16;                      // window passes: items per thread (tile = 256 x items)
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
@@ -1438,6 +1440,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
     p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
     p.ms_version = (int)env_u32("SG_RS_MS", 2, 1, 2);
+    p.ms_items = env_u32("SG_MS_ITEMS", 16, 8, 16) >= 16 ? 16 : 8;
     p.cap[0] = n;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
@@ -1683,16 +1686,20 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // scattered layouts: rank the records, bucket them by window, scatter
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
     const uint32_t persist = kSMs * 4;
-    const uint32_t persist2 = kSMs * MS2_CTAS_PER_SM;
+    const uint32_t it = p.ms_items;
+    const uint32_t tile2 = MS_THREADS * it;
+    const uint32_t persist2 = kSMs * (it >= 16 ? 2 : 3);
     const size_t sm_part = MsSmem::bytes(p.cbins), sm_ref = MsSmem::bytes(1u << (p.cshift - p.fshift));
-    const size_t sm_part2 = (size_t)MS2_TILE * 12 + MsSmem::bytes(p.cbins, MS2_TILE);
-    const size_t sm_ref2 = (size_t)MS2_TILE * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), MS2_TILE);
+    const size_t sm_part2 = (size_t)tile2 * 12 + MsSmem::bytes(p.cbins, tile2);
+    const size_t sm_ref2 = (size_t)tile2 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), tile2);
     if (p.ms_version == 2) {
-        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_partition2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part2));
-        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_refine2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref2));
+        auto kp = it >= 16 ? k_rs_rec_partition2<16> : k_rs_rec_partition2<8>;
+        auto kr = it >= 16 ? k_rs_rec_refine2<16> : k_rs_rec_refine2<8>;
+        SG_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part2));
+        SG_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref2));
         rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
-        k_rs_rec_partition2<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs,
-                                                                   b.st, p.cshift, p.cbins);
+        kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift,
+                                                  p.cbins);
         rec.end();
         SG_LAUNCH_CHECK();
     } else {
@@ -1706,8 +1713,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     rec.begin(K_RS5_REFINE, 0, p.ms_version == 2 ? persist2 : persist, MS_THREADS, n);
     if (p.ms_version == 2)
-        k_rs_rec_refine2<<<persist2, MS_THREADS, sm_ref2, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n,
-                                                               p.cshift, p.fshift);
+        (it >= 16 ? k_rs_rec_refine2<16> : k_rs_rec_refine2<8>)<<<persist2, MS_THREADS, sm_ref2, s>>>(
+            b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
     else
         k_rs_rec_refine<<<persist, MS_THREADS, sm_ref, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
                                                             p.fshift);
@@ -1727,6 +1734,36 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
 static int read_status(const ListStatus* st_dev, ListStatus& h, cudaStream_t s) {
     SG_CUDA(cudaMemcpyAsync(&h, st_dev, sizeof(ListStatus), cudaMemcpyDeviceToHost, s));
     SG_CUDA(cudaStreamSynchronize(s));
+    return SG_OK;
+}
+
+// pinned host copy of the status block, enqueued behind the pipeline so the
+// call synchronises once
+static ListStatus* pinned_status() {
+    static thread_local ListStatus* p = nullptr;
+    if (!p && cudaMallocHost(&p, sizeof(ListStatus)) != cudaSuccess) p = nullptr;
+    return p;
+}
+
+// meta["splitter_set"] request, served on the same stream before the sync
+struct MetaReq {
+    const int64_t* spl;
+    uint32_t r;
+    int64_t* dev_out;   // 3 x r
+    int64_t* host_out;  // 3 x r (pinned for an async copy)
+    void* ws;
+    size_t ws_bytes;
+};
+
+template <class OutT>
+static int enqueue_meta(const MetaReq* mr, const void* rank, uint64_t n, cudaStream_t s) {
+    if (!mr || mr->r == 0) return SG_OK;
+    const int odt = sizeof(OutT) == 8 ? SG_I64 : (std::is_signed<OutT>::value ? SG_I32 : SG_U32);
+    const int rc = sg_splitter_meta(rank, odt, n, mr->spl, mr->r, mr->dev_out, mr->ws, mr->ws_bytes, s);
+    if (rc != SG_OK) return rc;
+    if (mr->host_out)
+        SG_CUDA(cudaMemcpyAsync(mr->host_out, mr->dev_out, sizeof(int64_t) * 3 * (size_t)mr->r, cudaMemcpyDeviceToHost,
+                                s));
     return SG_OK;
 }
 
@@ -1776,7 +1813,7 @@ static int wyllie_entry(const void* succ_v, void* rank_v, uint64_t n, int varian
 
 template <class SuccT, class OutT>
 static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
-                    cudaStream_t s, sg_stats* stats, sg_violation* viol) {
+                    cudaStream_t s, sg_stats* stats, sg_violation* viol, const MetaReq* mr) {
     const RsPlan p = plan_rs(n, seed, (int)sizeof(OutT));
     ms_configure();
     Carver c(ws, ws_bytes);
@@ -1789,24 +1826,35 @@ static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed,
         for (int k = 0; k < SG_MAX_LEVELS; ++k) stats->level_size[k] = 0;
     }
     Recorder rec(stats, s);
+    auto wyllie_instead = [&](Recorder& r, sg_stats* st) -> int {
+        if (stats) stats->fallback = 1;
+        return wyllie_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, SG_WY_MULTI_KERNEL, b.st, b.word0, s, r,
+                                       st);
+    };
+    ListStatus* hs = pinned_status();
+    ListStatus hloc;
+    ListStatus& h = hs ? *hs : hloc;
     if (p.levels > 0 && !p.rec_ok) {
         // output windows would not fit shared memory (n > ~2^31): pointer jumping
-        if (stats) stats->fallback = 1;
-        int rc = wyllie_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, SG_WY_MULTI_KERNEL, b.st, b.word0, s,
-                                         rec, stats);
+        int rc = wyllie_instead(rec, stats);
+        if (rc != SG_OK) return rc;
+        rc = enqueue_meta<OutT>(mr, rank_v, n, s);
         if (rc != SG_OK) return rc;
         SG_CUDA(rec.finish());
-        ListStatus h;
         rc = read_status(b.st, h, s);
         if (rc != SG_OK) return rc;
         return classify(h, n, viol);
     }
     int rc = rs_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, p, b, s, rec, stats);
     if (rc != SG_OK) return rc;
-    SG_CUDA(rec.finish());
-    ListStatus h;
-    rc = read_status(b.st, h, s);
+    rc = enqueue_meta<OutT>(mr, rank_v, n, s);
     if (rc != SG_OK) return rc;
+    if (hs) SG_CUDA(cudaMemcpyAsync(hs, b.st, sizeof(ListStatus), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(rec.finish());  // the one synchronisation of a normal call
+    if (!hs) {
+        rc = read_status(b.st, h, s);
+        if (rc != SG_OK) return rc;
+    }
     if (stats) {
         for (int k = 0; k <= p.levels && k < SG_MAX_LEVELS; ++k) stats->level_size[k] = h.R[k];
         stats->list_path = h.local ? 1u : 0u;
@@ -1814,10 +1862,10 @@ static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed,
     if (h.oor_first == NONE64 && h.loop_count == 1 && h.overflow) {
         // a walk hit the hop cap or a level overflowed its capacity: rank the
         // list by pointer jumping instead (terminates on every input)
-        if (stats) stats->fallback = 1;
         Recorder rec2(nullptr, s);
-        rc = wyllie_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, SG_WY_MULTI_KERNEL, b.st, b.word0, s,
-                                     rec2, nullptr);
+        rc = wyllie_instead(rec2, nullptr);
+        if (rc != SG_OK) return rc;
+        rc = enqueue_meta<OutT>(mr, rank_v, n, s);
         if (rc != SG_OK) return rc;
         SG_CUDA(rec2.finish());
         rc = read_status(b.st, h, s);
@@ -1881,7 +1929,18 @@ int sg_rs_rank(const void* succ, int succ_dtype, void* rank, int rank_dtype, uin
     ::sg::apply_tuning();
     if (st) memset(st, 0, sizeof(sg_stats));
     SG_DISPATCH_LIST(rs_entry, succ_dtype, rank_dtype, succ, rank, n, seed, ws, ws_bytes, (cudaStream_t)stream, st,
-                     viol);
+                     viol, (const MetaReq*)nullptr);
+}
+
+int sg_rs_rank_meta(const void* succ, int succ_dtype, void* rank, int rank_dtype, uint64_t n, uint64_t seed, void* ws,
+                    size_t ws_bytes, const int64_t* spl, uint32_t r, int64_t* meta_dev, int64_t* meta_host,
+                    void* meta_ws, size_t meta_ws_bytes, void* stream, sg_stats* st, sg_violation* viol) {
+    if (n == 0 || n >= 0xFFFFFFFFull) return SG_ERR_CAPABILITY;
+    ::sg::apply_tuning();
+    if (st) memset(st, 0, sizeof(sg_stats));
+    const MetaReq mr{spl, r, meta_dev, meta_host, meta_ws, meta_ws_bytes};
+    SG_DISPATCH_LIST(rs_entry, succ_dtype, rank_dtype, succ, rank, n, seed, ws, ws_bytes, (cudaStream_t)stream, st,
+                     viol, &mr);
 }
 
 }  // extern "C"

@@ -25,13 +25,13 @@ constexpr int MS_ITEMS = 8;
 constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
 constexpr int MS_MAXB = 1024;
 
-// peer ranking: 0 match.any, 1 ballots (SG_MS_PEERS, for measurement)
+// peer ranking: 0 match.any, 1 ballots, 2 alternate per item (SG_MS_PEERS)
 static __constant__ int g_ms_peers = 1;
 
 static inline void ms_configure() {
     const char* e = getenv("SG_MS_PEERS");
     if (e && *e) {
-        const int v = atoi(e) ? 1 : 0;
+        const int v = atoi(e);
         cudaMemcpyToSymbol(g_ms_peers, &v, sizeof(int));
     }
 }
@@ -80,7 +80,7 @@ __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], 
     for (int j = 0; j < ITEMS; ++j) {
         // peers: lanes with the same bin
         unsigned peers;
-        if (g_ms_peers == 0) {
+        if (g_ms_peers == 0 || (g_ms_peers == 2 && (j & 1))) {  // 2: alternate, MIO and ALU side by side
             peers = __match_any_sync(0xffffffffu, bn[j]);
         } else {
             // bit-by-bit ballots over the NBITS bin bits (VOTE is an ALU op;

@@ -116,9 +116,11 @@ def _raise_invalid(sl, code, viol):
     raise InvalidListError(str(ListViolation(VIOLATION_KINDS.get(kind, "unreachable"), int(index))))
 
 
-def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False):
+def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=None):
     """Rank `sl` on the GPU.  Returns (rank tensor, native stats, status,
-    violation, host_input)."""
+    violation, host_input).  `meta` = (spl_nodes, cache key) asks the ruling
+    set call for meta["splitter_set"] in the same device pass; its host copy
+    is returned through meta_out (a list) as a (3, r) int64 array."""
     n = sl.n
     if n >= 0xFFFFFFFF:
         raise CapabilityError(f"device node ids are 32-bit: n={n} is too large")
@@ -142,8 +144,21 @@ def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False):
                                   ws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
         else:
             ws = _device.workspace(L.sg_rs_workspace_bytes(n), dev)
-            rc = L.sg_rs_rank(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
-                              _device.ptr(ws), ws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
+            if meta is None:
+                rc = L.sg_rs_rank(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
+                                  _device.ptr(ws), ws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
+            else:
+                spl_nodes, key, meta_out = meta
+                r = len(spl_nodes)
+                idx = _device_index(spl_nodes, dev, key)
+                res = torch.empty((3, r), dtype=torch.int64, device=dev)
+                host = _pinned_meta(3 * r)
+                mws = _device.workspace(L.sg_splitter_meta_workspace_bytes(r), dev)
+                rc = L.sg_rs_rank_meta(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
+                                       _device.ptr(ws), ws.numel(), _device.ptr(idx), r, _device.ptr(res),
+                                       ctypes.c_void_p(host.data_ptr()), _device.ptr(mws), mws.numel(), stream,
+                                       ctypes.byref(st), ctypes.byref(viol))
+                meta_out.append(host[:3 * r].numpy().reshape(3, r).copy())
         del ws
     if rc not in (_native.SG_OK, _native.SG_ERR_INVALID_LIST):
         _native.check(rc, f"sg_{kind}_rank")
@@ -224,6 +239,16 @@ def _draw_splitters_cached(n, r, seed):
 
 
 _IDX_CACHE = {}
+_PINNED = {}
+
+
+def _pinned_meta(count):
+    """Reused pinned host staging for the splitter meta (copied out per call)."""
+    buf = _PINNED.get("meta")
+    if buf is None or buf.numel() < count:
+        buf = torch.empty(max(count, 3 * 16384), dtype=torch.int64, pin_memory=True)
+        _PINNED["meta"] = buf
+    return buf
 
 
 def _device_index(spl_nodes, dev, key):
@@ -268,7 +293,10 @@ def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_su
     p = int(p)
     packing = _as_packing(packing)
     err = _rs_param_error(n, p, packing, block_size, backend, accounting)
-    rank, st, rc, viol, host_input = _run_list("rs", sl, 0, seed, reuse_succ, scratch_out=err is not None)
+    meta = None
+    if not even and err is None and 0 < p < n and n < 0xFFFFFFFF:
+        meta = (_draw_splitters(n, p, seed), (n, p, int(seed)), [])
+    rank, st, rc, viol, host_input = _run_list("rs", sl, 0, seed, reuse_succ, scratch_out=err is not None, meta=meta)
     if rc == _native.SG_ERR_INVALID_LIST:
         _raise_invalid(sl, rc, viol)
     if err is not None:
@@ -283,9 +311,14 @@ def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_su
         node_at = torch.empty(n, dtype=torch.int64, device=rank.device)
         node_at[(n - 1) - rank.to(torch.int64)] = torch.arange(n, dtype=torch.int64, device=rank.device)
         spl_nodes = node_at[:: n // p].cpu().numpy()
+        splitters = _splitter_set(rank, spl_nodes, n)
+    elif meta is not None and meta[2]:
+        host = meta[2][0]
+        splitters = SplitterSet(p, np.ascontiguousarray(meta[0], dtype=np.int64))
+        splitters.splitter_rank, splitters.sublist_len, splitters.splitter_succ = host[0], host[1], host[2]
     else:
         spl_nodes = _draw_splitters(n, p, seed)
-    splitters = _splitter_set(rank, spl_nodes, n, key=None if even else (n, p, int(seed)))
+        splitters = _splitter_set(rank, spl_nodes, n, key=(n, p, int(seed)))
     stats.meta.update(n=n, p=p, packing=packing.value, splitter_set=splitters,
                       max_sublist=int(splitters.sublist_len.max()),
                       levels=int(st.levels), level_size=[int(st.level_size[k]) for k in range(st.levels + 1)],

@@ -90,10 +90,14 @@ def test_draw_splitters_match_reference(golden):
 
 # ---- splitter set from ranks (host tensors stand in for device ones) ----------
 
-def test_splitter_set_from_ranks(golden, orc):
+@pytest.mark.gpu
+def test_splitter_set_from_ranks(golden, orc, cuda):
+    """meta["splitter_set"] derivation (sg_splitter_meta) from oracle ranks
+    vs the reference's own RS3/RS4 outputs."""
     for n, p, ls, s in golden["rs_cases"].tolist():
         key = f"rs_{n}_{p}_{ls}_{s}"
         rank = torch.from_numpy(orc.seq_rank(orc.gen_list(n, ls))) if n > 3 else torch.tensor([2, 1, 0])
+        rank = rank.to(cuda)
         spl = _splitter_set(rank, _draw_splitters(n, p, s), n)
         assert spl.r == p
         assert np.array_equal(spl.splitter_node, golden[key + "_node"])

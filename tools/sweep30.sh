@@ -1,0 +1,5 @@
+#!/bin/bash
+python -c "import __graft_entry__ as e; e.build()" > /dev/null 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+python tools/probe_overhead.py lr26
+for w in lr26 lr28 lr28o; do timeout 200 python tools/probe_one.py $w 5; done
