@@ -525,7 +525,7 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
     SG_LAUNCH_CHECK();
     if (((uintptr_t)view.e & 15) == 0) {
         const size_t smem = (size_t)MS2_TILE * E::kBytes + MsSmem::bytes((uint32_t)p.parts, MS2_TILE);
-        SG_CUDA(cudaFuncSetAttribute(k_cc_part_scatter2<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SG_CUDA(set_smem_max(k_cc_part_scatter2<E>, smem));
         const unsigned long long ntile = (m + MS2_TILE - 1) / MS2_TILE;
         const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * PART2_CTAS_PER_SM ? ntile
                                                                                             : kSMs * PART2_CTAS_PER_SM);
@@ -533,7 +533,7 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
                                                            b.edges);
     } else {
         const size_t smem = MsSmem::bytes((uint32_t)p.parts);
-        SG_CUDA(cudaFuncSetAttribute(k_cc_part_scatter<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SG_CUDA(set_smem_max(k_cc_part_scatter<E>, smem));
         const unsigned long long ntile = (m + MS_TILE - 1) / MS_TILE;
         const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * 4 ? ntile : kSMs * 4);
         k_cc_part_scatter<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <utility>
 #include <vector>
 
 #include "sg.h"
@@ -110,9 +112,25 @@ class Recorder {
     sg_stats* st_;
     cudaStream_t s_;
     std::vector<cudaEvent_t> ev_;
+    std::vector<size_t> begin_ix_, end_ix_;  // event indices of each launch
     int open_ = -1;
+    bool shared_ = false;  // the last end event doubles as the next begin event
     cudaEvent_t t0_ = nullptr;
 };
+
+// Raise a kernel's dynamic shared memory limit once per device (the attribute
+// persists; setting it on every call costs host time on short pipelines).
+template <class F>
+inline cudaError_t set_smem_max(F* f, size_t bytes) {
+    static thread_local std::map<std::pair<int, const void*>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    size_t& have = done[std::make_pair(dev, (const void*)f)];
+    if (have >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
 
 // Workspace carving ------------------------------------------------------------
 struct Carver {

@@ -1563,7 +1563,7 @@ static int launch_contract(uint32_t grid, cudaStream_t s, const SuccT* succ, Lis
                            uint32_t* node_word) {
     const bool vec = ((uintptr_t)succ & 15) == 0;
     auto k = vec ? k_rs_contract<SuccT, true> : k_rs_contract<SuccT, false>;
-    SG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ContractSmem)));
+    SG_CUDA(set_smem_max(k, sizeof(ContractSmem)));
     k<<<grid, TILE_THREADS, sizeof(ContractSmem), s>>>(succ, st, tile_off, headsid, seg_head, seg_succ, lvl1,
                                                        node_word);
     return SG_OK;
@@ -1695,16 +1695,16 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     if (p.ms_version == 2) {
         auto kp = it >= 16 ? k_rs_rec_partition2<16> : k_rs_rec_partition2<8>;
         auto kr = it >= 16 ? k_rs_rec_refine2<16> : k_rs_rec_refine2<8>;
-        SG_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part2));
-        SG_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref2));
+        SG_CUDA(set_smem_max(kp, sm_part2));
+        SG_CUDA(set_smem_max(kr, sm_ref2));
         rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
         kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift,
                                                   p.cbins);
         rec.end();
         SG_LAUNCH_CHECK();
     } else {
-        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_part));
-        SG_CUDA(cudaFuncSetAttribute(k_rs_rec_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ref));
+        SG_CUDA(set_smem_max(k_rs_rec_partition, sm_part));
+        SG_CUDA(set_smem_max(k_rs_rec_refine, sm_ref));
         rec.begin(K_RS5_PARTITION, 0, persist, MS_THREADS, n);
         k_rs_rec_partition<<<persist, MS_THREADS, sm_part, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
                                                                 p.cshift, p.cbins);

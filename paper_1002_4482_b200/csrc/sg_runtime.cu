@@ -38,6 +38,7 @@ Recorder::Recorder(sg_stats* st, cudaStream_t s) : st_(st), s_(s) {
         t0_ = pool_event(0);
         if (t0_) cudaEventRecord(t0_, s_);
         ev_.push_back(t0_);
+        shared_ = true;  // the first launch starts at t0
     }
 }
 
@@ -57,9 +58,15 @@ void Recorder::begin(int kernel, int round, uint32_t blocks, uint32_t threads, u
     L.items = items;
     L.ms = 0.f;
     L.pad = 0;
-    cudaEvent_t a = pool_event(ev_.size());
-    if (a) cudaEventRecord(a, s_);
-    ev_.push_back(a);
+    if (shared_) {  // back-to-back launches: the previous end event starts this one
+        begin_ix_.push_back(ev_.size() - 1);
+    } else {
+        cudaEvent_t a = pool_event(ev_.size());
+        if (a) cudaEventRecord(a, s_);
+        ev_.push_back(a);
+        begin_ix_.push_back(ev_.size() - 1);
+    }
+    shared_ = false;
     open_ = int(k);
 }
 
@@ -68,16 +75,17 @@ void Recorder::end() {
     cudaEvent_t b = pool_event(ev_.size());
     if (b) cudaEventRecord(b, s_);
     ev_.push_back(b);
+    end_ix_.push_back(ev_.size() - 1);
     st_->n_launches = uint32_t(open_) + 1;
     open_ = -1;
+    shared_ = true;
 }
 
 cudaError_t Recorder::finish() {
     cudaError_t e = cudaStreamSynchronize(s_);
     if (e != cudaSuccess || !st_) return e;
-    // ev_[0] = t0, then (begin, end) pairs in launch order
-    for (uint32_t k = 0; k < st_->n_launches; ++k) {
-        size_t ia = 1 + 2 * size_t(k), ib = ia + 1;
+    for (uint32_t k = 0; k < st_->n_launches && k < begin_ix_.size() && k < end_ix_.size(); ++k) {
+        const size_t ia = begin_ix_[k], ib = end_ix_[k];
         if (ib < ev_.size() && ev_[ia] && ev_[ib]) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, ev_[ia], ev_[ib]) == cudaSuccess) st_->launch[k].ms = ms;
