@@ -56,8 +56,8 @@ def kernel_bytes(kernel, order, out):
         "rs5_partition": 12 + 8,                       # record {cur, sid|local} in, {cur, rank} pair out
         "rs5_refine": 8 + 8,
         "rs5_scatter": 8 + out,
-        "rs3_contract": 4,                             # succ in (segments out are O(n / 4096))
-        "rs5_expand": 4 + out,                         # succ in, rank out
+        "rs3_contract": 4 + 4,                         # succ in, {segment, distance} word out
+        "rs5_expand": 4 + out,                         # node word in, rank out
         "rs1_validate": 4,
         "cc_hook_uf": CC_EDGE_SWEEP_BYTES,
         "cc_hook_sv": CC_EDGE_SWEEP_BYTES,
