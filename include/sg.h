@@ -213,6 +213,13 @@ int sg_cc_hook_part(const void* edges, int edge_dtype, uint64_t m, uint64_t row0
                     void* ws, size_t ws_bytes, int reuse, void* stream);
 /* D[i] = root(i) for lo <= i < hi; adds the number of roots in [lo,hi)
  * to *roots (device u64). */
+/* Sparse merge for the sharded rounds: append (i, D[i]) for every i < n with
+ * D[i] != Dold[i] (count accumulates; at most cap written), and lower
+ * D[idx[j]] to val[j] (atomic min) for j < k. */
+int sg_cc_changes(const uint32_t* Dold, const uint32_t* D, uint64_t n, uint32_t* idx,
+                  uint32_t* val, uint64_t cap, uint64_t* count, void* stream);
+int sg_cc_apply_min(uint32_t* D, const uint32_t* idx, const uint32_t* val, uint64_t k,
+                    void* stream);
 int sg_cc_compress(uint32_t* D, uint64_t lo, uint64_t hi, uint64_t* roots,
                    void* stream);
 /* out[i] = (dtype) D[i] for i < n */

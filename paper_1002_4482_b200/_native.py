@@ -37,7 +37,7 @@ EXPORTS = (
     "sg_wyllie_workspace_bytes", "sg_rs_workspace_bytes", "sg_wyllie_rank", "sg_rs_rank",
     "sg_gather_i64", "sg_cc_workspace_bytes", "sg_cc", "sg_cc_init", "sg_cc_hook",
     "sg_cc_hook_workspace_bytes", "sg_cc_hook_part", "sg_splitter_meta_workspace_bytes", "sg_splitter_meta",
-    "sg_rs_rank_meta",
+    "sg_rs_rank_meta", "sg_cc_changes", "sg_cc_apply_min",
     "sg_cc_compress", "sg_cc_labels", "sg_kiss_batch_host", "sg_kiss_device",
     "sg_list_from_order", "sg_edge_keys", "sg_edges_from_keys", "sg_list_violation_host",
 )
@@ -93,6 +93,8 @@ _SIGS = {
     "sg_cc_hook_workspace_bytes": (_SZ, [_U64, _U64]),
     "sg_cc_hook_part": (_I, [_P, _I, _U64, _U64, _U64, _P, _I, _I, _P, _P, _SZ, _I, _P]),
     "sg_cc_compress": (_I, [_P, _U64, _U64, _P, _P]),
+    "sg_cc_changes": (_I, [_P, _P, _U64, _P, _P, _U64, _P, _P]),
+    "sg_cc_apply_min": (_I, [_P, _P, _P, _U64, _P]),
     "sg_cc_labels": (_I, [_P, _U64, _P, _I, _P]),
     "sg_kiss_batch_host": (_I, [ctypes.POINTER(ctypes.c_uint64), _U64, _P]),
     "sg_kiss_device": (_I, [_P, _U64, _U64, _U64, _P, _P]),

@@ -444,6 +444,42 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
 }
 
 // ---------------------------------------------------------------------------
+// sparse merge of the sharded rounds (dist.py): after the dense merge of
+// round 1 every replica is identical, so later rounds only exchange the
+// entries a rank's hook sweep lowered
+
+__global__ void k_cc_changes(const uint32_t* __restrict__ Dold, const uint32_t* __restrict__ D, unsigned long long n,
+                             uint32_t* __restrict__ idx, uint32_t* __restrict__ val, unsigned long long cap,
+                             unsigned long long* __restrict__ count) {
+    const uint32_t lane = lane_id();
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const unsigned long long i = i0 + threadIdx.x;
+        const uint32_t d = i < n ? D[i] : 0u;
+        const bool ch = i < n && d != Dold[i];
+        const unsigned m = __ballot_sync(0xffffffffu, ch);
+        if (m == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (ch) {
+            const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
+            if (k < cap) {
+                idx[k] = (uint32_t)i;
+                val[k] = d;
+            }
+        }
+    }
+}
+
+__global__ void k_cc_apply_min(uint32_t* __restrict__ D, const uint32_t* __restrict__ idx,
+                               const uint32_t* __restrict__ val, unsigned long long k) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride)
+        atomicMin(D + idx[i], val[i]);
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 static uint32_t hook_grid(unsigned long long m) { return grid_for(m, HOOK_THREADS, 4, kSMs * 8); }
@@ -796,6 +832,23 @@ int sg_cc_hook_part(const void* edges, int edge_dtype, uint64_t m, uint64_t row0
         if (rc != SG_OK) return rc;
     }
     return hook_partitions(p, b, m, n, D, variant, (unsigned long long*)flags, s);
+}
+
+int sg_cc_changes(const uint32_t* Dold, const uint32_t* D, uint64_t n, uint32_t* idx, uint32_t* val, uint64_t cap,
+                  uint64_t* count, void* stream) {
+    if (n == 0) return SG_OK;
+    // count is accumulated: the caller zeroes it
+    k_cc_changes<<<vtx_grid(n), COMP_THREADS, 0, (cudaStream_t)stream>>>(Dold, D, n, idx, val, cap,
+                                                                          (unsigned long long*)count);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+int sg_cc_apply_min(uint32_t* D, const uint32_t* idx, const uint32_t* val, uint64_t k, void* stream) {
+    if (k == 0) return SG_OK;
+    k_cc_apply_min<<<vtx_grid(k), COMP_THREADS, 0, (cudaStream_t)stream>>>(D, idx, val, k);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
 }
 
 int sg_cc_compress(uint32_t* D, uint64_t lo, uint64_t hi, uint64_t* roots, void* stream) {

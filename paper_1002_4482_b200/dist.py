@@ -99,6 +99,19 @@ class CudaOps:
         _native.check(self.lib.sg_cc_compress(_device.ptr(D), lo, hi, _device.ptr(roots), self.stream()),
                       "sg_cc_compress")
 
+    def changes(self, Dold, D, n, cap):
+        """(idx, val, count tensor) of the entries i < n this rank lowered."""
+        idx = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
+        val = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _native.check(self.lib.sg_cc_changes(_device.ptr(Dold), _device.ptr(D), n, _device.ptr(idx), _device.ptr(val),
+                                             cap, _device.ptr(cnt), self.stream()), "sg_cc_changes")
+        return idx, val, cnt
+
+    def apply_min(self, D, idx, val):
+        _native.check(self.lib.sg_cc_apply_min(_device.ptr(D), _device.ptr(idx), _device.ptr(val), idx.numel(),
+                                               self.stream()), "sg_cc_apply_min")
+
     def synchronize(self):
         torch.cuda.synchronize(self.device)
 
@@ -125,7 +138,7 @@ class CudaTrace:
         self.spans.append((name, a, b))
 
 
-def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None, trace=None):
+def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None, trace=None, sparse_cap=None):
     """Run the sharded rounds.  `edges` is this rank's (m_g, 2) block whose
     first row is global row `row0`.  Returns (D replica as int32 tensor of
     size >= n, info dict)."""
@@ -144,12 +157,16 @@ def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None
     roots = torch.zeros(1, dtype=torch.int64, device=D.device)
     info = {"rounds": 0, "roots_per_round": [n], "edge_sweeps": 0, "vertex_sweeps": 0,
             "allreduce_bytes": 0, "allgather_bytes": 0, "comm_s": 0.0}
+    # sparse merge while every rank lowered at most n/8/G entries
+    cap = max(1, (n // 8) // G) if sparse_cap is None else max(1, int(sparse_cap))
+    sparse = hasattr(ops, "changes")
     r = 0
     while True:
         r += 1
         if r > bound:
             raise RuntimeError(f"no convergence after {r - 1} rounds (bound {bound})")
         flags.zero_()
+        Dold = D.clone() if (sparse and r > 1 and G > 1) else None
         with trace.span("cc_hook_uf" if variant == "uf" else "cc_hook_sv"):
             ops.hook(edges, row0, n, D, variant, r == 1, flags)
         info["edge_sweeps"] += 1
@@ -165,13 +182,40 @@ def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None
         # one UF sweep unites every edge of the block, so a single rank is
         # done after round 1 (the single-GPU path's one-sweep argument)
         changed = int(flags[0].item()) and not (variant == "uf" and G == 1)
-        D[n] = 0 if changed else 1
         t0 = time.perf_counter()
-        with trace.span("nccl_allreduce_min"):
-            comm.allreduce_min_(D)
+        if Dold is not None:
+            # replicas are identical after the previous merge: exchange only
+            # the entries this round lowered (hooks and path halving), padded
+            # to the largest rank's count; dense if that is too many
+            idx, val, cnt = ops.changes(Dold, D, n, cap)
+            hdr = torch.stack([cnt[0], torch.tensor(int(changed), dtype=torch.int64, device=D.device)])
+            comm.allreduce_max_(hdr)
+            kmax, any_changed = (int(x) for x in hdr.cpu().tolist())
+            converged = any_changed == 0
+            if not converged and kmax <= cap:
+                k = int(cnt.item())
+                if kmax > k:  # pad: (0, int32 max) is a no-op min on D[0] == 0
+                    idx[k:kmax] = 0
+                    val[k:kmax] = 0x7FFFFFFF
+                gi = torch.empty(G * kmax, dtype=torch.int32, device=D.device)
+                gv = torch.empty(G * kmax, dtype=torch.int32, device=D.device)
+                with trace.span("nccl_allgather_changes"):
+                    comm.allgather_(gi, idx[:kmax].contiguous())
+                    comm.allgather_(gv, val[:kmax].contiguous())
+                ops.apply_min(D, gi, gv)
+                info["sparse_rounds"] = info.get("sparse_rounds", 0) + 1
+                info["allgather_bytes"] += 2 * G * kmax * 4
+            elif not converged:
+                with trace.span("nccl_allreduce_min"):
+                    comm.allreduce_min_(D)
+                info["allreduce_bytes"] += D.numel() * D.element_size()
+        else:
+            D[n] = 0 if changed else 1
+            with trace.span("nccl_allreduce_min"):
+                comm.allreduce_min_(D)
+            info["allreduce_bytes"] += D.numel() * D.element_size()
+            converged = int(D[n].item()) == 1
         info["comm_s"] += time.perf_counter() - t0
-        info["allreduce_bytes"] += D.numel() * D.element_size()
-        converged = int(D[n].item()) == 1
         if variant == "sv" or converged:
             roots.zero_()
             with trace.span("cc_shortcut"):

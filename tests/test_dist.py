@@ -62,6 +62,19 @@ class HostOps:
         if changed:
             flags[0] = 1
 
+    def changes(self, Dold, D, n, cap):
+        ch = torch.nonzero(D[:n] != Dold[:n]).flatten()
+        k = ch.numel()
+        idx = torch.zeros(max(cap, 1), dtype=torch.int32)
+        val = torch.zeros(max(cap, 1), dtype=torch.int32)
+        kk = min(k, cap)
+        idx[:kk] = ch[:kk].to(torch.int32)
+        val[:kk] = D[ch[:kk]]
+        return idx, val, torch.tensor([k], dtype=torch.int64)
+
+    def apply_min(self, D, idx, val):
+        np.minimum.at(D.numpy(), idx.numpy().astype(np.int64), val.numpy())
+
     def compress(self, D, lo, hi, roots):
         d = D.numpy()
         c = 0
@@ -82,7 +95,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, edges, variant, q):
+def _worker(rank, world, port, n, edges, variant, q, sparse_cap=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -93,7 +106,7 @@ def _worker(rank, world, port, n, edges, variant, q):
         r1 = min(r0 + per, m)
         blk = torch.from_numpy(np.ascontiguousarray(edges[r0:r1]).reshape(-1, 2))
         try:
-            D, info = sharded_components(n, blk, r0, TorchDistComm(), HostOps(), variant=variant)
+            D, info = sharded_components(n, blk, r0, TorchDistComm(), HostOps(), variant=variant, sparse_cap=sparse_cap)
             q.put((rank, "ok", D[:n].numpy().copy(), info))
         except Exception as exc:  # report to the parent
             q.put((rank, "err", type(exc).__name__, str(exc)))
@@ -101,11 +114,11 @@ def _worker(rank, world, port, n, edges, variant, q):
         dist.destroy_process_group()
 
 
-def _run(n, edges, variant, world=2):
+def _run(n, edges, variant, world=2, sparse_cap=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, edges, variant, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, edges, variant, q, sparse_cap)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=120) for _ in range(world)]
@@ -118,14 +131,20 @@ def _run(n, edges, variant, world=2):
 def test_two_rank_components_match_oracle(orc, variant):
     from paper_1002_4482_b200 import gen_random_graph, gen_tree_graph
 
-    for gr in (gen_random_graph(400, 0.004, seed=3), gen_tree_graph(600, 2, seed=1)):
+    sparse = 0
+    for gr in (gen_random_graph(400, 0.004, seed=3), gen_tree_graph(600, 2, seed=1),
+               gen_random_graph(3000, 0.0004, seed=5)):
         want = orc.seq_components(gr.n, gr.edges)
-        res = _run(gr.n, gr.edges, variant)
-        for rank, status, D, info in res:
-            assert status == "ok", D
-            assert np.array_equal(D.astype(np.int64), want), (variant, rank)
-            assert info["roots_per_round"][-1] == len(np.unique(want))
-            assert info["rounds"] <= 30
+        for cap in (None, gr.n):  # default threshold, and always-sparse after round 1
+            res = _run(gr.n, gr.edges, variant, sparse_cap=cap)
+            for rank, status, D, info in res:
+                assert status == "ok", D
+                assert np.array_equal(D.astype(np.int64), want), (variant, rank)
+                assert info["roots_per_round"][-1] == len(np.unique(want))
+                assert info["rounds"] <= 30
+                sparse += info.get("sparse_rounds", 0)
+    if variant == "uf":
+        assert sparse > 0  # rounds after the first merged only the lowered entries
 
 
 def test_two_rank_edgeless(orc):
