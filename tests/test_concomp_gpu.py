@@ -247,3 +247,39 @@ def test_sharded_path_on_nccl_single_rank(cuda, orc, monkeypatch, tmp_path, vari
             sgdist.sv_components_dist(g.EdgeGraph(60_000, e), 8, variant=variant)
     finally:
         dist.destroy_process_group()
+
+
+def test_sparse_merge_building_blocks(cuda):
+    """sg_cc_changes / sg_cc_apply_min: the sharded rounds' changed-entry
+    exchange (dist.py) reproduces the dense min all-reduce."""
+    L = _native.lib()
+    n = 1 << 20
+    rng = np.random.default_rng(7)
+    base = np.arange(n, dtype=np.int32)
+    a = base.copy()
+    b = base.copy()
+    ia = rng.choice(n, 5000, replace=False)
+    ib = rng.choice(n, 7000, replace=False)
+    a[ia] = (ia * rng.random(ia.size)).astype(np.int32)
+    b[ib] = (ib * rng.random(ib.size)).astype(np.int32)
+    old = torch.from_numpy(base).to(cuda)
+    out = {}
+    for name, arr in (("a", a), ("b", b)):
+        D = torch.from_numpy(arr).to(cuda)
+        cap = 8192
+        idx = torch.empty(cap, dtype=torch.int32, device=cuda)
+        val = torch.empty(cap, dtype=torch.int32, device=cuda)
+        cnt = torch.zeros(1, dtype=torch.int64, device=cuda)
+        rc = L.sg_cc_changes(_device.ptr(old), _device.ptr(D), n, _device.ptr(idx), _device.ptr(val), cap,
+                             _device.ptr(cnt), _device.stream_ptr(cuda))
+        assert rc == 0
+        k = int(cnt.item())
+        assert k == int((arr != base).sum())
+        got = dict(zip(idx[:k].cpu().tolist(), val[:k].cpu().tolist()))
+        assert got == {int(i): int(arr[i]) for i in np.flatnonzero(arr != base)}
+        out[name] = (idx[:k], val[:k])
+    D = torch.from_numpy(a).to(cuda)  # rank a applies rank b's changes
+    rc = L.sg_cc_apply_min(_device.ptr(D), _device.ptr(out["b"][0]), _device.ptr(out["b"][1]), out["b"][0].numel(),
+                           _device.stream_ptr(cuda))
+    assert rc == 0
+    assert np.array_equal(D.cpu().numpy(), np.minimum(a, b))
