@@ -609,7 +609,9 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
 
 constexpr int REC_CH = 1024;
 
-template <class SuccT>
+// kPacked: one u64 record {cur : 64-sb | sid : sb-lb | local : lb} instead of
+// cur u32 + {sid, local} u64 (the host picks the field widths from n)
+template <class SuccT, bool kPacked>
 __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_rec(const SuccT* __restrict__ succ,
                                                               const uint2* __restrict__ rgrp,
                                                               const uint32_t* __restrict__ spl,
@@ -617,8 +619,8 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
                                                               unsigned long long* __restrict__ rec_sl,
                                                               ListStatus* st, uint32_t kbits, uint32_t salt,
                                                               uint32_t cap_hops, unsigned long long maxchunks,
-                                                              int load_mode) {
-    if (layout_local(st)) return;  // k_rs_walk<Level0> takes this list
+                                                              int load_mode, uint32_t sb, uint32_t lb) {
+    if (layout_local(st)) return;  // k_rs_contract takes this list
     const unsigned long long N = st->R[0];
     const unsigned long long R = st->R[1];
     unsigned long long* q = &st->qhead[0];
@@ -630,7 +632,12 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
     bool done = false;
     auto close_chunk = [&]() {  // pad the tail with NIL records
         if (chunk == ~0ull) return;
-        for (uint32_t k = fill + lane; k < REC_CH; k += 32) rec_cur[chunk * REC_CH + k] = NIL;
+        for (uint32_t k = fill + lane; k < REC_CH; k += 32) {
+            if (kPacked)
+                rec_sl[chunk * REC_CH + k] = ~0ull;
+            else
+                rec_cur[chunk * REC_CH + k] = NIL;
+        }
     };
     ChainPool pool;
     for (;;) {
@@ -665,8 +672,12 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
         }
         if (!done) {
             const unsigned long long r = chunk * REC_CH + fill + __popc(act & lt);
-            rec_cur[r] = cur;
-            rec_sl[r] = ((unsigned long long)sid << 32) | pre;
+            if (kPacked) {
+                rec_sl[r] = ((unsigned long long)cur << sb) | ((unsigned long long)sid << lb) | pre;
+            } else {
+                rec_cur[r] = cur;
+                rec_sl[r] = ((unsigned long long)sid << 32) | pre;
+            }
         }
         fill += cnt;
         if (!done) {
@@ -771,11 +782,11 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_refine(const unsigned 
 // TMA-staged versions (persistent, 2 CTAs per SM): the next 4096-element
 // tile streams into shared memory while the current one is split.
 
-template <int IT>
+template <int IT, bool kPacked>
 __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_partition2(
     const uint32_t* __restrict__ rec_cur, const unsigned long long* __restrict__ rec_sl,
     const uint32_t* __restrict__ IS1, unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ pairs,
-    ListStatus* st, uint32_t cshift, uint32_t cbins) {
+    ListStatus* st, uint32_t cshift, uint32_t cbins, uint32_t sb, uint32_t lb) {
     if (layout_local(st) || st->overflow) return;
     extern __shared__ __align__(128) unsigned char ms_raw[];
     uint32_t* s_cur = reinterpret_cast<uint32_t*>(ms_raw);
@@ -791,9 +802,14 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_partiti
         if (threadIdx.x == 0 && tile < ntiles) {
             const unsigned long long e0 = tile * (MS_THREADS * IT);
             const uint32_t cnt = (uint32_t)min((unsigned long long)(MS_THREADS * IT), total - e0);
-            mbar_expect_tx(&bar, cnt * 12u);
-            bulk_g2s(s_cur, rec_cur + e0, cnt * 4u, &bar);
-            bulk_g2s(s_sl, rec_sl + e0, cnt * 8u, &bar);
+            if (kPacked) {
+                mbar_expect_tx(&bar, cnt * 8u);
+                bulk_g2s(s_sl, rec_sl + e0, cnt * 8u, &bar);
+            } else {
+                mbar_expect_tx(&bar, cnt * 12u);
+                bulk_g2s(s_cur, rec_cur + e0, cnt * 4u, &bar);
+                bulk_g2s(s_sl, rec_sl + e0, cnt * 8u, &bar);
+            }
         }
     };
     auto bin_of = [&](unsigned long long pr) { return (uint32_t)((pr >> 32) >> cshift); };
@@ -810,6 +826,21 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_partiti
 #pragma unroll
         for (int g = 0; g < IT / 4; ++g) {
             const uint32_t e = (g * MS_THREADS + threadIdx.x) * 4;  // 4 records per vector access
+            if (kPacked) {
+                const ulonglong2 r01 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[e >> 1] : make_ulonglong2(~0ull, ~0ull);
+                const ulonglong2 r23 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[(e >> 1) + 1] : make_ulonglong2(~0ull, ~0ull);
+                const unsigned long long rr[4] = {r01.x, r01.y, r23.x, r23.y};
+                const unsigned long long smask = (1ull << (sb - lb)) - 1, lmask = (1ull << lb) - 1;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = g * 4 + q;
+                    const bool nil = rr[q] == ~0ull;
+                    const unsigned long long o = (rr[q] >> lb) & smask;
+                    pr[j] = ((unsigned long long)(nil ? NIL : (uint32_t)(rr[q] >> sb)) << 32) | (uint32_t)(rr[q] & lmask);
+                    bn[j] = __ldg(IS1 + (o < R1 ? o : 0));
+                }
+                continue;
+            }
             const uint4 c4 = e < cnt ? reinterpret_cast<const uint4*>(s_cur)[e >> 2] : make_uint4(NIL, NIL, NIL, NIL);
             const ulonglong2 s01 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[e >> 1] : make_ulonglong2(0, 0);
             const ulonglong2 s23 = e < cnt ? reinterpret_cast<const ulonglong2*>(s_sl)[(e >> 1) + 1] : make_ulonglong2(0, 0);
@@ -1389,6 +1420,8 @@ struct RsPlan {
     int contract = 1;                            // allow the tile contraction for local layouts
     int ms_version = 2;                          // 2: TMA-staged window passes, 1: register tiles
     uint32_t ms_items = 16;                      // window passes: items per thread (tile = 256 x items)
+    bool packed = false;                         // level-0 records packed into one u64
+    uint32_t rec_sb = 0, rec_lb = 0;             // packed record: cur << sb | sid << lb | local
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
     uint32_t salt[SG_MAX_LEVELS] = {};
@@ -1453,6 +1486,20 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
         ++p.levels;
         p.cap[p.levels] = cap;
         N = exp;
+    }
+    if (p.levels > 0 && env_u32("SG_RS_PACKED", 1, 0, 1) && p.ms_version == 2) {
+        // field widths: cur needs ceil(log2 n) bits; sid needs room for cap[1]
+        // ids plus an all-ones pad value that is never an id
+        uint32_t cb = 1, sbits = 1;
+        while (cb < 40 && (1ull << cb) < n) ++cb;
+        while (sbits < 40 && (1ull << sbits) <= p.cap[1]) ++sbits;
+        if (cb <= 32 && cb + sbits + 10 <= 64) {
+            p.packed = true;
+            p.rec_lb = 64 - cb - sbits;
+            p.rec_sb = 64 - cb;
+            const unsigned long long lmax = p.rec_lb >= 32 ? 0xFFFFFFFFull : ((1ull << p.rec_lb) - 1);
+            if (p.walk_cap > lmax) p.walk_cap = (uint32_t)lmax;  // longer chains: Wyllie fallback
+        }
     }
     return p;
 }
@@ -1633,9 +1680,14 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         if (k == 0) {
             // scattered layouts: record walk; local layouts: tile contraction
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
-            k_rs_walk_rec<SuccT><<<walk_grid, WALK_THREADS, 0, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.rec_cur,
-                                                                    b.rec_sl, b.st, p.kbits[0], p.salt[0],
-                                                                    p.walk_cap, p.maxchunks, p.load_mode);
+            if (p.packed)
+                k_rs_walk_rec<SuccT, true><<<walk_grid, WALK_THREADS, 0, s>>>(
+                    succ, b.rgrp, b.spl[0], b.lvl[1], b.rec_cur, b.rec_sl, b.st, p.kbits[0], p.salt[0], p.walk_cap,
+                    p.maxchunks, p.load_mode, p.rec_sb, p.rec_lb);
+            else
+                k_rs_walk_rec<SuccT, false><<<walk_grid, WALK_THREADS, 0, s>>>(
+                    succ, b.rgrp, b.spl[0], b.lvl[1], b.rec_cur, b.rec_sl, b.st, p.kbits[0], p.salt[0], p.walk_cap,
+                    p.maxchunks, p.load_mode, 0, 0);
             rec.end();
             SG_LAUNCH_CHECK();
             const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
@@ -1693,13 +1745,14 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     const size_t sm_part2 = (size_t)tile2 * 12 + MsSmem::bytes(p.cbins, tile2);
     const size_t sm_ref2 = (size_t)tile2 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), tile2);
     if (p.ms_version == 2) {
-        auto kp = it >= 16 ? k_rs_rec_partition2<16> : k_rs_rec_partition2<8>;
+        auto kp = p.packed ? (it >= 16 ? k_rs_rec_partition2<16, true> : k_rs_rec_partition2<8, true>)
+                           : (it >= 16 ? k_rs_rec_partition2<16, false> : k_rs_rec_partition2<8, false>);
         auto kr = it >= 16 ? k_rs_rec_refine2<16> : k_rs_rec_refine2<8>;
         SG_CUDA(set_smem_max(kp, sm_part2));
         SG_CUDA(set_smem_max(kr, sm_ref2));
         rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
         kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift,
-                                                  p.cbins);
+                                                  p.cbins, p.rec_sb, p.rec_lb);
         rec.end();
         SG_LAUNCH_CHECK();
     } else {
