@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
+#include <chrono>
+#include <cstdio>
 #include <map>
 #include <utility>
 #include <vector>
@@ -116,6 +119,24 @@ class Recorder {
     int open_ = -1;
     bool shared_ = false;  // the last end event doubles as the next begin event
     cudaEvent_t t0_ = nullptr;
+};
+
+// SG_HOST_TIMING=1: host-side timestamps of a call's phases on stderr
+struct HostClock {
+    const char* name;
+    bool on;
+    std::chrono::steady_clock::time_point t0, last;
+    explicit HostClock(const char* nm) : name(nm), on(getenv("SG_HOST_TIMING") != nullptr) {
+        if (on) t0 = last = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[sg %s] %-20s +%8.1f us  (total %8.1f us)\n", name, what,
+                std::chrono::duration<double, std::micro>(t - last).count(),
+                std::chrono::duration<double, std::micro>(t - t0).count());
+        last = t;
+    }
 };
 
 // Raise a kernel's dynamic shared memory limit once per device (the attribute

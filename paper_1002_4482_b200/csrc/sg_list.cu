@@ -1867,6 +1867,7 @@ static int wyllie_entry(const void* succ_v, void* rank_v, uint64_t n, int varian
 template <class SuccT, class OutT>
 static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed, void* ws, size_t ws_bytes,
                     cudaStream_t s, sg_stats* stats, sg_violation* viol, const MetaReq* mr) {
+    HostClock hc("rs_entry");
     const RsPlan p = plan_rs(n, seed, (int)sizeof(OutT));
     ms_configure();
     Carver c(ws, ws_bytes);
@@ -1898,12 +1899,18 @@ static int rs_entry(const void* succ_v, void* rank_v, uint64_t n, uint64_t seed,
         if (rc != SG_OK) return rc;
         return classify(h, n, viol);
     }
+    hc.mark("setup");
     int rc = rs_run<SuccT, OutT>((const SuccT*)succ_v, (OutT*)rank_v, n, p, b, s, rec, stats);
     if (rc != SG_OK) return rc;
+    hc.mark("pipeline enqueued");
     rc = enqueue_meta<OutT>(mr, rank_v, n, s);
     if (rc != SG_OK) return rc;
     if (hs) SG_CUDA(cudaMemcpyAsync(hs, b.st, sizeof(ListStatus), cudaMemcpyDeviceToHost, s));
+    hc.mark("meta enqueued");
+    SG_CUDA(cudaStreamSynchronize(s));
+    hc.mark("synchronised");
     SG_CUDA(rec.finish());  // the one synchronisation of a normal call
+    hc.mark("events read");
     if (!hs) {
         rc = read_status(b.st, h, s);
         if (rc != SG_OK) return rc;
