@@ -58,15 +58,23 @@ def workspace(nbytes, device):
 
 
 def exec_stats(st):
-    """native sg_stats -> ExecStats (launch log, barriers, device wall time)."""
+    """native sg_stats -> ExecStats (launch log built lazily, barriers,
+    device wall time)."""
     es = ExecStats(backend="sm_100a")
-    for k in range(min(st.n_launches, _native.SG_MAX_LAUNCHES)):
-        L = st.launch[k]
-        name = _native.kernel_name(L.kernel)
-        c = KernelCounters(launches=1, items=int(L.items), ms=float(L.ms))
-        es.launch_log.append(LaunchRecord(kernel=name, counters=c, round=int(L.round), blocks=int(L.blocks),
-                                          threads=int(L.threads), ms=float(L.ms)))
-    es.barriers = max(0, len(es.launch_log) - 1)
+    nl = min(st.n_launches, _native.SG_MAX_LAUNCHES)
+
+    def build():  # `st` is this call's own sg_stats, kept alive by the closure
+        out = []
+        for k in range(nl):
+            L = st.launch[k]
+            ms = float(L.ms)
+            out.append(LaunchRecord(kernel=_native.kernel_name(L.kernel),
+                                    counters=KernelCounters(launches=1, items=int(L.items), ms=ms),
+                                    round=int(L.round), blocks=int(L.blocks), threads=int(L.threads), ms=ms))
+        return out
+
+    es.set_launch_log_source(build)
+    es.barriers = max(0, nl - 1)
     es.wall_time = float(st.total_ms) / 1e3
     return es
 
