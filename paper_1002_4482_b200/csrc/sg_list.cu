@@ -1211,7 +1211,17 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                 const uint32_t m = (uint32_t)S.brk[l >> 4] >> (l & 15u);
                 const uint32_t r = m ? (uint32_t)(__ffs(m) - 1) : 16u - (l & 15u);
                 if (r) {
-                    for (uint32_t j = 0; j < r; ++j) S.own[sw32(l + j)] = (k << 16) | (off + j);
+                    if (r == 16) {  // a whole block: four 16-B stores (sw32 permutes each group by XOR)
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            const uint32_t gp = sw32(l + 4 * g), xr = gp & 3u;
+                            const uint32_t b0 = (k << 16) | (off + 4 * g);
+                            *reinterpret_cast<uint4*>(&S.own[gp & ~3u]) =
+                                make_uint4(b0 + (0u ^ xr), b0 + (1u ^ xr), b0 + (2u ^ xr), b0 + (3u ^ xr));
+                        }
+                    } else {
+                        for (uint32_t j = 0; j < r; ++j) S.own[sw32(l + j)] = (k << 16) | (off + j);
+                    }
                     l += r;
                     off += r;
                     if (m == 0) {  // l: the next block's first id, a ruler
