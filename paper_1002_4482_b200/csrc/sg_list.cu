@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
 // global queue with one atomic and hands them to its lanes as their chains
 // end.  (One atomic per refill from every warp serialised the walk on the
 // queue head: half of all stall samples sat on that broadcast.)
-constexpr uint32_t QBATCH = 64;
+constexpr uint32_t QBATCH = 64;  // >= 32: one refill must cover a whole warp's request
 
 struct ChainPool {
     unsigned long long base = 0;   // next unclaimed id in the warp's batch (warp-uniform)
