@@ -1460,7 +1460,10 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     RsPlan p;
     // a fine window fills 32 KiB of shared memory in rs5_scatter; coarse
     // windows: few enough bins for one multisplit, >= 64 pairs per bin per tile
-    p.fshift = out_bytes >= 8 ? 12 : 13;
+    // a fine window fills SG_RS_WIN_KB (default 64) KiB of shared memory in rs5_scatter
+    const uint32_t win_kb = env_u32("SG_RS_WIN_KB", 64, 8, 128);
+    p.fshift = 10;
+    while (((size_t)out_bytes << (p.fshift + 1)) <= ((size_t)win_kb << 10)) ++p.fshift;
     uint32_t cs = p.fshift + 1;
     if (cs < 13) cs = 13;  // 2^cshift must be a multiple of MS_TILE
     while (cs < 40 && ((n + (1ull << cs) - 1) >> cs) > 256ull) ++cs;
@@ -1783,6 +1786,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
                                                             p.fshift);
     rec.end();
     SG_LAUNCH_CHECK();
+    SG_CUDA(set_smem_max(k_rs_rec_scatter<OutT>, sizeof(OutT) << p.fshift));
     rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);
     k_rs_rec_scatter<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(
         b.rec_sl, rank, n, p.fshift, b.st, ((uintptr_t)rank & 15) == 0 ? 1 : 0);
