@@ -8,15 +8,19 @@
 //    least doubles per launch, so ceil(log2 n) launches still suffice.
 //    Converged nodes (pointer at the tail) are skipped without a gather.
 //
-//  * Recursive sparse ruling set (reference RS1..RS5: listrank.py:197-408).
-//    Level 0 walks the input list from a hashed ruling set (every ~2^kbits-th
-//    node id, Fibonacci hashing, node 0 always included), writing one packed
-//    {owner:32 | local:32} word per node and one {next ruler, sublist
-//    weight} pair per ruler.  The ruler list is ranked the same way
-//    (weighted) until it fits one CTA, which finishes it with weighted
-//    pointer jumping; expand passes then turn inclusive suffix sums back
-//    into ranks.  Per node the level-0 walk costs one dependent random load
-//    (succ[cur]) and one random 8-byte store; the ruler test is ALU-only.
+//  * Recursive sparse ruling set (reference RS1..RS5: listrank.py:197-408)
+//    for scattered layouts.  Level 0 walks the input list from a hashed
+//    ruling set (every ~2^kbits-th node id, Fibonacci hashing, node 0 always
+//    included): one dependent random load (succ[cur]) per node, and one
+//    {cur, sid, local} record streamed out; one {next ruler, sublist weight}
+//    pair per ruler.  The ruler list is ranked the same way (weighted, in
+//    place) until it fits one CTA, which finishes it with weighted pointer
+//    jumping; expand passes turn inclusive suffix sums back into ranks, and
+//    TMA-staged multisplit passes put the level-0 ranks in node order.
+//
+//  * Tile contraction for local layouts (ordered or locally shuffled lists):
+//    in-tile segments are ranked in shared memory, the segment list is
+//    ranked by the levels above, a streaming pass expands.
 //
 // Validation happens inside the pipeline (no host round trip): range / tail
 // census in the first pass, and "the head's weighted pointer reaches the
@@ -603,9 +607,8 @@ __global__ void __launch_bounds__(WALK_THREADS) k_rs_walk(View src, unsigned lon
 // one atom per hop -- and appends {cur, sid, local} records contiguously per
 // warp (all active lanes of a warp emit one record per step, compacted with a
 // ballot), i.e. as full-line streaming writes.  Each warp owns 1024-record
-// chunks and keeps a per-chunk histogram of the records' output windows for
-// the partition pass.  The node-order scatter of the ranks then happens window
-// by window inside L2 (rs5_partition / rs5_scatter).
+// chunks.  The node-order materialisation of the ranks follows in the window
+// passes (rs5_partition / rs5_refine / rs5_scatter).
 
 constexpr int REC_CH = 1024;
 
@@ -714,70 +717,6 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
 // Both bucketing passes are ballot multisplits (sg_msplit.cuh).  Invalid
 // inputs can overfill a window; such writes are dropped (the call reports
 // the list invalid anyway).
-__device__ __forceinline__ int ceil_log2(uint32_t x) {
-    int b = 0;
-    while ((1u << b) < x) ++b;
-    return b;
-}
-
-__global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_partition(const uint32_t* __restrict__ rec_cur,
-                                                                 const unsigned long long* __restrict__ rec_sl,
-                                                                 const uint32_t* __restrict__ IS1,
-                                                                 unsigned long long* __restrict__ cursor,
-                                                                 unsigned long long* __restrict__ pairs,
-                                                                 ListStatus* st, uint32_t cshift, uint32_t cbins) {
-    if (layout_local(st) || st->overflow) return;
-    extern __shared__ __align__(16) unsigned char ms_raw[];
-    MsSmem sm = MsSmem::carve(ms_raw, cbins);
-    const unsigned long long total = st->chunks * REC_CH;
-    const unsigned long long R1 = st->R[1];
-    auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b) -> bool {
-        const uint32_t c = __ldcs(rec_cur + e);
-        const unsigned long long sl = __ldcs(rec_sl + e);
-        if (c == NIL) return false;
-        b = c >> cshift;
-        const unsigned long long o = sl >> 32;  // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
-        const uint32_t rk = o < R1 ? __ldg(IS1 + o) - (uint32_t)sl - 1u : 0u;
-        pr = ((unsigned long long)c << 32) | rk;
-        return true;
-    };
-    auto bin_of = [&](unsigned long long pr) { return (uint32_t)((pr >> 32) >> cshift); };
-    auto slot = [&](uint32_t b) { return make_ulonglong2((unsigned long long)b << cshift, 1ull << cshift); };
-    bool over = false;
-    const int nbits = ceil_log2(cbins);
-    for (unsigned long long e0 = (unsigned long long)blockIdx.x * MS_TILE; e0 < total;
-         e0 += (unsigned long long)gridDim.x * MS_TILE)
-        over |= ms_tile(get, bin_of, slot, e0, min(e0 + MS_TILE, total), cbins, nbits, cursor, pairs, sm);
-    if (over) st->bad = 1;
-}
-
-__global__ void __launch_bounds__(MS_THREADS, 4) k_rs_rec_refine(const unsigned long long* __restrict__ in,
-                                                              unsigned long long* __restrict__ cursor,
-                                                              unsigned long long* __restrict__ out, ListStatus* st,
-                                                              unsigned long long n, uint32_t cshift, uint32_t fshift) {
-    if (layout_local(st) || st->overflow) return;
-    const uint32_t fb = 1u << (cshift - fshift);
-    extern __shared__ __align__(16) unsigned char ms_raw[];
-    MsSmem sm = MsSmem::carve(ms_raw, fb);
-    bool over = false;
-    // tiles never straddle a coarse window (2^cshift is a multiple of MS_TILE)
-    for (unsigned long long e0 = (unsigned long long)blockIdx.x * MS_TILE; e0 < n;
-         e0 += (unsigned long long)gridDim.x * MS_TILE) {
-        const unsigned long long c = e0 >> cshift;
-        auto get = [&](unsigned long long e, unsigned long long& pr, uint32_t& b) -> bool {
-            pr = __ldcs(in + e);
-            const unsigned long long cur = pr >> 32;
-            if ((cur >> cshift) != c) return false;  // only for invalid inputs
-            b = (uint32_t)((cur >> fshift) & (fb - 1));
-            return true;
-        };
-        auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
-        auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
-        over |= ms_tile(get, bin_of, slot, e0, min(e0 + MS_TILE, n), fb, (int)(cshift - fshift), cursor + c * fb,
-                        out, sm);
-    }
-    if (over) st->bad = 1;
-}
 
 // TMA-staged versions (persistent, 2 CTAs per SM): the next 4096-element
 // tile streams into shared memory while the current one is split.
@@ -1428,8 +1367,6 @@ struct RsPlan {
     uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
     bool rec_ok = true;                          // fine windows fit shared memory
     int contract = 1;                            // allow the tile contraction for local layouts
-    int ms_version = 2;                          // 2: TMA-staged window passes, 1: register tiles
-    uint32_t ms_items = 16;                      // window passes: items per thread (tile = 256 x items)
     bool packed = false;                         // level-0 records packed into one u64
     uint32_t rec_sb = 0, rec_lb = 0;             // packed record: cur << sb | sid << lb | local
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
@@ -1485,8 +1422,6 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
     p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
-    p.ms_version = (int)env_u32("SG_RS_MS", 2, 1, 2);
-    p.ms_items = env_u32("SG_MS_ITEMS", 16, 8, 16) >= 16 ? 16 : 8;
     p.cap[0] = n;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
@@ -1500,7 +1435,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
         p.cap[p.levels] = cap;
         N = exp;
     }
-    if (p.levels > 0 && env_u32("SG_RS_PACKED", 1, 0, 1) && p.ms_version == 2) {
+    if (p.levels > 0 && env_u32("SG_RS_PACKED", 1, 0, 1)) {
         // field widths: cur needs ceil(log2 n) bits; sid needs room for cap[1]
         // ids plus an all-ones pad value that is never an id
         uint32_t cb = 1, sbits = 1;
@@ -1750,40 +1685,21 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     // scattered layouts: rank the records, bucket them by window, scatter
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
-    const uint32_t persist = kSMs * 4;
-    const uint32_t it = p.ms_items;
-    const uint32_t tile2 = MS_THREADS * it;
-    const uint32_t persist2 = kSMs * (it >= 16 ? 2 : 3);
-    const size_t sm_part = MsSmem::bytes(p.cbins), sm_ref = MsSmem::bytes(1u << (p.cshift - p.fshift));
+    constexpr uint32_t tile2 = MS_THREADS * MS2_ITEMS;
+    const uint32_t persist2 = kSMs * 2;
     const size_t sm_part2 = (size_t)tile2 * 12 + MsSmem::bytes(p.cbins, tile2);
     const size_t sm_ref2 = (size_t)tile2 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), tile2);
-    if (p.ms_version == 2) {
-        auto kp = p.packed ? (it >= 16 ? k_rs_rec_partition2<16, true> : k_rs_rec_partition2<8, true>)
-                           : (it >= 16 ? k_rs_rec_partition2<16, false> : k_rs_rec_partition2<8, false>);
-        auto kr = it >= 16 ? k_rs_rec_refine2<16> : k_rs_rec_refine2<8>;
-        SG_CUDA(set_smem_max(kp, sm_part2));
-        SG_CUDA(set_smem_max(kr, sm_ref2));
-        rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
-        kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift,
-                                                  p.cbins, p.rec_sb, p.rec_lb);
-        rec.end();
-        SG_LAUNCH_CHECK();
-    } else {
-        SG_CUDA(set_smem_max(k_rs_rec_partition, sm_part));
-        SG_CUDA(set_smem_max(k_rs_rec_refine, sm_ref));
-        rec.begin(K_RS5_PARTITION, 0, persist, MS_THREADS, n);
-        k_rs_rec_partition<<<persist, MS_THREADS, sm_part, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st,
-                                                                p.cshift, p.cbins);
-        rec.end();
-        SG_LAUNCH_CHECK();
-    }
-    rec.begin(K_RS5_REFINE, 0, p.ms_version == 2 ? persist2 : persist, MS_THREADS, n);
-    if (p.ms_version == 2)
-        (it >= 16 ? k_rs_rec_refine2<16> : k_rs_rec_refine2<8>)<<<persist2, MS_THREADS, sm_ref2, s>>>(
-            b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
-    else
-        k_rs_rec_refine<<<persist, MS_THREADS, sm_ref, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
-                                                            p.fshift);
+    auto kp = p.packed ? k_rs_rec_partition2<MS2_ITEMS, true> : k_rs_rec_partition2<MS2_ITEMS, false>;
+    auto kr = k_rs_rec_refine2<MS2_ITEMS>;
+    SG_CUDA(set_smem_max(kp, sm_part2));
+    SG_CUDA(set_smem_max(kr, sm_ref2));
+    rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
+    kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift, p.cbins,
+                                              p.rec_sb, p.rec_lb);
+    rec.end();
+    SG_LAUNCH_CHECK();
+    rec.begin(K_RS5_REFINE, 0, persist2, MS_THREADS, n);
+    kr<<<persist2, MS_THREADS, sm_ref2, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
     rec.end();
     SG_LAUNCH_CHECK();
     SG_CUDA(set_smem_max(k_rs_rec_scatter<OutT>, sizeof(OutT) << p.fshift));
