@@ -24,6 +24,7 @@ validated exactly like ``vkm.Machine`` (vkm.py:434-454) and recorded in
 import ctypes
 import functools
 import math
+import threading
 from collections import namedtuple
 from dataclasses import dataclass
 
@@ -239,15 +240,16 @@ def _draw_splitters_cached(n, r, seed):
 
 
 _IDX_CACHE = {}
-_PINNED = {}
+_PINNED = threading.local()
 
 
 def _pinned_meta(count):
-    """Reused pinned host staging for the splitter meta (copied out per call)."""
-    buf = _PINNED.get("meta")
+    """Reused pinned host staging for the splitter meta, one per host thread
+    (the contents are copied out before the call returns)."""
+    buf = getattr(_PINNED, "meta", None)
     if buf is None or buf.numel() < count:
         buf = torch.empty(max(count, 3 * 16384), dtype=torch.int64, pin_memory=True)
-        _PINNED["meta"] = buf
+        _PINNED.meta = buf
     return buf
 
 
