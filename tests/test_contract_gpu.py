@@ -121,6 +121,11 @@ def test_contraction_invalid_lists(cuda):
     s = ordered(n)
     s[0], s[3] = 4, 1
     _expect_invalid(s)
+    # a tile that is one run except that its last id links back into it
+    # (not a single-run tile: the fast path must not take it)
+    s = ordered(n)
+    s[2 * TILE - 1] = TILE + 5
+    _expect_invalid(s)
     # in-tile cycle through rulers, reached from the head: ... 40 -> 17
     s = ordered(n)
     s[40] = 17
