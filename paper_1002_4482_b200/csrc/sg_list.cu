@@ -1073,6 +1073,51 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
                     v[j * 4 + c] = l < tn ? succ[base + l] : SuccT(0);
                 }
         }
+        // Single-run tile (every id's successor is the next id, the last one
+        // leaves the tile or is the tail), decided from the registers: one
+        // segment, distance to its end = tn - 1 - l, written in closed form
+        // without the shared-memory ranking.
+        {
+            bool run = true;
+            const uint32_t last = tn - 1;
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) {
+                    const uint32_t l = (j * TILE_THREADS + t) * VEC + c;
+                    const unsigned long long x = as_index<SuccT>(v[j * 4 + c]);
+                    if (l < last)
+                        run &= x == base + l + 1;
+                    else if (l == last)
+                        run &= (x - base >= tn) || x == base + l;
+                }
+            if (__syncthreads_and(run)) {
+                const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
+                                                        : (uint32_t)(R1 - tile_off[tile]);
+                if (segs != 1u) bad = true;
+                if (t == 0 && segs == 1u) {
+                    const unsigned long long sid = tile_off[tile];
+                    seg_head[sid] = (uint32_t)base;
+                    headsid[base] = (uint32_t)sid;
+                    lvl1[sid] = make_uint2(0u, tn);
+                    const unsigned long long x = as_index<SuccT>(succ[base + last]);
+                    seg_succ[sid] = (x >= N || x == base + last) ? NIL : (uint32_t)x;
+                }
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
+                    if (full) {
+                        *reinterpret_cast<uint4*>(node_word + base + l0) =
+                            make_uint4(last - l0, last - l0 - 1, last - l0 - 2, last - l0 - 3);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < VEC; ++c)
+                            if (l0 + c < tn) node_word[base + l0 + c] = last - (l0 + c);
+                    }
+                }
+                continue;  // no shared memory was touched
+            }
+        }
         reinterpret_cast<uint4*>(S.pred)[t] = make_uint4(0u, 0u, 0u, 0u);  // 4096 flags
         __syncthreads();
         uint32_t links = 0;
@@ -1105,41 +1150,6 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
         }
         __syncthreads();
         if (tile == 0 && S.pred[0]) bad = true;  // node 0 must start the list
-        // Single-run tile (every id's successor is the next id, the last one
-        // leaves the tile or is the tail): one segment, distance to its end
-        // = tn - 1 - l, no walk or jumping needed.  Block t's break mask must
-        // be exactly the ids >= tn - 1, and id tn - 1 must leave the tile.
-        {
-            const uint32_t lo = t * 16u, last = tn - 1;
-            const uint32_t want = last <= lo ? 0xFFFFu : (last < lo + 16u ? (0xFFFFu << (last - lo)) & 0xFFFFu : 0u);
-            if (__syncthreads_and(S.brk[t] == want && S.nx[sw16(last)] == CT_END)) {
-                const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
-                                                        : (uint32_t)(R1 - tile_off[tile]);
-                if (segs != 1u) bad = true;
-                if (t == 0 && segs == 1u) {
-                    const unsigned long long sid = tile_off[tile];
-                    seg_head[sid] = (uint32_t)base;
-                    headsid[base] = (uint32_t)sid;
-                    lvl1[sid] = make_uint2(0u, tn);
-                    const unsigned long long x = as_index<SuccT>(succ[base + last]);
-                    seg_succ[sid] = (x >= N || x == base + last) ? NIL : (uint32_t)x;
-                }
-#pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                    const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
-                    if (full) {
-                        *reinterpret_cast<uint4*>(node_word + base + l0) =
-                            make_uint4(last - l0, last - l0 - 1, last - l0 - 2, last - l0 - 3);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < VEC; ++c)
-                            if (l0 + c < tn) node_word[base + l0 + c] = last - (l0 + c);
-                    }
-                }
-                __syncthreads();  // shared memory is reused by the next tile
-                continue;
-            }
-        }
         // 2. local rulers (blocked: thread t owns nodes 16t .. 16t+15): heads
         //    and every CT_STRIDE-th node; numbered in index order
         uint32_t rflags = 0, hflags = 0;
