@@ -173,7 +173,10 @@ def test_full_size_properties_2_26(cuda):
     labels, stats = g.sv_components(e32, p=1024)
     _check_label_properties(e32.edges, labels, n)
     # minimality: every vertex labelled r lies in r's component and r is its smallest member
-    assert stats.meta["roots_per_round"][-1] == int((labels == torch.arange(n, device=cuda, dtype=labels.dtype)).sum())
+    roots = int((labels == torch.arange(n, device=cuda, dtype=labels.dtype)).sum())
+    assert stats.meta["roots_per_round"][-1] == roots
+    # the reference's own count for C5 (seq_components on gen_random_graph(2^26, .., seed=0))
+    assert e32.m == m and roots == 22_599
     sv, _ = g.sv_components(e32, p=1024, variant="sv")
     assert torch.equal(sv, labels)
 
@@ -283,3 +286,16 @@ def test_sparse_merge_building_blocks(cuda):
                            _device.stream_ptr(cuda))
     assert rc == 0
     assert np.array_equal(D.cpu().numpy(), np.minimum(a, b))
+
+
+def test_c4_matches_reference_counts(cuda):
+    """C4 (BASELINE configs[3]): gen_random_graph(2^22, m = 2^24, seed 0) has
+    1 437 components, the largest with 4 192 867 vertices (the reference's
+    seq_components)."""
+    n, m = 1 << 22, 1 << 24
+    gr = g.gen_random_graph(n, m / (n * (n - 1) // 2), seed=0, device=cuda)
+    assert gr.m == m
+    labels, _ = g.sv_components(gr, p=1024)
+    counts = torch.bincount(labels.to(torch.int64), minlength=n)
+    assert int((counts > 0).sum()) == 1_437
+    assert int(counts.max()) == 4_192_867

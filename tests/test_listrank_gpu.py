@@ -349,6 +349,18 @@ def _check_rank_properties(succ, rank):
 
 
 @pytest.mark.parametrize("kind", ["random", "ordered"])
+def test_full_size_properties_2_28(cuda, kind):
+    """BASELINE configs[2]: 2^28 nodes, random and ordered layouts."""
+    n = 1 << 28
+    sl = g.gen_list(n, seed=0, device=cuda, dtype=torch.int32) if kind == "random" else \
+        g.ordered_list(n, device=cuda, dtype=torch.int32)
+    rank, stats = g.rs_rank(sl, 16384)
+    assert stats.meta["path"] == ("ruling_set" if kind == "random" else "contract")
+    _check_rank_properties(sl.succ, rank)
+    assert stats.meta["fallback"] is False
+
+
+@pytest.mark.parametrize("kind", ["random", "ordered"])
 def test_full_size_properties_2_26(cuda, kind):
     n = 1 << 26
     sl = g.gen_list(n, seed=0, device=cuda, dtype=torch.int32) if kind == "random" else \
