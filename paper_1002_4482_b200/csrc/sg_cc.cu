@@ -627,6 +627,14 @@ static int read_flags(const unsigned long long* dev, CcHostFlags& h, cudaStream_
     return SG_OK;
 }
 
+// pinned host copy of the flags, enqueued behind the last kernel so a call
+// synchronises once
+static CcHostFlags* pinned_flags() {
+    static thread_local CcHostFlags* p = nullptr;
+    if (!p && cudaMallocHost(&p, sizeof(CcHostFlags)) != cudaSuccess) p = nullptr;
+    return p;
+}
+
 static int graph_violation(const CcHostFlags& h, sg_violation* v) {
     if (h.f[1]) {
         if (v) {
@@ -730,10 +738,15 @@ int sg_cc(const void* edges, int edge_dtype, uint64_t m, uint64_t n, void* label
         rc = compress_dispatch(D, 0, n, roots, labels, label_dtype, s);
         rec.end();
         if (rc != SG_OK) return rc;
-        SG_CUDA(rec.finish());
-        CcHostFlags h;
-        rc = read_flags(flags, h, s);
-        if (rc != SG_OK) return rc;
+        CcHostFlags* hp = pinned_flags();
+        CcHostFlags hloc;
+        if (hp) SG_CUDA(cudaMemcpyAsync(hp, flags, sizeof(CcHostFlags), cudaMemcpyDeviceToHost, s));
+        SG_CUDA(rec.finish());  // the one synchronisation of a UF call
+        if (!hp) {
+            rc = read_flags(flags, hloc, s);
+            if (rc != SG_OK) return rc;
+        }
+        const CcHostFlags& h = hp ? *hp : hloc;
         rc = graph_violation(h, viol);
         if (rc != SG_OK) return rc;
         if (st) {
