@@ -707,6 +707,158 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
     close_chunk();
 }
 
+// Level-0 walk that bins its records by coarse output window on the fly
+// (packed records only), so the rs5_partition pass disappears.  The walk is
+// bound by the dependent random load; the binning runs in its shadow.  Each
+// CTA keeps WB_SLOTS records per coarse window in shared memory:
+//   reserve  res[b]++ (a lane that finds the buffer full retries next round),
+//   store    the record into the reserved slot, then commit com[b]++;
+//   flush    the lane whose commit completes the buffer hands it to its warp,
+//            which claims WB_SLOTS slots of window b's region with one global
+//            atomic and writes them as one 128-B line, then reopens the buffer
+//            (com = 0 before res = 0: a reserver that sees res reopened also
+//            sees com reset).
+// A valid list puts exactly 2^cshift records into each full window, so the
+// regions are known in advance; an invalid list can overfill one -- those
+// records are dropped and the call is flagged (it reports the list invalid).
+constexpr uint32_t WB_MAXBINS = 256;
+
+template <class SuccT, int WB_THREADS, int WB_CTAS_PER_SM, uint32_t WB_SLOTS>
+__global__ void __launch_bounds__(WB_THREADS, WB_CTAS_PER_SM) k_rs_walk_bin(
+    const SuccT* __restrict__ succ, const uint2* __restrict__ rgrp, const uint32_t* __restrict__ spl,
+    uint2* __restrict__ up, unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ out,
+    ListStatus* st, uint32_t kbits, uint32_t salt, uint32_t cap_hops, int load_mode, uint32_t sb, uint32_t lb,
+    uint32_t cshift, uint32_t cbins) {
+    if (layout_local(st)) return;  // k_rs_contract takes this list
+    extern __shared__ __align__(16) unsigned long long buf[];  // [cbins][WB_SLOTS]
+    __shared__ uint32_t res[WB_MAXBINS], com[WB_MAXBINS];
+    for (uint32_t i = threadIdx.x; i < cbins; i += blockDim.x) res[i] = com[i] = 0;
+    __syncthreads();
+    const unsigned long long N = st->R[0];
+    const unsigned long long R = st->R[1];
+    const unsigned long long wsize = 1ull << cshift;
+    unsigned long long* q = &st->qhead[0];
+    const uint32_t lane = lane_id();
+    bool over = false;
+    // warp-cooperative copy of `cnt` records of bin b into its window, claimed at `base`
+    auto store_run = [&](uint32_t b, uint32_t cnt, unsigned long long base, uint32_t k) {
+        if (k < cnt) {
+            const unsigned long long v = buf[b * WB_SLOTS + k];
+            if (base + k < wsize)
+                __stcs(out + ((unsigned long long)b << cshift) + base + k, v);
+            else
+                over = true;
+        }
+    };
+    uint32_t sid = NIL, cur = 0, pre = 0;
+    bool done = false;
+    ChainPool pool;
+    for (;;) {
+        const bool need = !done && sid == NIL;
+        const unsigned long long s = pool.take(need, q, R, lane);
+        if (need) {
+            if (s != ~0ull) {
+                sid = (uint32_t)s;
+                cur = spl[s];
+                pre = 0;
+            } else {
+                done = true;
+            }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        unsigned long long nxl = 0;
+        if (!done) nxl = as_index<SuccT>(ld_mode(succ + cur, load_mode));
+        // place this step's record while the load is in flight
+        bool pend = !done;
+        const uint32_t b = cur >> cshift;
+        const unsigned long long recv = ((unsigned long long)cur << sb) | ((unsigned long long)sid << lb) | pre;
+        while (__any_sync(0xffffffffu, pend)) {
+            bool last = false;
+            if (pend) {
+                const uint32_t pos = atomicAdd(&res[b], 1u);
+                if (pos < WB_SLOTS) {
+                    buf[b * WB_SLOTS + pos] = recv;
+                    __threadfence_block();
+                    last = atomicAdd(&com[b], 1u) == WB_SLOTS - 1;
+                    pend = false;
+                }
+            }
+            unsigned m = __ballot_sync(0xffffffffu, last);
+            if (m == 0) continue;
+            __threadfence_block();
+            // all full buffers of this warp: claim their lines together, then copy two per pass
+            unsigned long long base = 0;
+            if (last) base = atomicAdd(&cursor[b], (unsigned long long)WB_SLOTS);
+            if (WB_SLOTS == 16) {
+                while (m) {
+                    const int s0 = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int s1 = m ? __ffs(m) - 1 : s0;
+                    if (m) m &= m - 1;
+                    const int src = lane < 16 ? s0 : s1;
+                    const uint32_t fb = __shfl_sync(0xffffffffu, b, src);
+                    const unsigned long long fbase = __shfl_sync(0xffffffffu, base, src);
+                    if (lane < 16 || s1 != s0) store_run(fb, WB_SLOTS, fbase, lane & 15u);
+                    __syncwarp();
+                    if ((lane & 15u) == 0 && (lane < 16 || s1 != s0)) {
+                        atomicExch(&com[fb], 0u);
+                        __threadfence_block();
+                        atomicExch(&res[fb], 0u);
+                    }
+                    __syncwarp();
+                }
+            } else {
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t fb = __shfl_sync(0xffffffffu, b, src);
+                    const unsigned long long fbase = __shfl_sync(0xffffffffu, base, src);
+                    for (uint32_t k = lane; k < WB_SLOTS; k += 32) store_run(fb, WB_SLOTS, fbase, k);
+                    __syncwarp();
+                    if (lane == 0) {
+                        atomicExch(&com[fb], 0u);
+                        __threadfence_block();
+                        atomicExch(&res[fb], 0u);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (!done) {
+            ++pre;
+            bool end = true;
+            uint2 upv = make_uint2(sid, pre);
+            if (nxl == cur) {  // the tail
+            } else if (nxl >= N) {  // out-of-range successor (invalid input)
+                st->bad = 1;
+            } else if (is_ruler((uint32_t)nxl, kbits, salt)) {
+                upv.x = ruler_id(rgrp, (uint32_t)nxl);
+            } else if (pre >= cap_hops) {
+                st->overflow = 1;
+            } else {
+                end = false;
+                cur = (uint32_t)nxl;
+            }
+            if (end) {
+                up[sid] = upv;
+                sid = NIL;
+            }
+        }
+    }
+    // drain the partial buffers: one warp per bin
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5;
+    for (uint32_t bb = warp; bb < cbins; bb += WB_THREADS / 32) {
+        const uint32_t cnt = com[bb];
+        if (cnt == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&cursor[bb], (unsigned long long)cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (uint32_t k = lane; k < cnt; k += 32) store_run(bb, cnt, base, k);
+    }
+    if (__any_sync(0xffffffffu, over) && lane == 0) st->bad = 1;
+}
+
 // Node-order materialisation of the ranks in three streaming passes.  For a
 // valid list every node appears in exactly one record, so every output window
 // receives exactly its own node count: window w of 2^shift nodes owns the
@@ -809,10 +961,16 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_partiti
     if (over) st->bad = 1;
 }
 
-template <int IT>
+// kMode 0: {cur, rank} pairs in and out.  kMode 1: packed walk records
+// binned by k_rs_walk_bin in, ranked here (rank = IS_1[sid] - local - 1,
+// listrank.py:375-379), pairs out.  (Ranking them in rs5_scatter instead
+// measured slower: the IS_1 gather costs the same ~0.8 ms at 2^28 wherever it
+// runs -- it is bound by L2 sector reads -- and rs5_scatter has less to hide it behind.)
+template <int IT, int kMode, int NB = 8>  // NB: bits of the fine bin (>= cshift - fshift)
 __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
-    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift) {
+    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
+    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
     if (layout_local(st) || st->overflow) return;
     const uint32_t fb = 1u << (cshift - fshift);
     extern __shared__ __align__(128) unsigned char ms_raw[];
@@ -821,6 +979,8 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
     __shared__ unsigned long long bar;
     // tiles never straddle a coarse window (2^cshift is a multiple of (MS_THREADS * IT))
     const unsigned long long ntiles = (n + (MS_THREADS * IT) - 1) / (MS_THREADS * IT);
+    const unsigned long long R1 = st->R[1];
+    const unsigned long long pol_last = l2_evict_last();
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     auto issue = [&](unsigned long long tile) {
@@ -829,7 +989,7 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
             const uint32_t cnt = (uint32_t)min((unsigned long long)(MS_THREADS * IT), n - e0);
             const uint32_t bytes = (cnt * 8u + 15u) & ~15u;  // the buffer is padded to whole windows
             mbar_expect_tx(&bar, bytes);
-            bulk_g2s(s_in, in + e0, bytes, &bar);
+            bulk_g2s_hint(s_in, in + e0, bytes, &bar, l2_evict_first());
         }
     };
     bool over = false;
@@ -852,16 +1012,31 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
             for (int q = 0; q < 2; ++q) {
                 const int j = g * 2 + q;
                 pr[j] = vv[q];
+                if (kMode == 1) {  // gathers first, all in flight together; IS_1 stays in L2
+                    const unsigned long long o = (vv[q] >> lb) & ((1ull << (sb - lb)) - 1);
+                    bn[j] = ld_hint(IS1 + (o < R1 ? o : 0), pol_last);
+                    continue;
+                }
                 const unsigned long long cur = pr[j] >> 32;
                 bn[j] = (e + q < cnt && (cur >> cshift) == c) ? (uint32_t)((cur >> fshift) & (fb - 1))
                                                              : (uint32_t)MS_MAXB;
+            }
+        }
+        if (kMode == 1) {
+#pragma unroll
+            for (int j = 0; j < IT; ++j) {
+                const uint32_t e = ((j >> 1) * MS_THREADS + threadIdx.x) * 2 + (j & 1);
+                const unsigned long long cur = pr[j] >> sb;
+                const uint32_t local = (uint32_t)(pr[j] & ((1ull << lb) - 1));
+                pr[j] = (cur << 32) | (bn[j] - local - 1u);
+                bn[j] = (e < cnt && (cur >> cshift) == c) ? (uint32_t)((cur >> fshift) & (fb - 1)) : (uint32_t)MS_MAXB;
             }
         }
         __syncthreads();
         issue(tile + gridDim.x);
         auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
         auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
-        over |= ms_split<IT, 8>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
+        over |= ms_split<IT, NB>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
     }
     if (over) st->bad = 1;
 }
@@ -1413,6 +1588,7 @@ struct RsPlan {
     bool rec_ok = true;                          // fine windows fit shared memory
     int contract = 1;                            // allow the tile contraction for local layouts
     bool packed = false;                         // level-0 records packed into one u64
+    bool fused = false;                          // packed records binned by the walk (no rs5_partition)
     uint32_t rec_sb = 0, rec_lb = 0;             // packed record: cur << sb | sid << lb | local
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
@@ -1492,6 +1668,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
             p.rec_sb = 64 - cb;
             const unsigned long long lmax = p.rec_lb >= 32 ? 0xFFFFFFFFull : ((1ull << p.rec_lb) - 1);
             if (p.walk_cap > lmax) p.walk_cap = (uint32_t)lmax;  // longer chains: Wyllie fallback
+            p.fused = p.cbins <= WB_MAXBINS && env_u32("SG_RS_FUSED", 1, 0, 1) != 0;
         }
     }
     return p;
@@ -1521,10 +1698,10 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     b.st = c.take<ListStatus>(1);
     b.word0 = c.take<unsigned long long>(n);
     if (p.levels > 0) {
-        const unsigned long long nrec = p.maxchunks * REC_CH;
+        const unsigned long long nrec = p.fused ? 0 : p.maxchunks * REC_CH;
         b.rid = c.take<uint32_t>(n);
         b.rgrp = c.take<uint2>(n / 32 + 2);
-        b.rec_cur = c.take<uint32_t>(nrec);
+        b.rec_cur = c.take<uint32_t>(p.packed ? 0 : nrec);
         const unsigned long long npad = (unsigned long long)p.cbins << p.cshift;
         b.rec_sl = c.take<unsigned long long>(nrec > npad ? nrec : npad);  // reused by rs5_refine
         b.pairs = c.take<unsigned long long>((unsigned long long)p.cbins << p.cshift);
@@ -1672,6 +1849,24 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         SG_LAUNCH_CHECK();
         if (k == 0) {
             // scattered layouts: record walk; local layouts: tile contraction
+            if (p.fused) {
+                SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
+                static const int cfg = (int)env_u32("SG_WB_CFG", 0, 0, 1);
+                auto launch = [&](auto kern, int threads, int ctas, size_t smem) -> cudaError_t {
+                    const cudaError_t e = set_smem_max(kern, smem);
+                    if (e != cudaSuccess) return e;
+                    rec.begin(K_RS3_WALK, 0, kSMs * ctas, threads, capN);
+                    kern<<<kSMs * ctas, threads, smem, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.cursor, b.pairs, b.st,
+                                                         p.kbits[0], p.salt[0], p.walk_cap, p.load_mode, p.rec_sb,
+                                                         p.rec_lb, p.cshift, p.cbins);
+                    return cudaSuccess;
+                };
+                const size_t nb = (size_t)p.cbins * sizeof(unsigned long long);
+                if (cfg == 1)
+                    SG_CUDA(launch(k_rs_walk_bin<SuccT, 512, 4, 16>, 512, 4, nb * 16));
+                else
+                    SG_CUDA(launch(k_rs_walk_bin<SuccT, 1024, 2, 32>, 1024, 2, nb * 32));
+            } else {
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
             if (p.packed)
                 k_rs_walk_rec<SuccT, true><<<walk_grid, WALK_THREADS, 0, s>>>(
@@ -1681,6 +1876,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
                 k_rs_walk_rec<SuccT, false><<<walk_grid, WALK_THREADS, 0, s>>>(
                     succ, b.rgrp, b.spl[0], b.lvl[1], b.rec_cur, b.rec_sl, b.st, p.kbits[0], p.salt[0], p.walk_cap,
                     p.maxchunks, p.load_mode, 0, 0);
+            }
             rec.end();
             SG_LAUNCH_CHECK();
             const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
@@ -1729,22 +1925,38 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         SG_LAUNCH_CHECK();
     }
     // scattered layouts: rank the records, bucket them by window, scatter
-    SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
     constexpr uint32_t tile2 = MS_THREADS * MS2_ITEMS;
     const uint32_t persist2 = kSMs * 2;
-    const size_t sm_part2 = (size_t)tile2 * 12 + MsSmem::bytes(p.cbins, tile2);
     const size_t sm_ref2 = (size_t)tile2 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), tile2);
-    auto kp = p.packed ? k_rs_rec_partition2<MS2_ITEMS, true> : k_rs_rec_partition2<MS2_ITEMS, false>;
-    auto kr = k_rs_rec_refine2<MS2_ITEMS>;
-    SG_CUDA(set_smem_max(kp, sm_part2));
-    SG_CUDA(set_smem_max(kr, sm_ref2));
-    rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
-    kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift, p.cbins,
-                                              p.rec_sb, p.rec_lb);
-    rec.end();
-    SG_LAUNCH_CHECK();
-    rec.begin(K_RS5_REFINE, 0, persist2, MS_THREADS, n);
-    kr<<<persist2, MS_THREADS, sm_ref2, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift);
+    if (!p.fused) {
+        SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
+        const size_t sm_part2 = (size_t)tile2 * 12 + MsSmem::bytes(p.cbins, tile2);
+        auto kp = p.packed ? k_rs_rec_partition2<MS2_ITEMS, true> : k_rs_rec_partition2<MS2_ITEMS, false>;
+        SG_CUDA(set_smem_max(kp, sm_part2));
+        rec.begin(K_RS5_PARTITION, 0, persist2, MS_THREADS, n);
+        kp<<<persist2, MS_THREADS, sm_part2, s>>>(b.rec_cur, b.rec_sl, b.IS[1], b.cursor, b.pairs, b.st, p.cshift,
+                                                  p.cbins, p.rec_sb, p.rec_lb);
+        rec.end();
+        SG_LAUNCH_CHECK();
+    }
+    static const int rit = (int)env_u32("SG_REF_IT", 8, 8, 16);
+    if (p.fused && rit == 8) {
+        constexpr uint32_t t8 = MS_THREADS * 8;
+        const size_t sm8 = (size_t)t8 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), t8);
+        const uint32_t fbits = p.cshift - p.fshift;  // ballots per element in the split
+        auto kr = fbits <= 4 ? k_rs_rec_refine2<8, 1, 4>
+                             : (fbits <= 6 ? k_rs_rec_refine2<8, 1, 6> : k_rs_rec_refine2<8, 1, 8>);
+        SG_CUDA(set_smem_max(kr, sm8));
+        rec.begin(K_RS5_REFINE, 0, kSMs * 3, MS_THREADS, n);
+        kr<<<kSMs * 3, MS_THREADS, sm8, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
+                                             b.IS[1], p.rec_sb, p.rec_lb);
+    } else {
+        auto kr = p.fused ? k_rs_rec_refine2<MS2_ITEMS, 1> : k_rs_rec_refine2<MS2_ITEMS, 0>;
+        SG_CUDA(set_smem_max(kr, sm_ref2));
+        rec.begin(K_RS5_REFINE, 0, persist2, MS_THREADS, n);
+        kr<<<persist2, MS_THREADS, sm_ref2, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
+                                                 b.IS[1], p.rec_sb, p.rec_lb);
+    }
     rec.end();
     SG_LAUNCH_CHECK();
     SG_CUDA(set_smem_max(k_rs_rec_scatter<OutT>, sizeof(OutT) << p.fshift));

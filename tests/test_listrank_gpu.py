@@ -379,3 +379,36 @@ def test_walk_cap_fallback(cuda, orc, monkeypatch):
     rank, stats = g.rs_rank(sl, 32)
     assert stats.meta["fallback"] is True
     assert np.array_equal(rank, orc.seq_rank(sl.succ))
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("n", [5_000, 300_001, 3_000_017])
+def test_record_paths_match_oracle(cuda, orc, monkeypatch, fused, n):
+    """Both level-0 record pipelines: the walk that bins its records by output
+    window itself (k_rs_walk_bin, default) and the chunked walk followed by
+    rs5_partition (SG_RS_FUSED=0)."""
+    monkeypatch.setenv("SG_RS_FUSED", fused)
+    sl = g.gen_list(n, seed=n % 97)
+    rank, _ = g.rs_rank(sl, 256, seed=3)
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_record_paths_invalid_lists(cuda, monkeypatch, fused):
+    """Invalid lists overfill some output windows of the binned walk: the
+    records are dropped and the reference violation is still reported."""
+    monkeypatch.setenv("SG_RS_FUSED", fused)
+    n = 1_000_003
+    base = g.gen_list(n, seed=5).succ
+    order = np.argsort(-np.asarray(g.rs_rank(g.SuccessorList(base), 1)[0]))
+    s = base.copy()
+    a = int(order[n // 2])
+    s[a] = s[int(s[a])]                     # in-degree 2
+    s2 = base.copy()
+    s2[int(order[n // 3])] = int(order[n // 5])   # cycle back into the list
+    for bad in (s, s2):
+        want = g.validate_list(g.SuccessorList(bad))
+        assert want.kind != "ok"
+        with pytest.raises(g.InvalidListError) as ei:
+            g.rs_rank(g.SuccessorList(bad), 64)
+        assert str(ei.value) == str(want)
