@@ -86,8 +86,9 @@ typedef struct sg_launch {
     uint32_t blocks;    /* grid size                                      */
     uint32_t threads;   /* block size                                     */
     uint64_t items;     /* work items the launch covers (nodes / edges)   */
-    float ms;           /* CUDA-event duration on the launching stream    */
-    uint32_t pad;
+    float ms;           /* CUDA-event duration on the launching stream,
+                           filled by sg_stats_resolve()                   */
+    uint32_t pad;       /* library-private: event indices                 */
 } sg_launch;
 
 /* Execution statistics (the fields ExecStats needs, core.py:317-405). */
@@ -102,8 +103,9 @@ typedef struct sg_stats {
     uint32_t n_roots;         /* entries in roots_per_round               */
     uint32_t list_path;       /* rs: 0 ruling-set walk, 1 tile contraction */
     uint64_t roots_per_round[SG_MAX_ROUNDS];
-    float total_ms;           /* event time of the whole device pipeline  */
-    uint32_t pad2;
+    float total_ms;           /* event time of the whole device pipeline
+                                 (filled by sg_stats_resolve())           */
+    uint32_t pad2;            /* library-private: event-set ticket        */
     sg_launch launch[SG_MAX_LAUNCHES];
 } sg_stats;
 
@@ -119,6 +121,11 @@ typedef struct sg_violation {
 const char* sg_strerror(int status);
 const char* sg_kernel_name(int kernel_id);
 int sg_version(void);
+/* Fill launch[k].ms and total_ms of a finished call.  Calls return without
+ * reading their CUDA events (that costs ~3 us per launch of host time after
+ * the pipeline's last kernel); the events of one call stay valid for the
+ * next 15 calls on the device.  SG_ERR_RUNTIME: recycled (ms stay 0). */
+int sg_stats_resolve(sg_stats* st);
 /* last CUDA error string seen by this thread (for SG_ERR_CUDA) */
 const char* sg_last_cuda_error(void);
 

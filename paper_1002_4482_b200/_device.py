@@ -62,8 +62,15 @@ def exec_stats(st):
     device wall time)."""
     es = ExecStats(backend="sm_100a")
     nl = min(st.n_launches, _native.SG_MAX_LAUNCHES)
+    resolved = []
+
+    def resolve():  # event times are read on first use (sg_stats_resolve)
+        if not resolved:
+            _native.lib().sg_stats_resolve(ctypes.byref(st))
+            resolved.append(True)
 
     def build():  # `st` is this call's own sg_stats, kept alive by the closure
+        resolve()
         out = []
         for k in range(nl):
             L = st.launch[k]
@@ -73,9 +80,13 @@ def exec_stats(st):
                                     round=int(L.round), blocks=int(L.blocks), threads=int(L.threads), ms=ms))
         return out
 
+    def wall():
+        resolve()
+        return float(st.total_ms) / 1e3
+
     es.set_launch_log_source(build)
+    es.set_wall_time_source(wall)
     es.barriers = max(0, nl - 1)
-    es.wall_time = float(st.total_ms) / 1e3
     return es
 
 

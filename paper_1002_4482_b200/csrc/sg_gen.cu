@@ -38,6 +38,117 @@ __global__ void k_spl_meta(const uint32_t* __restrict__ keys, const uint32_t* __
     out[2 * (size_t)r + i] = last ? (long long)i : (long long)order[j + 1];
 }
 
+// Up to SPL_BLOCK_MAX splitters: keys, sort and meta in one CTA (one launch
+// instead of cub's five; the meta sits on the tail of every rs_rank call).
+// Random splitters have near-uniform ranks, so a counting sort by the top
+// log2(SPL_BLOCK_MAX) key bits leaves ~1 key per bucket; each bucket is then
+// finished by insertion sort (keys are distinct ranks).
+constexpr int SPL_THREADS = 1024;
+constexpr uint32_t SPL_BLOCK_MAX = 16384;
+constexpr int SPL_PER = SPL_BLOCK_MAX / SPL_THREADS;
+
+template <class RankT>
+__global__ void __launch_bounds__(SPL_THREADS) k_spl_meta_block(const RankT* __restrict__ rank,
+                                                                const long long* __restrict__ spl, uint32_t r,
+                                                                unsigned long long n, int shift,
+                                                                long long* __restrict__ out) {
+    extern __shared__ __align__(16) uint32_t spl_sm[];
+    uint32_t* start = spl_sm;                    // [SPL_BLOCK_MAX + 1] bucket counts, then starts
+    uint32_t* skey = start + SPL_BLOCK_MAX + 1;  // [r] keys in list order
+    uint32_t* sval = skey + SPL_BLOCK_MAX;       // [r] splitter indices in list order
+    __shared__ uint32_t warp_tot[SPL_THREADS / 32];
+    const uint32_t t = threadIdx.x, lane = t & 31u, w = t >> 5;
+    // (ranks of an invalid list are garbage: keep every key inside the table)
+    auto bucket = [&](uint32_t k) { return min(k >> shift, SPL_BLOCK_MAX - 1); };
+    for (uint32_t b = t; b <= SPL_BLOCK_MAX; b += SPL_THREADS) start[b] = 0;
+    __syncthreads();
+    uint32_t key[SPL_PER], slot[SPL_PER];
+#pragma unroll
+    for (int j = 0; j < SPL_PER; ++j) {
+        const uint32_t i = j * SPL_THREADS + t;
+        key[j] = i < r ? (uint32_t)(n - 1 - (unsigned long long)rank[spl[i]]) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < SPL_PER; ++j) {
+        const uint32_t i = j * SPL_THREADS + t;
+        slot[j] = i < r ? atomicAdd(&start[bucket(key[j])], 1u) : 0u;
+    }
+    __syncthreads();
+    // exclusive scan of the counts: thread t owns buckets [t*SPL_PER, (t+1)*SPL_PER)
+    uint32_t c[SPL_PER], tot = 0;
+#pragma unroll
+    for (int j = 0; j < SPL_PER; ++j) {
+        c[j] = start[t * SPL_PER + j];
+        tot += c[j];
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += v;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (uint32_t k = 0; k < w; ++k) pre += warp_tot[k];
+    uint32_t run = pre + incl - tot;
+#pragma unroll
+    for (int j = 0; j < SPL_PER; ++j) {
+        start[t * SPL_PER + j] = run;
+        run += c[j];
+    }
+    if (t == SPL_THREADS - 1) start[SPL_BLOCK_MAX] = run;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SPL_PER; ++j) {
+        const uint32_t i = j * SPL_THREADS + t;
+        if (i < r) {
+            const uint32_t pos = start[bucket(key[j])] + slot[j];
+            skey[pos] = key[j];
+            sval[pos] = i;
+        }
+    }
+    __syncthreads();
+    // finish each bucket (a handful of keys at most for random splitters)
+    for (uint32_t b = t; b < SPL_BLOCK_MAX; b += SPL_THREADS) {
+        const uint32_t lo = start[b], hi = start[b + 1];
+        for (uint32_t x = lo + 1; x < hi; ++x) {
+            const uint32_t kx = skey[x], vx = sval[x];
+            uint32_t y = x;
+            while (y > lo && skey[y - 1] > kx) {
+                skey[y] = skey[y - 1];
+                sval[y] = sval[y - 1];
+                --y;
+            }
+            skey[y] = kx;
+            sval[y] = vx;
+        }
+    }
+    __syncthreads();
+    for (uint32_t q = t; q < r; q += SPL_THREADS) {
+        const uint32_t i = sval[q];
+        const long long sr = (long long)(n - 1 - skey[q]);
+        const bool last = q + 1 == r;
+        out[i] = sr;
+        out[(size_t)r + i] = last ? sr + 1 : sr - (long long)(n - 1 - skey[q + 1]);
+        out[2 * (size_t)r + i] = last ? (long long)i : (long long)sval[q + 1];
+    }
+}
+
+template <class RankT>
+static int launch_spl_block(const void* rank, const int64_t* spl, uint32_t r, uint64_t n, int bits, int64_t* out,
+                            cudaStream_t s) {
+    int lb = 0;
+    while ((1u << (lb + 1)) <= SPL_BLOCK_MAX) ++lb;
+    const int shift = bits > lb ? bits - lb : 0;
+    const size_t smem = sizeof(uint32_t) * (3 * (size_t)SPL_BLOCK_MAX + 1);
+    auto k = k_spl_meta_block<RankT>;
+    SG_CUDA(set_smem_max(k, smem));
+    k<<<1, SPL_THREADS, smem, s>>>((const RankT*)rank, (const long long*)spl, r, n, shift, (long long*)out);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
 __global__ void __launch_bounds__(128) k_kiss(const unsigned long long* __restrict__ states, unsigned long long chunks,
                                               unsigned long long chunk_len, unsigned long long n,
                                               unsigned long long* __restrict__ out) {
@@ -162,6 +273,16 @@ int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t
     if (r == 0) return SG_OK;
     if (n == 0 || n > 0xFFFFFFFFull) return SG_ERR_VALUE;
     cudaStream_t s = (cudaStream_t)stream;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < n) ++bits;
+    if (r <= SPL_BLOCK_MAX && getenv("SG_SPL_DEVICE_SORT") == nullptr) {
+        switch (rank_dtype) {
+            case SG_U32: return launch_spl_block<uint32_t>(rank, spl, r, n, bits, out, s);
+            case SG_I32: return launch_spl_block<int32_t>(rank, spl, r, n, bits, out, s);
+            case SG_I64: return launch_spl_block<int64_t>(rank, spl, r, n, bits, out, s);
+            default: return SG_ERR_VALUE;
+        }
+    }
     Carver c(ws, ws_bytes);
     uint32_t* k0 = c.take<uint32_t>(r);
     uint32_t* k1 = c.take<uint32_t>(r);
@@ -179,8 +300,6 @@ int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t
         default: return SG_ERR_VALUE;
     }
     SG_LAUNCH_CHECK();
-    int bits = 1;
-    while (bits < 32 && (1ull << bits) < n) ++bits;
     SG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, k0, k1, v0, v1, (int)r, 0, bits, s));
     k_spl_meta<<<g, 256, 0, s>>>(k1, v1, r, n, (long long*)out);
     SG_LAUNCH_CHECK();

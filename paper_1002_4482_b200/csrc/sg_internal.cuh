@@ -108,17 +108,21 @@ class Recorder {
     // returns false if the launch table is full (recording stops, launches do not)
     void begin(int kernel, int round, uint32_t blocks, uint32_t threads, uint64_t items);
     void end();
-    // synchronises the stream and fills the ms fields; returns a cudaError
+    // synchronises the stream; the ms fields are filled later by
+    // sg_stats_resolve from the call's event set (ticket in sg_stats.pad2,
+    // event indices in sg_launch.pad)
     cudaError_t finish();
 
   private:
+    cudaEvent_t event(size_t i);
     sg_stats* st_;
     cudaStream_t s_;
-    std::vector<cudaEvent_t> ev_;
-    std::vector<size_t> begin_ix_, end_ix_;  // event indices of each launch
+    void* set_ = nullptr;  // this call's event set
+    size_t n_ev_ = 0;      // events recorded so far
+    size_t last_ = 0;      // index of the last end event
+    size_t begin_ix_ = 0;  // begin event of the open launch
     int open_ = -1;
     bool shared_ = false;  // the last end event doubles as the next begin event
-    cudaEvent_t t0_ = nullptr;
 };
 
 // SG_HOST_TIMING=1: host-side timestamps of a call's phases on stderr

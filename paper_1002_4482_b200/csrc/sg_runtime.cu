@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 
 #include "sg_internal.cuh"
@@ -16,14 +17,31 @@ void set_cuda_error(cudaError_t e) {
     g_last_cuda_error = std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e);
 }
 
-// Events are reused across calls (one pool per device per host thread):
-// creating two events per launch would cost more than the short launches.
-static thread_local std::vector<cudaEvent_t> g_pool[64];
+// Event sets.  A call records its launch boundaries into one of kSets sets
+// per device (round robin; events are reused -- creating two per launch would
+// cost more than the short launches).  The elapsed times are read only when
+// someone asks (sg_stats_resolve): ~30 cudaEventElapsedTime calls cost ~80 us
+// of host time, which would otherwise sit between the pipeline's last kernel
+// and the call's return.  A set is recycled kSets calls later; stats resolved
+// after that report SG_ERR_RUNTIME and keep ms = 0.
+constexpr int kSets = 16;
+struct EventSet {
+    std::vector<cudaEvent_t> ev;
+    uint32_t gen = 0;
+};
+static std::mutex g_sets_mu;
+static EventSet g_sets[64][kSets];
+static uint32_t g_next_set[64];
+static uint32_t g_gen = 0;
 
-static cudaEvent_t pool_event(size_t i) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::vector<cudaEvent_t>& pool = g_pool[dev & 63];
+// ticket: dev (6 bits) | set (4 bits) | generation (22 bits, never 0)
+static inline uint32_t make_ticket(int dev, int set, uint32_t gen) {
+    return ((uint32_t)(dev & 63) << 26) | ((uint32_t)set << 22) | (gen & 0x3FFFFFu);
+}
+
+cudaEvent_t Recorder::event(size_t i) {
+    if (!set_) return nullptr;
+    std::vector<cudaEvent_t>& pool = static_cast<EventSet*>(set_)->ev;
     while (pool.size() <= i) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
@@ -35,9 +53,23 @@ static cudaEvent_t pool_event(size_t i) {
 Recorder::Recorder(sg_stats* st, cudaStream_t s) : st_(st), s_(s) {
     if (st_) {
         st_->n_launches = 0;
-        t0_ = pool_event(0);
-        if (t0_) cudaEventRecord(t0_, s_);
-        ev_.push_back(t0_);
+        st_->total_ms = 0.f;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> lk(g_sets_mu);
+            const int k = (int)(g_next_set[dev & 63]++ % kSets);
+            uint32_t gen = ++g_gen & 0x3FFFFFu;
+            if (gen == 0) gen = ++g_gen & 0x3FFFFFu;
+            EventSet& es = g_sets[dev & 63][k];
+            es.gen = gen;
+            set_ = &es;
+            st_->pad2 = make_ticket(dev, k, gen);
+        }
+        cudaEvent_t t0 = event(0);
+        if (t0) cudaEventRecord(t0, s_);
+        n_ev_ = 1;
+        last_ = 0;
         shared_ = true;  // the first launch starts at t0
     }
 }
@@ -57,14 +89,12 @@ void Recorder::begin(int kernel, int round, uint32_t blocks, uint32_t threads, u
     L.threads = threads;
     L.items = items;
     L.ms = 0.f;
-    L.pad = 0;
     if (shared_) {  // back-to-back launches: the previous end event starts this one
-        begin_ix_.push_back(ev_.size() - 1);
+        begin_ix_ = last_;
     } else {
-        cudaEvent_t a = pool_event(ev_.size());
+        cudaEvent_t a = event(n_ev_);
         if (a) cudaEventRecord(a, s_);
-        ev_.push_back(a);
-        begin_ix_.push_back(ev_.size() - 1);
+        begin_ix_ = n_ev_++;
     }
     shared_ = false;
     open_ = int(k);
@@ -72,31 +102,48 @@ void Recorder::begin(int kernel, int round, uint32_t blocks, uint32_t threads, u
 
 void Recorder::end() {
     if (open_ < 0) return;
-    cudaEvent_t b = pool_event(ev_.size());
+    cudaEvent_t b = event(n_ev_);
     if (b) cudaEventRecord(b, s_);
-    ev_.push_back(b);
-    end_ix_.push_back(ev_.size() - 1);
+    last_ = n_ev_++;
+    st_->launch[open_].pad = (uint32_t)(begin_ix_ << 16) | (uint32_t)(last_ & 0xFFFFu);
     st_->n_launches = uint32_t(open_) + 1;
     open_ = -1;
     shared_ = true;
 }
 
-cudaError_t Recorder::finish() {
-    cudaError_t e = cudaStreamSynchronize(s_);
-    if (e != cudaSuccess || !st_) return e;
-    for (uint32_t k = 0; k < st_->n_launches && k < begin_ix_.size() && k < end_ix_.size(); ++k) {
-        const size_t ia = begin_ix_[k], ib = end_ix_[k];
-        if (ib < ev_.size() && ev_[ia] && ev_[ib]) {
+cudaError_t Recorder::finish() { return cudaStreamSynchronize(s_); }
+
+}  // namespace sg
+
+// Fill launch[k].ms and total_ms of a finished call from its events.
+extern "C" int sg_stats_resolve(sg_stats* st) {
+    using namespace sg;
+    if (!st) return SG_ERR_VALUE;
+    if (st->n_launches == 0) return SG_OK;
+    const uint32_t t = st->pad2;
+    const int dev = (int)(t >> 26), k = (int)((t >> 22) & 15u);
+    const uint32_t gen = t & 0x3FFFFFu;
+    std::lock_guard<std::mutex> lk(g_sets_mu);
+    EventSet& es = g_sets[dev][k];
+    if (gen == 0 || es.gen != gen) return SG_ERR_RUNTIME;  // the event set was recycled
+    uint32_t last = 0;
+    for (uint32_t i = 0; i < st->n_launches && i < SG_MAX_LAUNCHES; ++i) {
+        sg_launch& L = st->launch[i];
+        const uint32_t ia = L.pad >> 16, ib = L.pad & 0xFFFFu;
+        if (ia < es.ev.size() && ib < es.ev.size()) {
             float ms = 0.f;
-            if (cudaEventElapsedTime(&ms, ev_[ia], ev_[ib]) == cudaSuccess) st_->launch[k].ms = ms;
+            if (cudaEventElapsedTime(&ms, es.ev[ia], es.ev[ib]) == cudaSuccess) L.ms = ms;
         }
+        if (ib > last) last = ib;
     }
-    if (ev_.size() > 1 && ev_[0] && ev_.back()) {
+    if (last < es.ev.size() && last > 0) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, ev_[0], ev_.back()) == cudaSuccess) st_->total_ms = ms;
+        if (cudaEventElapsedTime(&ms, es.ev[0], es.ev[last]) == cudaSuccess) st->total_ms = ms;
     }
-    return cudaSuccess;
+    return SG_OK;
 }
+
+namespace sg {
 
 // Optional device tuning from the environment, applied once per process and
 // device: SG_L2_FETCH=<bytes> sets cudaLimitMaxL2FetchGranularity (a hint).

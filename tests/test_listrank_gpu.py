@@ -319,7 +319,19 @@ def test_c_abi_u32_path(cuda, orc):
                       _device.ptr(ws), ws.numel(), _device.stream_ptr(cuda), ctypes.byref(st), ctypes.byref(v))
     assert rc == 0
     assert np.array_equal(rank.cpu().numpy().astype(np.int64), orc.seq_rank(host))
-    assert st.levels >= 1 and st.level_size[0] == n and st.n_launches > 0 and st.total_ms > 0
+    assert st.levels >= 1 and st.level_size[0] == n and st.n_launches > 0
+    assert st.total_ms == 0 and st.launch[0].ms == 0      # event times are read on demand
+    assert L.sg_stats_resolve(ctypes.byref(st)) == 0
+    assert st.total_ms > 0 and all(st.launch[k].ms >= 0 for k in range(st.n_launches))
+    assert abs(sum(st.launch[k].ms for k in range(st.n_launches)) - st.total_ms) < 0.05 * st.total_ms + 0.05
+    # a call's event set is recycled 16 calls later: resolving then reports it
+    st2 = _native.Stats()
+    rc = L.sg_rs_rank(_device.ptr(succ), _native.SG_U32, _device.ptr(rank), _native.SG_U32, n, 0,
+                      _device.ptr(ws), ws.numel(), _device.stream_ptr(cuda), ctypes.byref(st2), ctypes.byref(v))
+    for _ in range(16):
+        g.rs_rank(g.SuccessorList(succ), 64)
+    assert L.sg_stats_resolve(ctypes.byref(st2)) == _native.SG_ERR_RUNTIME
+    assert st2.total_ms == 0
 
 
 # ---------------------------------------------------------------- scale
