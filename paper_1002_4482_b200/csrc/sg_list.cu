@@ -1129,6 +1129,67 @@ __global__ void __launch_bounds__(1024) k_rs_final(View src, uint2* A, uint2* B,
     }
 }
 
+// Multi-CTA weighted pointer jumping on a ruler list too big for one CTA
+// (used right above level 0: a level's walk is bound by its longest sublist,
+// ~2^kbits * ln(R) dependent hops, so three more walked levels cost more than
+// ~log2(R) in-place jump rounds over an L2-resident list).  Entries are
+// {inclusive weight up to `next`, next}; next = NIL once the sum reaches the
+// tail.  Rounds update in place: every version of an entry a reader can see is
+// a consistent (weight, next) pair of one 64-bit access, and each round at
+// least doubles every live pointer's reach, so ceil(log2 R) + 1 rounds suffice.
+template <class View>
+__global__ void __launch_bounds__(256) k_rs_top_init(View src, uint2* __restrict__ A, ListStatus* st, int level) {
+    const unsigned long long R = st->R[level];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += stride) {
+        unsigned long long nx;
+        uint32_t w;
+        src.load((uint32_t)i, nx, w);
+        uint32_t nxt = NIL;
+        if (nx >= R) {
+            st->bad = 1;
+        } else if (nx != i) {
+            nxt = (uint32_t)nx;
+        }
+        A[i] = make_uint2(w, nxt);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rs_top_jump(uint2* A, ListStatus* st, int level,
+                                                     uint32_t* __restrict__ IS) {
+    constexpr int U = 4;
+    const unsigned long long R = st->R[level];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < R;
+         i0 += stride * U) {
+        uint2 a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long i = i0 + (unsigned long long)u * stride;
+            a[u] = i < R ? __ldcg(A + i) : make_uint2(0u, NIL);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) b[u] = a[u].y != NIL ? __ldcg(A + a[u].y) : make_uint2(0u, NIL);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long i = i0 + (unsigned long long)u * stride;
+            if (i >= R) continue;
+            if (a[u].y != NIL) {
+                a[u].x += b[u].x;
+                a[u].y = b[u].y;
+                __stcg(A + i, a[u]);
+            }
+            if (IS != nullptr) {  // last round: the inclusive suffix sums
+                IS[i] = a[u].x;
+                if (i == 0) {
+                    st->head_sum = a[u].x;
+                    st->head_ok = (a[u].y == NIL) ? 1ull : 0ull;
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // expand (RS5 at level 0, listrank.py:360-382)
 
@@ -1643,9 +1704,13 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
     p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
+
     p.cap[0] = n;
+    // a ruler list of at most SG_RS_TOPN (> FINAL_CAP) nodes above level 0 is
+    // ranked by multi-CTA pointer jumping (k_rs_top_jump) instead of more walks
+    const unsigned long long topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
     unsigned long long N = n;
-    while (N > fin && p.levels < SG_MAX_LEVELS - 1) {
+    while (N > fin && p.levels < SG_MAX_LEVELS - 1 && !(p.levels >= 1 && N <= topn)) {
         const uint32_t kb = p.levels == 0 ? kb0 : kb1;
         const unsigned long long exp = (N >> kb) + 1;
         unsigned long long cap = exp + exp / 4 + 4096;
@@ -1890,19 +1955,39 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             rec.begin(K_RS_CONTRACT_LINK, 0, lg, 256, capR);
             k_rs_contract_link<<<lg, 256, 0, s>>>(b.rid, b.spl[0], b.IS[1], b.lvl[1], b.st);
         } else {
-            rec.begin(K_RS4_WALK, k, walk_grid, WALK_THREADS, capN);
-            k_rs_walk<LevelK><<<walk_grid, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
+            // about one sublist per lane: a bigger grid only queues its warps
+            // on the work-queue atomic (~30 us at the small levels)
+            unsigned long long wgk = (capR + WALK_THREADS - 1) / WALK_THREADS;
+            if (wgk > walk_grid) wgk = walk_grid;
+            if (wgk < 1) wgk = 1;
+            rec.begin(K_RS4_WALK, k, (uint32_t)wgk, WALK_THREADS, capN);
+            k_rs_walk<LevelK><<<(uint32_t)wgk, WALK_THREADS, 0, s>>>(LevelK{b.lvl[k]}, wk, b.spl[k], b.lvl[k + 1], b.st,
                                                                  k, p.kbits[k], p.salt[k], p.walk_cap);
         }
         rec.end();
         SG_LAUNCH_CHECK();
     }
-    // top: single CTA on the last ruler list
+    // top: single CTA on the last ruler list, or multi-CTA jumping if it is big
     const int L = p.levels;
-    rec.begin(K_RS4_RANK, L, 1, 1024, p.cap[L]);
-    k_rs_final<LevelK><<<1, 1024, 0, s>>>(LevelK{b.lvl[L]}, b.fa, b.fb, b.IS[L], b.st, L);
-    rec.end();
-    SG_LAUNCH_CHECK();
+    if (p.cap[L] > FINAL_CAP) {
+        const uint32_t g = grid_for(p.cap[L], 256, 4, kSMs * 8);
+        rec.begin(K_RS4_RANK, L, g, 256, p.cap[L]);
+        k_rs_top_init<LevelK><<<g, 256, 0, s>>>(LevelK{b.lvl[L]}, b.fa, b.st, L);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        const int rounds = jump_rounds(p.cap[L]) + 1;
+        for (int r = 1; r <= rounds; ++r) {
+            rec.begin(K_RS4_RANK, L, g, 256, p.cap[L]);
+            k_rs_top_jump<<<g, 256, 0, s>>>(b.fa, b.st, L, r == rounds ? b.IS[L] : nullptr);
+            rec.end();
+            SG_LAUNCH_CHECK();
+        }
+    } else {
+        rec.begin(K_RS4_RANK, L, 1, 1024, p.cap[L]);
+        k_rs_final<LevelK><<<1, 1024, 0, s>>>(LevelK{b.lvl[L]}, b.fa, b.fb, b.IS[L], b.st, L);
+        rec.end();
+        SG_LAUNCH_CHECK();
+    }
     // upward: expand
     for (int k = L - 1; k >= 1; --k) {
         const uint32_t g = grid_for(p.cap[k], 256, 1, kSMs * 8);
