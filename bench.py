@@ -54,7 +54,7 @@ def kernel_bytes(kernel, order, out):
     return {
         "rs3_walk": 96 if order == "random" else 20,   # RS3: packed write + succ[cur] + packed read (listrank.py:279-283)
         "rs5_partition": 12 + 8,                       # record {cur, sid|local} in, {cur, rank} pair out
-        "rs5_refine": 8 + 8,
+        "rs5_refine": 8 + 8,                           # binned walk record in, {cur, rank} out (IS_1 gather: L2)
         "rs5_scatter": 8 + out,
         "rs3_contract": 4 + 4,                         # succ in, {segment, distance} word out
         "rs5_expand": 4 + out,                         # node word in, rank out
@@ -334,7 +334,10 @@ def main():
                 "pipeline": {"algorithmic_bytes": pipe_bytes,
                              "bytes_per_unit": (LR_BYTES_PER_NODE[order] if kind == "list" else None),
                              "achieved": round(pipe_bytes / (ms_per_step / 1e3) / 1e9, 1),
-                             "frac": round(pipe_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4)}}
+                             "frac": round(pipe_bytes / (ms_per_step / 1e3) / 1e9 / peak, 4),
+                             "note": ("SURVEY 8(d) bytes: every parent gather charged a 32-B DRAM sector; "
+                                      "frac > 1 means the window partition served them from L2")
+                             if kind != "list" else "SURVEY 8(d) bytes per node"}}
     kernels = {k: round(sum(v) / len(v), 4) for k, v in sorted(kern_ms.items())}
 
     # ---- e2e through the public API with pinned host buffers -------------------------

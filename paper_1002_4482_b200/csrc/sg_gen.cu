@@ -47,9 +47,9 @@ constexpr int SPL_THREADS = 1024;
 constexpr uint32_t SPL_BLOCK_MAX = 16384;
 constexpr int SPL_PER = SPL_BLOCK_MAX / SPL_THREADS;
 
-template <class RankT>
-__global__ void __launch_bounds__(SPL_THREADS) k_spl_meta_block(const RankT* __restrict__ rank,
-                                                                const long long* __restrict__ spl, uint32_t r,
+// keys come from k_spl_keys (many CTAs: one SM alone cannot keep enough
+// random rank gathers in flight -- they cost ~30 us here)
+__global__ void __launch_bounds__(SPL_THREADS) k_spl_meta_block(const uint32_t* __restrict__ keys, uint32_t r,
                                                                 unsigned long long n, int shift,
                                                                 long long* __restrict__ out) {
     extern __shared__ __align__(16) uint32_t spl_sm[];
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(SPL_THREADS) k_spl_meta_block(const RankT* __r
 #pragma unroll
     for (int j = 0; j < SPL_PER; ++j) {
         const uint32_t i = j * SPL_THREADS + t;
-        key[j] = i < r ? (uint32_t)(n - 1 - (unsigned long long)rank[spl[i]]) : 0u;
+        key[j] = i < r ? __ldg(keys + i) : 0u;
     }
 #pragma unroll
     for (int j = 0; j < SPL_PER; ++j) {
@@ -125,26 +125,37 @@ __global__ void __launch_bounds__(SPL_THREADS) k_spl_meta_block(const RankT* __r
         }
     }
     __syncthreads();
-    for (uint32_t q = t; q < r; q += SPL_THREADS) {
-        const uint32_t i = sval[q];
-        const long long sr = (long long)(n - 1 - skey[q]);
-        const bool last = q + 1 == r;
-        out[i] = sr;
-        out[(size_t)r + i] = last ? sr + 1 : sr - (long long)(n - 1 - skey[q + 1]);
-        out[2 * (size_t)r + i] = last ? (long long)i : (long long)sval[q + 1];
+    // the three output rows are indexed by splitter: permute each through
+    // shared memory (the bucket table is free now) and store it coalesced
+    uint32_t* stage = start;
+    for (int row = 0; row < 3; ++row) {
+        for (uint32_t q = t; q < r; q += SPL_THREADS) {
+            const uint32_t i = sval[q];
+            const uint32_t k = skey[q];
+            const bool last = q + 1 == r;
+            uint32_t v;
+            if (row == 0)
+                v = (uint32_t)(n - 1 - k);                       // splitter rank
+            else if (row == 1)
+                v = last ? (uint32_t)(n - k) : skey[q + 1] - k;  // sublist length
+            else
+                v = last ? i : sval[q + 1];                      // reduced successor
+            stage[i] = v;
+        }
+        __syncthreads();
+        for (uint32_t i = t; i < r; i += SPL_THREADS) out[(size_t)row * r + i] = (long long)stage[i];
+        __syncthreads();
     }
 }
 
-template <class RankT>
-static int launch_spl_block(const void* rank, const int64_t* spl, uint32_t r, uint64_t n, int bits, int64_t* out,
-                            cudaStream_t s) {
+static int launch_spl_block(const uint32_t* keys, uint32_t r, uint64_t n, int bits, int64_t* out, cudaStream_t s) {
     int lb = 0;
     while ((1u << (lb + 1)) <= SPL_BLOCK_MAX) ++lb;
     const int shift = bits > lb ? bits - lb : 0;
     const size_t smem = sizeof(uint32_t) * (3 * (size_t)SPL_BLOCK_MAX + 1);
-    auto k = k_spl_meta_block<RankT>;
+    auto k = k_spl_meta_block;
     SG_CUDA(set_smem_max(k, smem));
-    k<<<1, SPL_THREADS, smem, s>>>((const RankT*)rank, (const long long*)spl, r, n, shift, (long long*)out);
+    k<<<1, SPL_THREADS, smem, s>>>(keys, r, n, shift, (long long*)out);
     SG_LAUNCH_CHECK();
     return SG_OK;
 }
@@ -275,14 +286,7 @@ int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t
     cudaStream_t s = (cudaStream_t)stream;
     int bits = 1;
     while (bits < 32 && (1ull << bits) < n) ++bits;
-    if (r <= SPL_BLOCK_MAX && getenv("SG_SPL_DEVICE_SORT") == nullptr) {
-        switch (rank_dtype) {
-            case SG_U32: return launch_spl_block<uint32_t>(rank, spl, r, n, bits, out, s);
-            case SG_I32: return launch_spl_block<int32_t>(rank, spl, r, n, bits, out, s);
-            case SG_I64: return launch_spl_block<int64_t>(rank, spl, r, n, bits, out, s);
-            default: return SG_ERR_VALUE;
-        }
-    }
+    const bool block = r <= SPL_BLOCK_MAX && getenv("SG_SPL_DEVICE_SORT") == nullptr;
     Carver c(ws, ws_bytes);
     uint32_t* k0 = c.take<uint32_t>(r);
     uint32_t* k1 = c.take<uint32_t>(r);
@@ -300,6 +304,7 @@ int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t
         default: return SG_ERR_VALUE;
     }
     SG_LAUNCH_CHECK();
+    if (block) return launch_spl_block(k0, r, n, bits, out, s);
     SG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, k0, k1, v0, v1, (int)r, 0, bits, s));
     k_spl_meta<<<g, 256, 0, s>>>(k1, v1, r, n, (long long*)out);
     SG_LAUNCH_CHECK();
