@@ -285,7 +285,7 @@ __device__ __forceinline__ int part_of(E edges, unsigned long long e, unsigned l
 // partition sizes: persistent CTAs; per 32 edges a warp takes five ballots
 // (valid + 4 partition bits) and lane p keeps partition p's count in a
 // register; one atomic per partition per CTA at the end.  Validates rows.
-template <class E>
+template <class E, int NB>  // NB = ceil(log2 P) partition bits (ballots per edge)
 __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigned long long m, unsigned long long n,
                                                                 unsigned long long row0,
                                                                 uint32_t shift, int P,
@@ -297,8 +297,6 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
     const uint32_t lane = lane_id();
     unsigned long long mine = 0;  // edges of partition `lane` seen by this warp
     const unsigned long long ntiles = (m + PART_TILE - 1) / PART_TILE;
-    int nbits = 0;
-    while ((1 << nbits) < P) ++nbits;
     constexpr int H = PART_ITEMS / 2;  // half a tile in flight: fewer registers, more resident warps
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
 #pragma unroll 1
@@ -315,18 +313,21 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
 #pragma unroll
             for (int j = 0; j < H; ++j) {
                 const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
-                int p = -1;
+                bool ok = false;
                 if (e < m) {
                     if (uu[j] >= n || vv[j] >= n)
                         atomicMax(flags + 1, ~(row0 + e));
                     else if (uu[j] == vv[j])
                         atomicMax(flags + 2, ~(row0 + e));
                     else
-                        p = (int)((uu[j] > vv[j] ? uu[j] : vv[j]) >> shift);
+                        ok = true;
                 }
-                unsigned msk = __ballot_sync(0xffffffffu, p >= 0);
-                for (int k = 0; k < nbits; ++k) {
-                    const unsigned b = __ballot_sync(0xffffffffu, p >= 0 && ((p >> k) & 1));
+                // valid ids fit 32 bits (n < 2^32): the partition math runs in 32-bit
+                const uint32_t p = max((uint32_t)uu[j], (uint32_t)vv[j]) >> shift;
+                unsigned msk = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+                for (int k = 0; k < NB; ++k) {
+                    const unsigned b = __ballot_sync(0xffffffffu, (p >> k) & 1u);
                     msk &= ((lane >> k) & 1u) ? b : ~b;
                 }
                 mine += __popc(msk);
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_cc_part_scatter(E edges, unsi
 // streams into shared memory while the current one is split.
 constexpr int PART2_CTAS_PER_SM = 2;
 
-template <class E>
+template <class E, int NB>
 __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatter2(
     E edges, unsigned long long m, unsigned long long n, uint32_t shift, int P,
     const unsigned long long* __restrict__ off_part, unsigned long long* __restrict__ cursor, uint2* __restrict__ out) {
@@ -435,11 +436,11 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
                 edges.load(e0 + e, u, v);  // the odd tail element of the last tile
             const bool ok = u < n && v < n && u != v;
             pr[j] = ((unsigned long long)(uint32_t)v << 32) | (uint32_t)u;
-            bn[j] = ok ? (uint32_t)((u > v ? u : v) >> shift) : (uint32_t)MS_MAXB;
+            bn[j] = ok ? max((uint32_t)u, (uint32_t)v) >> shift : (uint32_t)MS_MAXB;
         }
         __syncthreads();  // staging consumed: refill it behind the split
         issue(tile + gridDim.x);
-        ms_split<MS2_ITEMS, 4>(pr, bn, bin_of, slot, (uint32_t)P, cursor, reinterpret_cast<unsigned long long*>(out), sm);
+        ms_split<MS2_ITEMS, NB>(pr, bn, bin_of, slot, (uint32_t)P, cursor, reinterpret_cast<unsigned long long*>(out), sm);
     }
 }
 
@@ -555,18 +556,23 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
-    k_cc_part_count<E><<<cg, PART_THREADS, 0, s>>>(view, m, n, row0, p.shift, p.parts, b.totals, flags);
+    int nbits = 0;
+    while ((1 << nbits) < p.parts) ++nbits;
+    auto kc = nbits <= 1 ? k_cc_part_count<E, 1>
+            : nbits == 2 ? k_cc_part_count<E, 2> : nbits == 3 ? k_cc_part_count<E, 3> : k_cc_part_count<E, 4>;
+    kc<<<cg, PART_THREADS, 0, s>>>(view, m, n, row0, p.shift, p.parts, b.totals, flags);
     SG_LAUNCH_CHECK();
     k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
     if (((uintptr_t)view.e & 15) == 0) {
         const size_t smem = (size_t)MS2_TILE * E::kBytes + MsSmem::bytes((uint32_t)p.parts, MS2_TILE);
-        SG_CUDA(set_smem_max(k_cc_part_scatter2<E>, smem));
+        auto ks = nbits <= 1 ? k_cc_part_scatter2<E, 1>
+                : nbits == 2 ? k_cc_part_scatter2<E, 2> : nbits == 3 ? k_cc_part_scatter2<E, 3> : k_cc_part_scatter2<E, 4>;
+        SG_CUDA(set_smem_max(ks, smem));
         const unsigned long long ntile = (m + MS2_TILE - 1) / MS2_TILE;
         const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * PART2_CTAS_PER_SM ? ntile
                                                                                             : kSMs * PART2_CTAS_PER_SM);
-        k_cc_part_scatter2<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor,
-                                                           b.edges);
+        ks<<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
     } else {
         const size_t smem = MsSmem::bytes((uint32_t)p.parts);
         SG_CUDA(set_smem_max(k_cc_part_scatter<E>, smem));
