@@ -288,57 +288,61 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
                                                             uint32_t* __restrict__ tile_cnt,
                                                             uint32_t* __restrict__ tile_end, ListStatus* st,
                                                             uint32_t kbits, uint32_t salt) {
+    // one warp per tile (persistent warps): no block barrier between tiles, so
+    // a warp's next loads never wait on its neighbours' reductions
     constexpr int VEC = 16 / sizeof(SuccT);  // ids per 16-B load
-    constexpr int NLD = TILE_ITEMS / VEC;    // loads per thread per tile
+    constexpr int SUB = 4;                   // 16-B loads per lane in flight
+    constexpr int PER = 32 * SUB * VEC;      // ids per warp step
     typedef typename std::conditional<sizeof(SuccT) == 4, uint4, ulonglong2>::type V;
-    typedef cub::BlockReduce<uint32_t, TILE_THREADS> BR;
-    __shared__ typename BR::TempStorage tmp;
     const unsigned long long N = st->R[0];
     const unsigned long long ntiles = (N + TILE - 1) / TILE;
-    // persistent blocks walk the tiles; all loads of a tile are issued before
-    // the (rare) atomics of the self-loop / range census
-    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t lane = lane_id();
+    const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    for (unsigned long long tile = gw; tile < ntiles; tile += nw) {
         const unsigned long long base = tile * TILE;
         const bool full = kVec && base + TILE <= N;
-        SuccT e[TILE_ITEMS];
-        if (full) {
-            const V* src = reinterpret_cast<const V*>(succ + base);
+        uint32_t packed = 0;  // rulers << 16 | ends
+#pragma unroll 1
+        for (uint32_t s0 = 0; s0 < (uint32_t)TILE; s0 += PER) {
+            SuccT e[SUB * VEC];
+            if (full) {
+                const V* src = reinterpret_cast<const V*>(succ + base + s0);
 #pragma unroll
-            for (int j = 0; j < NLD; ++j) {
-                const V v = __ldcs(src + j * TILE_THREADS + threadIdx.x);
+                for (int j = 0; j < SUB; ++j) {
+                    const V v = __ldcs(src + j * 32 + lane);
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) e[j * VEC + c] = reinterpret_cast<const SuccT*>(&v)[c];
+                    for (int c = 0; c < VEC; ++c) e[j * VEC + c] = reinterpret_cast<const SuccT*>(&v)[c];
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < SUB; ++j)
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c) {
+                        const unsigned long long i = base + s0 + (unsigned long long)(j * 32 + lane) * VEC + c;
+                        e[j * VEC + c] = i < N ? __ldcs(succ + i) : SuccT(0);
+                    }
             }
-        } else {
 #pragma unroll
-            for (int j = 0; j < NLD; ++j)
+            for (int j = 0; j < SUB; ++j)
 #pragma unroll
                 for (int c = 0; c < VEC; ++c) {
-                    const unsigned long long i = base + (unsigned long long)(j * TILE_THREADS + threadIdx.x) * VEC + c;
-                    e[j * VEC + c] = i < N ? __ldcs(succ + i) : SuccT(0);
+                    const uint32_t l = s0 + (j * 32 + lane) * VEC + c;
+                    if (full || base + l < N) {
+                        const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
+                        const uint32_t i = (uint32_t)base + l, x = (uint32_t)x64;
+                        const bool oor = x64 >= N, self = !oor && x == i;
+                        if (oor | self) note_succ(st, i, x64, N);
+                        packed += (is_ruler(i, kbits, salt) ? 0x10000u : 0u) +
+                                  ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
+                    }
                 }
         }
-        uint32_t packed = 0;  // rulers << 16 | ends
-        const uint32_t b32 = (uint32_t)base;
-#pragma unroll
-        for (int j = 0; j < NLD; ++j)
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-                const uint32_t l = (j * TILE_THREADS + threadIdx.x) * VEC + c;
-                if (full || base + l < N) {
-                    const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
-                    const uint32_t i = b32 + l, x = (uint32_t)x64;
-                    const bool oor = x64 >= N, self = !oor && x == i;
-                    if (oor | self) note_succ(st, i, x64, N);
-                    packed += (is_ruler(i, kbits, salt) ? 0x10000u : 0u) + ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
-                }
-            }
-        const uint32_t tot = BR(tmp).Sum(packed);
-        if (threadIdx.x == 0) {
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, packed);
+        if (lane == 0) {
             tile_cnt[tile] = tot >> 16;
             tile_end[tile] = tot & 0xFFFFu;
         }
-        __syncthreads();
     }
 }
 
@@ -1886,8 +1890,9 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
         uint32_t* tk = k == 0 ? b.tiles : b.tiles_up;
         if (k == 0) {
-            rec.begin(K_RS_COUNT, 0, nt, TILE_THREADS, capN);
-            const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
+            const uint32_t cw = (nt + TILE_THREADS / 32 - 1) / (TILE_THREADS / 32);  // one warp per tile
+            const uint32_t cg = cw < kSMs * 8 ? cw : kSMs * 8;
+            rec.begin(K_RS_COUNT, 0, cg, TILE_THREADS, capN);
             if (((uintptr_t)succ & 15) == 0)
                 k_rs_count0<SuccT, true><<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0],
                                                                       p.salt[0]);
