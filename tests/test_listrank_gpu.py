@@ -424,3 +424,24 @@ def test_record_paths_invalid_lists(cuda, monkeypatch, fused):
         with pytest.raises(g.InvalidListError) as ei:
             g.rs_rank(g.SuccessorList(bad), 64)
         assert str(ei.value) == str(want)
+
+
+@pytest.mark.parametrize("topn", ["0", "20000", "524288"])
+def test_top_level_ranking_paths(cuda, orc, monkeypatch, topn):
+    """The ruler list above level 0 is finished either by more walked levels
+    and the one-CTA final (SG_RS_TOPN=0), or by multi-CTA in-place pointer
+    jumping once it has at most SG_RS_TOPN rulers (default 2^19)."""
+    monkeypatch.setenv("SG_RS_TOPN", topn)
+    sl = g.gen_list(2_500_003, seed=11)
+    rank, st = g.rs_rank(sl, 128, seed=1)
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
+    names = [r.kernel for r in st.launch_log]
+    if topn == "0":
+        assert names.count("rs4_walk") >= 2 and names.count("rs4_rank") == 1
+    else:
+        assert names.count("rs4_rank") > 10          # init + ceil(log2 R) + 1 jump rounds
+    # an invalid list through the same path still reports the reference violation
+    s = sl.succ.copy()
+    s[int(np.flatnonzero(s == np.arange(s.size))[0])] = 0   # tail -> head: one big cycle
+    with pytest.raises(g.InvalidListError):
+        g.rs_rank(g.SuccessorList(s), 64)
