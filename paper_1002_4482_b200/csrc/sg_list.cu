@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(WALK_THREADS, 2048 / WALK_THREADS) k_rs_walk_r
 //   store    the record into the reserved slot, then commit com[b]++;
 //   flush    the lane whose commit completes the buffer hands it to its warp,
 //            which claims WB_SLOTS slots of window b's region with one global
-//            atomic and writes them as one 128-B line, then reopens the buffer
+//            atomic and writes them as one 256-B run, then reopens the buffer
 //            (com = 0 before res = 0: a reserver that sees res reopened also
 //            sees com reset).
 // A valid list puts exactly 2^cshift records into each full window, so the
@@ -790,42 +790,22 @@ __global__ void __launch_bounds__(WB_THREADS, WB_CTAS_PER_SM) k_rs_walk_bin(
             unsigned m = __ballot_sync(0xffffffffu, last);
             if (m == 0) continue;
             __threadfence_block();
-            // all full buffers of this warp: claim their lines together, then copy two per pass
+            // all full buffers of this warp: claim their runs together, then copy one per pass
             unsigned long long base = 0;
             if (last) base = atomicAdd(&cursor[b], (unsigned long long)WB_SLOTS);
-            if (WB_SLOTS == 16) {
-                while (m) {
-                    const int s0 = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int s1 = m ? __ffs(m) - 1 : s0;
-                    if (m) m &= m - 1;
-                    const int src = lane < 16 ? s0 : s1;
-                    const uint32_t fb = __shfl_sync(0xffffffffu, b, src);
-                    const unsigned long long fbase = __shfl_sync(0xffffffffu, base, src);
-                    if (lane < 16 || s1 != s0) store_run(fb, WB_SLOTS, fbase, lane & 15u);
-                    __syncwarp();
-                    if ((lane & 15u) == 0 && (lane < 16 || s1 != s0)) {
-                        atomicExch(&com[fb], 0u);
-                        __threadfence_block();
-                        atomicExch(&res[fb], 0u);
-                    }
-                    __syncwarp();
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t fb = __shfl_sync(0xffffffffu, b, src);
+                const unsigned long long fbase = __shfl_sync(0xffffffffu, base, src);
+                for (uint32_t k = lane; k < WB_SLOTS; k += 32) store_run(fb, WB_SLOTS, fbase, k);
+                __syncwarp();
+                if (lane == 0) {
+                    atomicExch(&com[fb], 0u);
+                    __threadfence_block();
+                    atomicExch(&res[fb], 0u);
                 }
-            } else {
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t fb = __shfl_sync(0xffffffffu, b, src);
-                    const unsigned long long fbase = __shfl_sync(0xffffffffu, base, src);
-                    for (uint32_t k = lane; k < WB_SLOTS; k += 32) store_run(fb, WB_SLOTS, fbase, k);
-                    __syncwarp();
-                    if (lane == 0) {
-                        atomicExch(&com[fb], 0u);
-                        __threadfence_block();
-                        atomicExch(&res[fb], 0u);
-                    }
-                    __syncwarp();
-                }
+                __syncwarp();
             }
         }
         if (!done) {
@@ -1921,21 +1901,17 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             // scattered layouts: record walk; local layouts: tile contraction
             if (p.fused) {
                 SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
-                static const int cfg = (int)env_u32("SG_WB_CFG", 0, 0, 1);
-                auto launch = [&](auto kern, int threads, int ctas, size_t smem) -> cudaError_t {
-                    const cudaError_t e = set_smem_max(kern, smem);
-                    if (e != cudaSuccess) return e;
-                    rec.begin(K_RS3_WALK, 0, kSMs * ctas, threads, capN);
-                    kern<<<kSMs * ctas, threads, smem, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.cursor, b.pairs, b.st,
-                                                         p.kbits[0], p.salt[0], p.walk_cap, p.load_mode, p.rec_sb,
-                                                         p.rec_lb, p.cshift, p.cbins);
-                    return cudaSuccess;
-                };
-                const size_t nb = (size_t)p.cbins * sizeof(unsigned long long);
-                if (cfg == 1)
-                    SG_CUDA(launch(k_rs_walk_bin<SuccT, 512, 4, 16>, 512, 4, nb * 16));
-                else
-                    SG_CUDA(launch(k_rs_walk_bin<SuccT, 1024, 2, 32>, 1024, 2, nb * 32));
+                // 2 x 1024 threads per SM (the walk needs every resident lane:
+                // 1536 per SM was 60 % slower), 32-record buffers per window
+                constexpr int WB_T = 1024, WB_C = 2;
+                constexpr uint32_t WB_S = 32;
+                auto kern = k_rs_walk_bin<SuccT, WB_T, WB_C, WB_S>;
+                const size_t smem = (size_t)p.cbins * WB_S * sizeof(unsigned long long);
+                SG_CUDA(set_smem_max(kern, smem));
+                rec.begin(K_RS3_WALK, 0, kSMs * WB_C, WB_T, capN);
+                kern<<<kSMs * WB_C, WB_T, smem, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.cursor, b.pairs, b.st,
+                                                     p.kbits[0], p.salt[0], p.walk_cap, p.load_mode, p.rec_sb, p.rec_lb,
+                                                     p.cshift, p.cbins);
             } else {
             rec.begin(K_RS3_WALK, 0, walk_grid, WALK_THREADS, capN);
             if (p.packed)
@@ -2029,8 +2005,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
     }
-    static const int rit = (int)env_u32("SG_REF_IT", 8, 8, 16);
-    if (p.fused && rit == 8) {
+    if (p.fused) {  // 8 records per thread, 3 CTAs per SM: more warps to hide the IS_1 gathers
         constexpr uint32_t t8 = MS_THREADS * 8;
         const size_t sm8 = (size_t)t8 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), t8);
         const uint32_t fbits = p.cshift - p.fshift;  // ballots per element in the split
@@ -2041,7 +2016,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         kr<<<kSMs * 3, MS_THREADS, sm8, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
                                              b.IS[1], p.rec_sb, p.rec_lb);
     } else {
-        auto kr = p.fused ? k_rs_rec_refine2<MS2_ITEMS, 1> : k_rs_rec_refine2<MS2_ITEMS, 0>;
+        auto kr = k_rs_rec_refine2<MS2_ITEMS, 0>;
         SG_CUDA(set_smem_max(kr, sm_ref2));
         rec.begin(K_RS5_REFINE, 0, persist2, MS_THREADS, n);
         kr<<<persist2, MS_THREADS, sm_ref2, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
