@@ -445,3 +445,17 @@ def test_top_level_ranking_paths(cuda, orc, monkeypatch, topn):
     s[int(np.flatnonzero(s == np.arange(s.size))[0])] = 0   # tail -> head: one big cycle
     with pytest.raises(g.InvalidListError):
         g.rs_rank(g.SuccessorList(s), 64)
+
+
+@pytest.mark.parametrize("n", [8_193, 65_537, 1_048_575, 2_097_153, (1 << 23) + 1])
+def test_plan_boundaries(cuda, orc, n):
+    """Sizes around the plan's switch points: the one-CTA final (8192), the
+    pointer-jumping top (2^19 rulers), and the coarse-window count (256
+    windows of 2^15 int32 ranks at 2^23: one more node doubles the window)."""
+    sl = g.gen_list(n, seed=n % 1009)
+    want = orc.seq_rank(sl.succ)
+    rank, _ = g.rs_rank(sl, 64, seed=2)                                   # int64 ranks (host input)
+    assert np.array_equal(rank, want)
+    d = torch.from_numpy(sl.succ.astype(np.int32)).to(cuda)
+    out, _ = g.rs_rank(g.SuccessorList(d), 64, seed=2)                     # int32 ranks (device input)
+    assert np.array_equal(out.cpu().numpy().astype(np.int64), want)
