@@ -75,6 +75,7 @@ struct ListStatus {
     unsigned long long R[SG_MAX_LEVELS + 1];      // nodes per level (R[0] = n)
     unsigned long long qhead[SG_MAX_LEVELS + 1];  // walk work-queue heads
     unsigned long long chunks;      // record chunks handed out by the level-0 record walk
+    unsigned long long top_live[3]; // cooperative top-level jumping: live pointers seen per round (mod 3)
 };
 
 // Error plumbing -------------------------------------------------------------

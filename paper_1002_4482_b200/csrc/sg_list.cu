@@ -33,6 +33,7 @@
 #include <cub/block/block_scan.cuh>
 #include <cub/block/block_store.cuh>
 
+#include <cooperative_groups.h>
 #include <stdlib.h>
 #include <type_traits>
 #include <string.h>
@@ -116,6 +117,7 @@ __global__ void k_status_init(ListStatus* st, unsigned long long n) {
         st->bad = 0;
         st->local = 0;
         st->chunks = 0;
+        st->top_live[0] = st->top_live[1] = st->top_live[2] = 0;
     }
     if (threadIdx.x <= SG_MAX_LEVELS) {
         st->R[threadIdx.x] = threadIdx.x == 0 ? n : 0;
@@ -1174,6 +1176,58 @@ __global__ void __launch_bounds__(256) k_rs_top_jump(uint2* A, ListStatus* st, i
     }
 }
 
+// The same as one cooperative launch: init, the jump rounds separated by
+// grid barriers (a round costs ~3 us instead of a ~5 us launch), stopping
+// once a round finds no live pointer, and the extraction.
+template <class View>
+__global__ void __launch_bounds__(512) k_rs_top_coop(View src, uint2* A, ListStatus* st, int level,
+                                                     uint32_t* __restrict__ IS, int rounds) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const unsigned long long R = st->R[level];
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (unsigned long long i = t0; i < R; i += stride) {
+        unsigned long long nx;
+        uint32_t w;
+        src.load((uint32_t)i, nx, w);
+        uint32_t nxt = NIL;
+        if (nx >= R) {
+            st->bad = 1;
+        } else if (nx != i) {
+            nxt = (uint32_t)nx;
+        }
+        A[i] = make_uint2(w, nxt);
+    }
+    grid.sync();
+    for (int r = 0; r < rounds; ++r) {
+        if (t0 == 0) st->top_live[(r + 1) % 3] = 0;  // next round's flag (last read two barriers ago)
+        int live = 0;
+        for (unsigned long long i = t0; i < R; i += stride) {
+            uint2 a = __ldcg(A + i);
+            if (a.y != NIL) {
+                const uint2 b = __ldcg(A + a.y);
+                a.x += b.x;
+                a.y = b.y;
+                __stcg(A + i, a);
+                live |= (b.y != NIL);
+            }
+        }
+        live = __syncthreads_or(live);
+        if (live && threadIdx.x == 0) atomicOr(&st->top_live[r % 3], 1ull);
+        grid.sync();
+        if (*(volatile unsigned long long*)&st->top_live[r % 3] == 0) break;  // every pointer reached the tail
+    }
+    for (unsigned long long i = t0; i < R; i += stride) {
+        const uint2 a = __ldcg(A + i);
+        IS[i] = a.x;
+        if (i == 0) {
+            st->head_sum = a.x;
+            st->head_ok = (a.y == NIL) ? 1ull : 0ull;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // expand (RS5 at level 0, listrank.py:360-382)
 
@@ -1634,6 +1688,7 @@ struct RsPlan {
     int contract = 1;                            // allow the tile contraction for local layouts
     bool packed = false;                         // level-0 records packed into one u64
     bool fused = false;                          // packed records binned by the walk (no rs5_partition)
+    bool coop_top = true;                        // top-level jumping as one cooperative launch
     uint32_t rec_sb = 0, rec_lb = 0;             // packed record: cur << sb | sid << lb | local
     unsigned long long maxchunks = 0;            // record chunks (REC_CH records each)
     uint32_t kbits[SG_MAX_LEVELS] = {};
@@ -1688,6 +1743,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
     p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
     p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
+    p.coop_top = env_u32("SG_RS_COOP", 1, 0, 1) != 0;
 
     p.cap[0] = n;
     // a ruler list of at most SG_RS_TOPN (> FINAL_CAP) nodes above level 0 is
@@ -1950,7 +2006,35 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     // top: single CTA on the last ruler list, or multi-CTA jumping if it is big
     const int L = p.levels;
-    if (p.cap[L] > FINAL_CAP) {
+    bool coop_done = false;
+    if (p.cap[L] > FINAL_CAP && p.coop_top) {
+        static int coop_blocks = -1;  // resident 512-thread CTAs per SM for the cooperative launch
+        if (coop_blocks < 0) {
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rs_top_coop<LevelK>, 512, 0) != cudaSuccess) nb = 0;
+            coop_blocks = nb;
+        }
+        if (coop_blocks > 0) {
+            LevelK view{b.lvl[L]};
+            uint2* A = b.fa;
+            ListStatus* stp = b.st;
+            int lv = L;
+            uint32_t* isp = b.IS[L];
+            int rounds = jump_rounds(p.cap[L]) + 1;
+            void* args[] = {&view, &A, &stp, &lv, &isp, &rounds};
+            const uint32_t g = (uint32_t)(kSMs * (coop_blocks < 2 ? coop_blocks : 2));
+            rec.begin(K_RS4_RANK, L, g, 512, p.cap[L]);
+            const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_rs_top_coop<LevelK>, g, 512, args, 0, s);
+            rec.end();
+            if (e == cudaSuccess) {
+                coop_done = true;
+            } else {
+                (void)cudaGetLastError();  // not co-resident here: the multi-launch rounds below
+            }
+        }
+    }
+    if (coop_done) {
+    } else if (p.cap[L] > FINAL_CAP) {
         const uint32_t g = grid_for(p.cap[L], 256, 4, kSMs * 8);
         rec.begin(K_RS4_RANK, L, g, 256, p.cap[L]);
         k_rs_top_init<LevelK><<<g, 256, 0, s>>>(LevelK{b.lvl[L]}, b.fa, b.st, L);

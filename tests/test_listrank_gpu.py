@@ -426,20 +426,26 @@ def test_record_paths_invalid_lists(cuda, monkeypatch, fused):
         assert str(ei.value) == str(want)
 
 
-@pytest.mark.parametrize("topn", ["0", "20000", "524288"])
-def test_top_level_ranking_paths(cuda, orc, monkeypatch, topn):
+@pytest.mark.parametrize("topn,coop", [("0", "1"), ("20000", "1"), ("20000", "0"), ("524288", "1")])
+def test_top_level_ranking_paths(cuda, orc, monkeypatch, topn, coop):
     """The ruler list above level 0 is finished either by more walked levels
     and the one-CTA final (SG_RS_TOPN=0), or by multi-CTA in-place pointer
-    jumping once it has at most SG_RS_TOPN rulers (default 2^19)."""
+    jumping once it has at most SG_RS_TOPN rulers (default 2^19): one
+    cooperative launch with grid barriers (default) or one launch per round
+    (SG_RS_COOP=0)."""
     monkeypatch.setenv("SG_RS_TOPN", topn)
+    monkeypatch.setenv("SG_RS_COOP", coop)
     sl = g.gen_list(2_500_003, seed=11)
     rank, st = g.rs_rank(sl, 128, seed=1)
     assert np.array_equal(rank, orc.seq_rank(sl.succ))
-    names = [r.kernel for r in st.launch_log]
+    top = [r for r in st.launch_log if r.kernel == "rs4_rank"]
     if topn == "0":
-        assert names.count("rs4_walk") >= 2 and names.count("rs4_rank") == 1
+        assert sum(r.kernel == "rs4_walk" for r in st.launch_log) >= 2
+        assert len(top) == 1 and top[0].blocks == 1
+    elif coop == "1":
+        assert len(top) == 1 and top[0].blocks > 1      # init + rounds + extraction in one grid
     else:
-        assert names.count("rs4_rank") > 10          # init + ceil(log2 R) + 1 jump rounds
+        assert len(top) > 10                            # init + ceil(log2 R) + 1 jump rounds
     # an invalid list through the same path still reports the reference violation
     s = sl.succ.copy()
     s[int(np.flatnonzero(s == np.arange(s.size))[0])] = 0   # tail -> head: one big cycle
