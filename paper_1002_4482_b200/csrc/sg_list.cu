@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
         mbar_wait(&bar, phase);
         phase ^= 1u;
         unsigned long long pr[IT];
-        uint32_t bn[IT];
+        uint32_t bn[IT], gv[IT];
 #pragma unroll
         for (int g = 0; g < IT / 2; ++g) {
             const uint32_t e = (g * MS_THREADS + threadIdx.x) * 2;
@@ -998,31 +998,27 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
             for (int q = 0; q < 2; ++q) {
                 const int j = g * 2 + q;
                 pr[j] = vv[q];
-                if (kMode == 1) {  // gathers first, all in flight together; IS_1 stays in L2
+                // kMode 1: the IS_1 gather is issued here and first used when
+                // the tile is placed, so it flies while the ballots rank it
+                const unsigned long long cur = kMode == 1 ? (vv[q] >> sb) : (vv[q] >> 32);
+                if (kMode == 1) {
                     const unsigned long long o = (vv[q] >> lb) & ((1ull << (sb - lb)) - 1);
-                    bn[j] = ld_hint(IS1 + (o < R1 ? o : 0), pol_last);
-                    continue;
+                    gv[j] = ld_hint(IS1 + (o < R1 ? o : 0), pol_last);
                 }
-                const unsigned long long cur = pr[j] >> 32;
                 bn[j] = (e + q < cnt && (cur >> cshift) == c) ? (uint32_t)((cur >> fshift) & (fb - 1))
                                                              : (uint32_t)MS_MAXB;
-            }
-        }
-        if (kMode == 1) {
-#pragma unroll
-            for (int j = 0; j < IT; ++j) {
-                const uint32_t e = ((j >> 1) * MS_THREADS + threadIdx.x) * 2 + (j & 1);
-                const unsigned long long cur = pr[j] >> sb;
-                const uint32_t local = (uint32_t)(pr[j] & ((1ull << lb) - 1));
-                pr[j] = (cur << 32) | (bn[j] - local - 1u);
-                bn[j] = (e < cnt && (cur >> cshift) == c) ? (uint32_t)((cur >> fshift) & (fb - 1)) : (uint32_t)MS_MAXB;
             }
         }
         __syncthreads();
         issue(tile + gridDim.x);
         auto bin_of = [&](unsigned long long pr) { return (uint32_t)(((pr >> 32) >> fshift) & (fb - 1)); };
         auto slot = [&](uint32_t b) { return make_ulonglong2((c * fb + b) << fshift, 1ull << fshift); };
-        over |= ms_split<IT, NB>(pr, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
+        auto pair = [&](int j) -> unsigned long long {
+            if (kMode != 1) return pr[j];
+            const unsigned long long cur = pr[j] >> sb;
+            return (cur << 32) | (uint32_t)(gv[j] - (uint32_t)(pr[j] & ((1ull << lb) - 1)) - 1u);
+        };
+        over |= ms_split_fn<IT, NB>(pair, bn, bin_of, slot, fb, cursor + c * fb, out, sm);
     }
     if (over) st->bad = 1;
 }

@@ -63,11 +63,13 @@ struct MsSmem {
 // cursor[bin] (global u64) counts the bin's slots already claimed.
 // bin_of(pair) recovers the bin when writing out.  Returns true if a bin
 // overflowed (only for inputs that break the caller's size contract).
-template <int ITEMS, int NBITS, class BinOf, class Slot>
-__device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], const uint32_t (&bn)[ITEMS],
-                                         BinOf bin_of, Slot slot, uint32_t nb,
-                                         unsigned long long* __restrict__ cursor,
-                                         unsigned long long* __restrict__ out, MsSmem& sm) {
+// pair(j) yields element j's value; it is first needed when the tile is
+// placed, after the ranking, so a value that waits on a gather can arrive
+// while the ballots run.
+template <int ITEMS, int NBITS, class PairFn, class BinOf, class Slot>
+__device__ __forceinline__ bool ms_split_fn(PairFn pair, const uint32_t (&bn)[ITEMS], BinOf bin_of, Slot slot,
+                                            uint32_t nb, unsigned long long* __restrict__ cursor,
+                                            unsigned long long* __restrict__ out, MsSmem& sm) {
     const uint32_t lane = lane_id();
     const int w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -146,7 +148,7 @@ __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], 
     // place into the sorted tile
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j)
-        if (bn[j] < nb) sm.buf[sm.start[bn[j]] + sm.w[w * nb + bn[j]] + rk[j]] = pr[j];
+        if (bn[j] < nb) sm.buf[sm.start[bn[j]] + sm.w[w * nb + bn[j]] + rk[j]] = pair(j);
     __syncthreads();
     // write out, run by run
     uint32_t total = 0;
@@ -163,6 +165,14 @@ __device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], 
     }
     __syncthreads();  // the smem is reused by the next tile
     return over;
+}
+
+template <int ITEMS, int NBITS, class BinOf, class Slot>
+__device__ __forceinline__ bool ms_split(const unsigned long long (&pr)[ITEMS], const uint32_t (&bn)[ITEMS],
+                                         BinOf bin_of, Slot slot, uint32_t nb,
+                                         unsigned long long* __restrict__ cursor,
+                                         unsigned long long* __restrict__ out, MsSmem& sm) {
+    return ms_split_fn<ITEMS, NBITS>([&](int j) { return pr[j]; }, bn, bin_of, slot, nb, cursor, out, sm);
 }
 
 // One tile: elements [e0, e1), element (j, t) = e0 + j*MS_THREADS + t.
