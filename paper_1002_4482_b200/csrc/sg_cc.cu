@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned l
         i += rng[0];
         m = rng[1];
     }
-    // HU edges per iteration: 2*HU independent parent loads in flight
-    constexpr int HU = 4;
+    // HU edges per iteration: 2*HU independent parent loads in flight (2 beats 4 and 8:
+    // fewer unions racing for the same roots, measured)
+    constexpr int HU = 2;
     for (; i + (HU - 1) * stride < m; i += HU * stride) {
         unsigned long long u[HU], v[HU];
         bool ok[HU];
