@@ -24,7 +24,6 @@ validated exactly like ``vkm.Machine`` (vkm.py:434-454) and recorded in
 import ctypes
 import functools
 import math
-import threading
 from collections import namedtuple
 from dataclasses import dataclass
 
@@ -153,13 +152,15 @@ def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=
                 r = len(spl_nodes)
                 idx = _device_index(spl_nodes, dev, key)
                 res = torch.empty((3, r), dtype=torch.int64, device=dev)
-                host = _pinned_meta(3 * r)
+                # a fresh block from torch's caching pinned allocator: the result
+                # array is a view of it (no 3r-element copy on the call's tail)
+                host = torch.empty(3 * r, dtype=torch.int64, pin_memory=True)
                 mws = _device.workspace(L.sg_splitter_meta_workspace_bytes(r), dev)
                 rc = L.sg_rs_rank_meta(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
                                        _device.ptr(ws), ws.numel(), _device.ptr(idx), r, _device.ptr(res),
                                        ctypes.c_void_p(host.data_ptr()), _device.ptr(mws), mws.numel(), stream,
                                        ctypes.byref(st), ctypes.byref(viol))
-                meta_out.append(host[:3 * r].numpy().reshape(3, r).copy())
+                meta_out.append(host.numpy().reshape(3, r))
         del ws
     if rc not in (_native.SG_OK, _native.SG_ERR_INVALID_LIST):
         _native.check(rc, f"sg_{kind}_rank")
@@ -240,17 +241,6 @@ def _draw_splitters_cached(n, r, seed):
 
 
 _IDX_CACHE = {}
-_PINNED = threading.local()
-
-
-def _pinned_meta(count):
-    """Reused pinned host staging for the splitter meta, one per host thread
-    (the contents are copied out before the call returns)."""
-    buf = getattr(_PINNED, "meta", None)
-    if buf is None or buf.numel() < count:
-        buf = torch.empty(max(count, 3 * 16384), dtype=torch.int64, pin_memory=True)
-        _PINNED.meta = buf
-    return buf
 
 
 def _device_index(spl_nodes, dev, key):
