@@ -286,7 +286,10 @@ __device__ __forceinline__ int part_of(E edges, unsigned long long e, unsigned l
 // partition sizes: persistent CTAs; per 32 edges a warp takes five ballots
 // (valid + 4 partition bits) and lane p keeps partition p's count in a
 // register; one atomic per partition per CTA at the end.  Validates rows.
-template <class E, int NB>  // NB = ceil(log2 P) partition bits (ballots per edge)
+// NB = ceil(log2 P) partition bits (ballots per edge); kNarrow: 32-bit ids
+// (u32 edges, or int32 edges with n <= 2^31, where a negative id reads as
+// >= 2^31 >= n), so the checks run in 32-bit
+template <class E, int NB, bool kNarrow>
 __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigned long long m, unsigned long long n,
                                                                 unsigned long long row0,
                                                                 uint32_t shift, int P,
@@ -316,9 +319,11 @@ __global__ void __launch_bounds__(PART_THREADS) k_cc_part_count(E edges, unsigne
                 const unsigned long long e = e0 + (unsigned long long)j * PART_THREADS;
                 bool ok = false;
                 if (e < m) {
-                    if (uu[j] >= n || vv[j] >= n)
+                    const bool oob = kNarrow ? ((uint32_t)uu[j] >= (uint32_t)n || (uint32_t)vv[j] >= (uint32_t)n)
+                                             : (uu[j] >= n || vv[j] >= n);
+                    if (oob)
                         atomicMax(flags + 1, ~(row0 + e));
-                    else if (uu[j] == vv[j])
+                    else if ((uint32_t)uu[j] == (uint32_t)vv[j])
                         atomicMax(flags + 2, ~(row0 + e));
                     else
                         ok = true;
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_cc_part_scatter(E edges, unsi
 // streams into shared memory while the current one is split.
 constexpr int PART2_CTAS_PER_SM = 2;
 
-template <class E, int NB>
+template <class E, int NB, bool kNarrow>  // kNarrow: as in k_cc_part_count
 __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatter2(
     E edges, unsigned long long m, unsigned long long n, uint32_t shift, int P,
     const unsigned long long* __restrict__ off_part, unsigned long long* __restrict__ cursor, uint2* __restrict__ out) {
@@ -435,7 +440,8 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
                 E::decode(stage, e, u, v);
             else if (e < cnt)
                 edges.load(e0 + e, u, v);  // the odd tail element of the last tile
-            const bool ok = u < n && v < n && u != v;
+            const bool ok = kNarrow ? ((uint32_t)u < (uint32_t)n && (uint32_t)v < (uint32_t)n && (uint32_t)u != (uint32_t)v)
+                                    : (u < n && v < n && u != v);
             pr[j] = ((unsigned long long)(uint32_t)v << 32) | (uint32_t)u;
             bn[j] = ok ? max((uint32_t)u, (uint32_t)v) >> shift : (uint32_t)MS_MAXB;
         }
@@ -559,16 +565,25 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
     const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
     int nbits = 0;
     while ((1 << nbits) < p.parts) ++nbits;
-    auto kc = nbits <= 1 ? k_cc_part_count<E, 1>
-            : nbits == 2 ? k_cc_part_count<E, 2> : nbits == 3 ? k_cc_part_count<E, 3> : k_cc_part_count<E, 4>;
+    const bool narrow = E::kBytes == 8 && n <= 0x80000000ull;  // (u32 ids are < 2^32 - 1 = n's cap anyway)
+    auto kc = narrow ? (nbits <= 1 ? k_cc_part_count<E, 1, true>
+                        : nbits == 2 ? k_cc_part_count<E, 2, true>
+                        : nbits == 3 ? k_cc_part_count<E, 3, true> : k_cc_part_count<E, 4, true>)
+                     : (nbits <= 1 ? k_cc_part_count<E, 1, false>
+                        : nbits == 2 ? k_cc_part_count<E, 2, false>
+                        : nbits == 3 ? k_cc_part_count<E, 3, false> : k_cc_part_count<E, 4, false>);
     kc<<<cg, PART_THREADS, 0, s>>>(view, m, n, row0, p.shift, p.parts, b.totals, flags);
     SG_LAUNCH_CHECK();
     k_cc_part_offsets<<<1, 32, 0, s>>>(b.totals, p.parts, b.off_part);
     SG_LAUNCH_CHECK();
     if (((uintptr_t)view.e & 15) == 0) {
         const size_t smem = (size_t)MS2_TILE * E::kBytes + MsSmem::bytes((uint32_t)p.parts, MS2_TILE);
-        auto ks = nbits <= 1 ? k_cc_part_scatter2<E, 1>
-                : nbits == 2 ? k_cc_part_scatter2<E, 2> : nbits == 3 ? k_cc_part_scatter2<E, 3> : k_cc_part_scatter2<E, 4>;
+        auto ks = narrow ? (nbits <= 1 ? k_cc_part_scatter2<E, 1, true>
+                            : nbits == 2 ? k_cc_part_scatter2<E, 2, true>
+                            : nbits == 3 ? k_cc_part_scatter2<E, 3, true> : k_cc_part_scatter2<E, 4, true>)
+                         : (nbits <= 1 ? k_cc_part_scatter2<E, 1, false>
+                            : nbits == 2 ? k_cc_part_scatter2<E, 2, false>
+                            : nbits == 3 ? k_cc_part_scatter2<E, 3, false> : k_cc_part_scatter2<E, 4, false>);
         SG_CUDA(set_smem_max(ks, smem));
         const unsigned long long ntile = (m + MS2_TILE - 1) / MS2_TILE;
         const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * PART2_CTAS_PER_SM ? ntile
