@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count(const SuccT* __restri
 // and in-tile chain ends per tile (nodes whose successor leaves the tile, or
 // the tail): the segment count of the tile contraction below.  Full tiles
 // are read with 16-B vector loads; node ids are 32-bit (n < 2^32 - 1).
-template <class SuccT, bool kVec>
+// kNarrow: 32-bit range check (u32 ids, or int32 ids with n <= 2^31, where a
+// negative id reads as >= 2^31 >= n)
+template <class SuccT, bool kVec, bool kNarrow>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restrict__ succ,
                                                             uint32_t* __restrict__ tile_cnt,
                                                             uint32_t* __restrict__ tile_end, ListStatus* st,
@@ -333,7 +335,8 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
                     if (full || base + l < N) {
                         const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
                         const uint32_t i = (uint32_t)base + l, x = (uint32_t)x64;
-                        const bool oor = x64 >= N, self = !oor && x == i;
+                        const bool oor = kNarrow ? x >= (uint32_t)N : x64 >= N;
+                        const bool self = !oor && x == i;
                         if (oor | self) note_succ(st, i, x64, N);
                         packed += (is_ruler(i, kbits, salt) ? 0x10000u : 0u) +
                                   ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
@@ -1925,12 +1928,11 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             const uint32_t cw = (nt + TILE_THREADS / 32 - 1) / (TILE_THREADS / 32);  // one warp per tile
             const uint32_t cg = cw < kSMs * 8 ? cw : kSMs * 8;
             rec.begin(K_RS_COUNT, 0, cg, TILE_THREADS, capN);
-            if (((uintptr_t)succ & 15) == 0)
-                k_rs_count0<SuccT, true><<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0],
-                                                                      p.salt[0]);
-            else
-                k_rs_count0<SuccT, false><<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0],
-                                                                       p.salt[0]);
+            const bool narrow = sizeof(SuccT) == 4 && n <= 0x80000000ull;
+            const bool vec = ((uintptr_t)succ & 15) == 0;
+            auto kc = vec ? (narrow ? k_rs_count0<SuccT, true, true> : k_rs_count0<SuccT, true, false>)
+                          : (narrow ? k_rs_count0<SuccT, false, true> : k_rs_count0<SuccT, false, false>);
+            kc<<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0], p.salt[0]);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
             k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, tk, b.st, k, p.kbits[k], p.salt[k], 1);
