@@ -121,10 +121,13 @@ typedef struct sg_violation {
 const char* sg_strerror(int status);
 const char* sg_kernel_name(int kernel_id);
 int sg_version(void);
+/* sha256 (hex, ';'-terminated) of the sources, headers and nvcc flags this
+ * library was built from (paper_1002_4482_b200/build.py). */
+const char* sg_source_hash(void);
 /* Fill launch[k].ms and total_ms of a finished call.  Calls return without
  * reading their CUDA events (that costs ~3 us per launch of host time after
  * the pipeline's last kernel); the events of one call stay valid for the
- * next 15 calls on the device.  SG_ERR_RUNTIME: recycled (ms stay 0). */
+ * next 63 calls on the device.  SG_ERR_RUNTIME: recycled (ms stay 0). */
 int sg_stats_resolve(sg_stats* st);
 /* last CUDA error string seen by this thread (for SG_ERR_CUDA) */
 const char* sg_last_cuda_error(void);

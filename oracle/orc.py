@@ -30,7 +30,7 @@ def build(force=False):
     """Compile liborc.so with gcc (no CUDA involved)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         tmp = LIB + ".tmp"
-        subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-pthread", "-o", tmp, SRC], check=True)
+        subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-o", tmp, SRC], check=True)
         os.replace(tmp, LIB)
     return LIB
 
@@ -54,10 +54,12 @@ def lib():
         L.orc_seq_components.argtypes = [I64, P, I64, P, P]
         L.orc_validate_graph.argtypes = [I64, P, I64, P]
         L.orc_validate_graph.restype = ctypes.c_int
-        L.orc_rank_walk_sample.argtypes = [P, I64, P, I64, ctypes.c_int]
-        L.orc_rank_walk_sample.restype = I64
-        L.orc_uf_sample.argtypes = [I64, P, I64, I64, P, P, P, P]
-        L.orc_uf_sample.restype = I64
+        L.orc_gen_list.argtypes = [I64, P, P]
+        L.orc_gen_list.restype = ctypes.c_int
+        L.orc_gen_random_graph.argtypes = [I64, I64, P, P]
+        L.orc_gen_random_graph.restype = ctypes.c_int
+        L.orc_seq_rank_sample.argtypes = [P, I64, P, P, I64, I64, P]
+        L.orc_seq_rank_sample.restype = I64
         _lib = L
     return _lib
 
@@ -167,8 +169,39 @@ def kiss_batch(state, n):
     return out, tuple(int(v) for v in st)
 
 
+def _state(seed):
+    return np.array(kiss_seed(seed), dtype=np.uint64)
+
+
 def gen_list(n, seed=0):
-    """gen.py:110-127: chain visiting interior nodes in KISS sort-key order."""
+    """gen.py:110-127: chain visiting interior nodes in KISS sort-key order
+    (orc.c: KISS batch + stable LSD radix argsort)."""
+    n = int(n)
+    assert 1 <= n < (1 << 32)
+    succ = np.empty(n, dtype=np.int64)
+    st = _state(seed)
+    if lib().orc_gen_list(n, st.ctypes.data, succ.ctypes.data):
+        raise MemoryError("orc_gen_list: allocation failed")
+    return succ
+
+
+def gen_random_graph(n, d, seed=0):
+    """gen.py:183-218 -> int64 (m,2) edges, rows sorted, u < v (orc.c:
+    draw-order rejection sampling with a hash set, then a radix sort)."""
+    n = int(n)
+    cap = n * (n - 1) // 2
+    m = int(round(d * cap))
+    if not 0 < d <= 1 or m > cap:
+        raise ValueError(f"density {d} out of range")
+    edges = np.empty((m, 2), dtype=np.int64)
+    st = _state(seed)
+    if lib().orc_gen_random_graph(n, m, st.ctypes.data, edges.ctypes.data):
+        raise MemoryError("orc_gen_random_graph: allocation failed")
+    return edges
+
+
+def gen_list_np(n, seed=0):
+    """numpy restatement of gen.py:110-127 (cross-check of the C generator)."""
     succ = np.empty(n, dtype=np.int64)
     if n == 1:
         succ[0] = 0
@@ -180,8 +213,8 @@ def gen_list(n, seed=0):
     return succ
 
 
-def gen_random_graph(n, d, seed=0):
-    """gen.py:183-218 -> int64 (m,2) edges, rows sorted, u < v."""
+def gen_random_graph_np(n, d, seed=0):
+    """numpy restatement of gen.py:183-218 (cross-check of the C generator)."""
     cap = n * (n - 1) // 2
     m = int(round(d * cap))
     state = kiss_seed(seed)
@@ -245,24 +278,25 @@ def splitter_set(succ, splitter_node):
     return sub_len, red, sr
 
 
-# ---- CPU-baseline samples ----------------------------------------------------
+# ---- CPU-baseline timing -----------------------------------------------------
 
-def rank_walk_sample(succ, hops, threads):
-    """Run seq_rank's two dependent walks (core.py:164, :175) from `threads`
-    start nodes for <= `hops` hops each; returns hops walked per pass."""
-    succ = _i64(succ)
-    pos = np.empty(succ.shape[0], dtype=np.int64)
-    return int(lib().orc_rank_walk_sample(succ.ctypes.data, succ.shape[0], pos.ctypes.data, int(hops),
-                                          int(threads)))
+class SeqRankSampler:
+    """Bounded samples of seq_rank (core.py:179-186) on a full-size list:
+    each call ranks the first `hops` nodes of the chain with seq_rank's
+    per-node work (both dependent walks over the n-sized arrays, the scans
+    and the rank fill; orc.c orc_seq_rank_sample)."""
 
+    def __init__(self, succ):
+        self.succ = _i64(succ)
+        n = self.succ.shape[0]
+        self.pos = np.zeros(n, dtype=np.int64)
+        self.rank = np.empty(n, dtype=np.int64)
+        self.pos.fill(0)            # fault the pages in outside any timed sample
+        self.rank.fill(0)
+        self.epoch = 0
 
-def uf_sample(n, edges, stride):
-    """Union-find over every stride-th edge + full labelling pass
-    (core.py:209-237); returns (edges used, t_union s, t_label s)."""
-    e = _i64(edges).reshape(-1, 2)
-    parent = np.empty(n, dtype=np.int64)
-    label = np.empty(n, dtype=np.int64)
-    tu, tl = ctypes.c_double(), ctypes.c_double()
-    used = lib().orc_uf_sample(int(n), e.ctypes.data, e.shape[0], int(stride), parent.ctypes.data,
-                               label.ctypes.data, ctypes.byref(tu), ctypes.byref(tl))
-    return int(used), tu.value, tl.value
+    def __call__(self, hops):
+        self.epoch += 1
+        an = ctypes.c_int64()
+        return int(lib().orc_seq_rank_sample(self.succ.ctypes.data, self.succ.shape[0], self.pos.ctypes.data,
+                                             self.rank.ctypes.data, int(hops), self.epoch, ctypes.byref(an)))

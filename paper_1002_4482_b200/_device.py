@@ -66,23 +66,26 @@ def exec_stats(st):
 
     def resolve():  # event times are read on first use (sg_stats_resolve)
         if not resolved:
-            _native.lib().sg_stats_resolve(ctypes.byref(st))
-            resolved.append(True)
+            rc = _native.lib().sg_stats_resolve(ctypes.byref(st))
+            resolved.append(rc == _native.SG_OK)
+            if rc != _native.SG_OK:
+                es.warnings.append("launch timings unavailable: this call's CUDA events were recycled "
+                                   "(read ExecStats timings within 64 calls on the device)")
+        return resolved[0]
 
     def build():  # `st` is this call's own sg_stats, kept alive by the closure
-        resolve()
+        ok = resolve()
         out = []
         for k in range(nl):
             L = st.launch[k]
-            ms = float(L.ms)
+            ms = float(L.ms) if ok else float("nan")  # unavailable, see es.warnings
             out.append(LaunchRecord(kernel=_native.kernel_name(L.kernel),
                                     counters=KernelCounters(launches=1, items=int(L.items), ms=ms),
                                     round=int(L.round), blocks=int(L.blocks), threads=int(L.threads), ms=ms))
         return out
 
     def wall():
-        resolve()
-        return float(st.total_ms) / 1e3
+        return float(st.total_ms) / 1e3 if resolve() else None
 
     es.set_launch_log_source(build)
     es.set_wall_time_source(wall)

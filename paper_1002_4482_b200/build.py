@@ -4,6 +4,7 @@ The library is built next to this file so it travels with the repository
 snapshot to the GPU box; nothing is installed into site-packages.
 """
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -28,31 +29,74 @@ def _nvcc():
     return cand
 
 
-def _stale(target, deps):
-    if not os.path.exists(target):
-        return True
-    t = os.path.getmtime(target)
-    return any(os.path.getmtime(d) > t for d in deps)
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3"]
+LINK = ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+MARKER = b"SG_SOURCE_HASH="
 
 
 def _deps(src):
-    heads = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    return [os.path.join(CSRC, src), os.path.join(INCLUDE, "sg.h"), __file__] + heads
+    heads = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+    return [os.path.join(CSRC, src), os.path.join(INCLUDE, "sg.h")] + heads
+
+
+def _digest(paths, extra):
+    h = hashlib.sha256()
+    for p in paths:
+        h.update(os.path.basename(p).encode() + b"\0")
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(extra).encode())
+    return h.hexdigest()
+
+
+def source_hash():
+    """sha256 over every source, header and flag libsg.so is built from."""
+    paths = [os.path.join(CSRC, s) for s in SOURCES]
+    paths += sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+    paths.append(os.path.join(INCLUDE, "sg.h"))
+    return _digest(paths, ARCH + FLAGS + LINK)
+
+
+def embedded_hash(path=LIB):
+    """The source hash compiled into a built library, or None."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        return None
+    i = data.find(MARKER)
+    if i < 0:
+        return None
+    j = data.find(b";", i)
+    return data[i + len(MARKER):j].decode(errors="replace")
 
 
 def build_native(force=False, verbose=False):
-    """Compile every csrc source for sm_100a and link libsg.so; returns its path."""
+    """Compile every csrc source for sm_100a and link libsg.so; returns its
+    path.  A library (or object) is reused only when the source hash
+    embedded in it (object: its sidecar) equals the tree's -- a shipped
+    binary built from other sources is rebuilt, whatever its mtime."""
     os.makedirs(BUILD, exist_ok=True)
+    want = source_hash()
+    if not force and embedded_hash() == want:
+        return LIB
     nvcc = _nvcc()
     objs = []
     jobs = []
     for src in SOURCES:
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
-        if force or _stale(obj, _deps(src)):
-            cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                   "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
-            jobs.append(cmd)
+        defs = [f"-DSG_SOURCE_HASH=\"{want}\""] if src == "sg_runtime.cu" else []
+        cmd = [nvcc, *ARCH, *FLAGS, *defs, "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+        sidecar = obj + ".sha256"
+        key = _digest(_deps(src), cmd[1:-3])
+        try:
+            with open(sidecar) as f:
+                fresh = f.read().strip() == key and os.path.exists(obj)
+        except OSError:
+            fresh = False
+        if force or not fresh:
+            jobs.append((cmd, sidecar, key))
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,13 +105,19 @@ def build_native(force=False, verbose=False):
         if verbose and (r.stdout or r.stderr):
             sys.stderr.write(r.stdout + r.stderr)
 
-    with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
-        list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        tmp = LIB + ".tmp"
-        cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    def compile_one(job):
+        cmd, sidecar, key = job
         run(cmd)
-        os.replace(tmp, LIB)
+        with open(sidecar, "w") as f:
+            f.write(key)
+
+    with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
+        list(ex.map(compile_one, jobs))
+    tmp = LIB + ".tmp"
+    run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, *LINK])
+    os.replace(tmp, LIB)
+    if embedded_hash() != want:
+        raise RuntimeError("libsg.so does not carry the expected source hash after the build")
     return LIB
 
 

@@ -452,6 +452,180 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
 }
 
 // ---------------------------------------------------------------------------
+// One-pass partition: a tile-local sort by window.
+//
+// Tile t (TT = MS2_TILE edges) is staged into shared memory by a bulk copy,
+// validated (first bad global row, core.py:196-206), ranked by window with
+// the ballot peer ranking of sg_msplit.cuh, sorted in shared memory and
+// written back to ITS OWN slot range [t*TT, (t+1)*TT) of the copy, with the
+// P+1 window offsets of the tile in toff[t].  No count pass and no global
+// atomics: every edge is read once and written once.  The hook of window k
+// then walks the k-th slice of every tile, tiles in order, so the edge order
+// inside a window is the stable partition's.
+constexpr int TP_CTAS_PER_SM = 2;
+
+template <class E, int NB, bool kNarrow>
+__global__ void __launch_bounds__(MS_THREADS, TP_CTAS_PER_SM) k_cc_part_tiles(
+    E edges, unsigned long long m, unsigned long long n, unsigned long long row0, uint32_t shift, int P,
+    uint32_t* __restrict__ toff, uint2* __restrict__ out, unsigned long long* flags) {
+    extern __shared__ __align__(128) unsigned char ms_raw[];
+    unsigned char* stage = ms_raw;
+    unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(ms_raw + MS2_TILE * E::kBytes);
+    __shared__ uint32_t s_w[MS_WARPS][MAX_PARTS];   // per-warp counts, then per-warp offsets
+    __shared__ uint32_t s_start[MAX_PARTS + 1];
+    __shared__ unsigned long long bar;
+    const unsigned long long ntiles = (m + MS2_TILE - 1) / MS2_TILE;
+    const uint32_t lane = lane_id();
+    const int w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    auto issue = [&](unsigned long long tile) {
+        if (threadIdx.x == 0 && tile < ntiles) {
+            const unsigned long long e0 = tile * MS2_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, m - e0);
+            const uint32_t full = cnt * E::kBytes & ~15u;
+            if (full) {
+                mbar_expect_tx(&bar, full);
+                bulk_g2s_hint(stage, reinterpret_cast<const unsigned char*>(edges.e) + e0 * E::kBytes, full, &bar,
+                              l2_evict_first());
+            } else {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
+            }
+        }
+    };
+    uint32_t phase = 0;
+    issue(blockIdx.x);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long e0 = tile * MS2_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, m - e0);
+        const uint32_t staged = (cnt * E::kBytes & ~15u) / E::kBytes;
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        if (lane < MAX_PARTS) s_w[w][lane] = 0;
+        unsigned long long pr[MS2_ITEMS];
+        uint32_t bn[MS2_ITEMS];
+#pragma unroll
+        for (int j = 0; j < MS2_ITEMS; ++j) {
+            const uint32_t e = j * MS_THREADS + threadIdx.x;
+            unsigned long long u = n, v = n;
+            if (e < staged)
+                E::decode(stage, e, u, v);
+            else if (e < cnt)
+                edges.load(e0 + e, u, v);  // the odd tail element of the last tile
+            bool ok = false;
+            if (e < cnt) {
+                const bool oob = kNarrow ? ((uint32_t)u >= (uint32_t)n || (uint32_t)v >= (uint32_t)n)
+                                         : (u >= n || v >= n);
+                if (oob)
+                    atomicMax(flags + 1, ~(row0 + e0 + e));
+                else if ((uint32_t)u == (uint32_t)v)
+                    atomicMax(flags + 2, ~(row0 + e0 + e));
+                else
+                    ok = true;
+            }
+            pr[j] = ((unsigned long long)(uint32_t)v << 32) | (uint32_t)u;
+            bn[j] = ok ? max((uint32_t)u, (uint32_t)v) >> shift : (uint32_t)MS_MAXB;
+        }
+        __syncthreads();  // staging consumed (and s_w zeroed): refill it behind the sort
+        issue(tile + gridDim.x);
+        uint32_t rk[MS2_ITEMS];
+#pragma unroll
+        for (int j = 0; j < MS2_ITEMS; ++j) {
+            const bool valid = bn[j] < (uint32_t)P;
+            const unsigned vb = __ballot_sync(0xffffffffu, valid);
+            unsigned peers = valid ? vb : ~vb;
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
+                peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+            }
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (valid && (int)lane == leader) {
+                old = s_w[w][bn[j]];
+                s_w[w][bn[j]] = old + __popc(peers);
+            }
+            rk[j] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
+        }
+        __syncthreads();
+        if (w == 0) {  // bin totals, warp offsets and tile offsets: one warp, P <= 16 bins
+            uint32_t acc = 0;
+            if (lane < (uint32_t)P) {
+#pragma unroll
+                for (int k = 0; k < MS_WARPS; ++k) {
+                    const uint32_t c = s_w[k][lane];
+                    s_w[k][lane] = acc;
+                    acc += c;
+                }
+            }
+            uint32_t incl = acc;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += v;
+            }
+            if (lane < (uint32_t)P) s_start[lane] = incl - acc;
+            if (lane == (uint32_t)P - 1) s_start[P] = incl;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < MS2_ITEMS; ++j)
+            if (bn[j] < (uint32_t)P) sbuf[s_start[bn[j]] + s_w[w][bn[j]] + rk[j]] = pr[j];
+        if (threadIdx.x <= (uint32_t)P) toff[tile * (MAX_PARTS + 1) + threadIdx.x] = s_start[threadIdx.x];
+        __syncthreads();
+        const uint32_t total = s_start[P];
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(out) + e0;
+        const ulonglong2* src2 = reinterpret_cast<const ulonglong2*>(sbuf);
+        for (uint32_t i = threadIdx.x; i < total / 2; i += MS_THREADS)
+            __stcs(reinterpret_cast<ulonglong2*>(dst) + i, src2[i]);
+        if ((total & 1u) && threadIdx.x == 0) __stcs(dst + total - 1, sbuf[total - 1]);
+        __syncthreads();  // sbuf and s_start are reused by the next tile
+    }
+}
+
+// hook of window k over the tile-sorted copy: CTAs take tiles in order and
+// hook the tile's k-th slice (HU edges per thread in flight)
+template <bool kUF>
+__global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_tiles(const uint2* __restrict__ edges,
+                                                                const uint32_t* __restrict__ toff,
+                                                                unsigned long long ntiles, int k, uint32_t* D,
+                                                                unsigned long long* flags) {
+    bool any = false;
+    constexpr int HU = 2;
+    for (unsigned long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t lo = __ldg(toff + t * (MAX_PARTS + 1) + k), hi = __ldg(toff + t * (MAX_PARTS + 1) + k + 1);
+        const uint2* te = edges + t * MS2_TILE;
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += HU * HOOK_THREADS) {
+            uint2 uv[HU];
+            bool ok[HU];
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                ok[q] = i + q * HOOK_THREADS < hi;
+                uv[q] = ok[q] ? __ldcs(te + i + q * HOOK_THREADS) : make_uint2(0, 0);
+            }
+            uint32_t pu[HU], pv[HU];
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                pu[q] = ok[q] ? ld_parent(D + uv[q].x) : 0;
+                pv[q] = ok[q] ? ld_parent(D + uv[q].y) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                if (!ok[q] || pu[q] == pv[q]) continue;
+                if (kUF) {
+                    any |= unite(D, uv[q].x, pu[q], uv[q].y, pv[q]);
+                } else {
+                    const uint32_t hi2 = pu[q] > pv[q] ? pu[q] : pv[q];
+                    const uint32_t lo2 = pu[q] > pv[q] ? pv[q] : pu[q];
+                    if (atomicMin(D + hi2, lo2) > lo2) any = true;
+                }
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, any) && lane_id() == 0) flags[0] = 1ull;
+}
+
+// ---------------------------------------------------------------------------
 // sparse merge of the sharded rounds (dist.py): after the dense merge of
 // round 1 every replica is identical, so later rounds only exchange the
 // entries a rank's hook sweep lowered
@@ -553,13 +727,47 @@ struct CcPartBufs {
     unsigned long long* totals = nullptr;   // [MAX_PARTS]
     unsigned long long* cursor = nullptr;   // [MAX_PARTS]
     unsigned long long* off_part = nullptr; // [MAX_PARTS + 2]
+    uint32_t* toff = nullptr;               // [tiles][MAX_PARTS + 1] (one-pass tile sort)
     uint2* edges = nullptr;
+    bool tiled = false;                     // which layout partition_edges produced
 };
+
+static unsigned long long part_tiles(unsigned long long m) { return (m + MS2_TILE - 1) / MS2_TILE; }
+
+// partition mode: 1 = one-pass tile sort (default), 0 = count + scatter (SG_CC_PART=2pass)
+static bool part_one_pass() {
+    const char* e = getenv("SG_CC_PART");
+    return !(e && strcmp(e, "2pass") == 0);
+}
+// the one-pass layout needs 16-B aligned input rows (bulk copies); a reused
+// partition (sg_cc_hook_part, reuse = 1) re-derives its layout from this
+static bool use_tiles(const void* edges) { return part_one_pass() && ((uintptr_t)edges & 15) == 0; }
 
 template <class E>
 static int partition_edges(E view, unsigned long long m, unsigned long long n, const CcPlan& p, CcPartBufs& b,
                            unsigned long long* flags, cudaStream_t s, unsigned long long row0 = 0) {
     const uint32_t nt = (uint32_t)p.ntiles;
+    b.tiled = false;
+    if (use_tiles(view.e)) {
+        int nbits = 0;
+        while ((1 << nbits) < p.parts) ++nbits;
+        const bool narrow = E::kBytes == 8 && n <= 0x80000000ull;
+        auto kt = narrow ? (nbits <= 1 ? k_cc_part_tiles<E, 1, true>
+                            : nbits == 2 ? k_cc_part_tiles<E, 2, true>
+                            : nbits == 3 ? k_cc_part_tiles<E, 3, true> : k_cc_part_tiles<E, 4, true>)
+                         : (nbits <= 1 ? k_cc_part_tiles<E, 1, false>
+                            : nbits == 2 ? k_cc_part_tiles<E, 2, false>
+                            : nbits == 3 ? k_cc_part_tiles<E, 3, false> : k_cc_part_tiles<E, 4, false>);
+        const size_t smem = (size_t)MS2_TILE * E::kBytes + (size_t)MS2_TILE * 8;
+        SG_CUDA(set_smem_max(kt, smem));
+        const unsigned long long ntile = part_tiles(m);
+        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * TP_CTAS_PER_SM ? ntile
+                                                                                         : kSMs * TP_CTAS_PER_SM);
+        kt<<<ns, MS_THREADS, smem, s>>>(view, m, n, row0, p.shift, p.parts, b.toff, b.edges, flags);
+        SG_LAUNCH_CHECK();
+        b.tiled = true;
+        return SG_OK;
+    }
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
@@ -613,6 +821,18 @@ static int partition_dispatch(const void* edges, int dt, unsigned long long m, u
 // one hook sweep over a partitioned edge list, window by window
 static int hook_partitions(const CcPlan& p, const CcPartBufs& b, unsigned long long m, unsigned long long n,
                            uint32_t* D, int variant, unsigned long long* flags, cudaStream_t s) {
+    if (b.tiled) {
+        const unsigned long long nt = part_tiles(m);
+        const uint32_t g = (uint32_t)(nt < (unsigned long long)kSMs * 8 ? nt : kSMs * 8);
+        for (int k = 0; k < p.parts; ++k) {
+            if (variant == SG_CC_UF)
+                k_cc_hook_tiles<true><<<g, HOOK_THREADS, 0, s>>>(b.edges, b.toff, nt, k, D, flags);
+            else
+                k_cc_hook_tiles<false><<<g, HOOK_THREADS, 0, s>>>(b.edges, b.toff, nt, k, D, flags);
+            SG_LAUNCH_CHECK();
+        }
+        return SG_OK;
+    }
     const unsigned long long per = m / p.parts + 1;
     for (int k = 0; k < p.parts; ++k) {
         int rc = launch_hook(EdgesU32{b.edges}, per, 0, n, D, variant, false, flags, s, b.off_part + k);
@@ -689,6 +909,7 @@ static bool carve_cc(Carver& c, uint64_t n, uint64_t m, const CcPlan& p, unsigne
         b.totals = c.take<unsigned long long>(MAX_PARTS);
         b.cursor = c.take<unsigned long long>(MAX_PARTS);
         b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+        b.toff = c.take<uint32_t>((size_t)part_tiles(m) * (MAX_PARTS + 1));
         b.edges = c.take<uint2>(m);
     }
     return c.ok;
@@ -843,6 +1064,7 @@ size_t sg_cc_hook_workspace_bytes(uint64_t n, uint64_t m) {
     b.totals = c.take<unsigned long long>(MAX_PARTS);
     b.cursor = c.take<unsigned long long>(MAX_PARTS);
     b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+    b.toff = c.take<uint32_t>((size_t)part_tiles(m) * (MAX_PARTS + 1));
     b.edges = c.take<uint2>(m);
     return c.off + 256;
 }
@@ -860,9 +1082,11 @@ int sg_cc_hook_part(const void* edges, int edge_dtype, uint64_t m, uint64_t row0
     b.totals = c.take<unsigned long long>(MAX_PARTS);
     b.cursor = c.take<unsigned long long>(MAX_PARTS);
     b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+    b.toff = c.take<uint32_t>((size_t)part_tiles(m) * (MAX_PARTS + 1));
     b.edges = c.take<uint2>(m);
     if (!c.ok) return SG_ERR_WORKSPACE;
-    if (!reuse) {  // rows are validated while they are counted (flags hold ~global row)
+    b.tiled = use_tiles(edges);
+    if (!reuse) {  // rows are validated while they are partitioned (flags hold ~global row)
         int rc = partition_dispatch(edges, edge_dtype, m, n, p, b, (unsigned long long*)flags, s, row0);
         if (rc != SG_OK) return rc;
     }

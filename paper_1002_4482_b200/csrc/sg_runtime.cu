@@ -24,7 +24,7 @@ void set_cuda_error(cudaError_t e) {
 // of host time, which would otherwise sit between the pipeline's last kernel
 // and the call's return.  A set is recycled kSets calls later; stats resolved
 // after that report SG_ERR_RUNTIME and keep ms = 0.
-constexpr int kSets = 16;
+constexpr int kSets = 64;
 struct EventSet {
     std::vector<cudaEvent_t> ev;
     uint32_t gen = 0;
@@ -34,9 +34,10 @@ static EventSet g_sets[64][kSets];
 static uint32_t g_next_set[64];
 static uint32_t g_gen = 0;
 
-// ticket: dev (6 bits) | set (4 bits) | generation (22 bits, never 0)
+// ticket: dev (6 bits) | set (6 bits) | generation (20 bits, never 0)
+constexpr uint32_t kGenMask = 0xFFFFFu;
 static inline uint32_t make_ticket(int dev, int set, uint32_t gen) {
-    return ((uint32_t)(dev & 63) << 26) | ((uint32_t)set << 22) | (gen & 0x3FFFFFu);
+    return ((uint32_t)(dev & 63) << 26) | ((uint32_t)set << 20) | (gen & kGenMask);
 }
 
 cudaEvent_t Recorder::event(size_t i) {
@@ -59,8 +60,8 @@ Recorder::Recorder(sg_stats* st, cudaStream_t s) : st_(st), s_(s) {
         {
             std::lock_guard<std::mutex> lk(g_sets_mu);
             const int k = (int)(g_next_set[dev & 63]++ % kSets);
-            uint32_t gen = ++g_gen & 0x3FFFFFu;
-            if (gen == 0) gen = ++g_gen & 0x3FFFFFu;
+            uint32_t gen = ++g_gen & kGenMask;
+            if (gen == 0) gen = ++g_gen & kGenMask;
             EventSet& es = g_sets[dev & 63][k];
             es.gen = gen;
             set_ = &es;
@@ -121,8 +122,8 @@ extern "C" int sg_stats_resolve(sg_stats* st) {
     if (!st) return SG_ERR_VALUE;
     if (st->n_launches == 0) return SG_OK;
     const uint32_t t = st->pad2;
-    const int dev = (int)(t >> 26), k = (int)((t >> 22) & 15u);
-    const uint32_t gen = t & 0x3FFFFFu;
+    const int dev = (int)(t >> 26), k = (int)((t >> 20) & 63u);
+    const uint32_t gen = t & kGenMask;
     std::lock_guard<std::mutex> lk(g_sets_mu);
     EventSet& es = g_sets[dev][k];
     if (gen == 0 || es.gen != gen) return SG_ERR_RUNTIME;  // the event set was recycled
@@ -199,6 +200,16 @@ const char* sg_kernel_name(int id) {
 }
 
 int sg_version(void) { return 1; }
+
+#ifndef SG_SOURCE_HASH
+#define SG_SOURCE_HASH "unknown"
+#endif
+// build.py embeds the sha256 of every source, header and flag it compiled
+// from; it reads this marker back from the .so to decide whether a shipped
+// library matches the tree (no mtimes involved).
+__attribute__((used)) static const char g_source_hash_marker[] = "SG_SOURCE_HASH=" SG_SOURCE_HASH ";";
+
+const char* sg_source_hash(void) { return g_source_hash_marker + 15; }
 
 const char* sg_last_cuda_error(void) { return sg::g_last_cuda_error.c_str(); }
 

@@ -324,13 +324,18 @@ def test_c_abi_u32_path(cuda, orc):
     assert L.sg_stats_resolve(ctypes.byref(st)) == 0
     assert st.total_ms > 0 and all(st.launch[k].ms >= 0 for k in range(st.n_launches))
     assert abs(sum(st.launch[k].ms for k in range(st.n_launches)) - st.total_ms) < 0.05 * st.total_ms + 0.05
-    # a call's event set is recycled 16 calls later: resolving then reports it
+    # a call's event set is recycled 64 calls later: resolving then reports it
     st2 = _native.Stats()
     rc = L.sg_rs_rank(_device.ptr(succ), _native.SG_U32, _device.ptr(rank), _native.SG_U32, n, 0,
                       _device.ptr(ws), ws.numel(), _device.stream_ptr(cuda), ctypes.byref(st2), ctypes.byref(v))
-    for _ in range(16):
+    early = g.rs_rank(g.SuccessorList(succ), 64)[1]      # ExecStats not read yet
+    for _ in range(64):
         g.rs_rank(g.SuccessorList(succ), 64)
     assert L.sg_stats_resolve(ctypes.byref(st2)) == _native.SG_ERR_RUNTIME
+    # the Python layer reports it instead of returning zeros
+    assert early.wall_time is None
+    assert all(np.isnan(r.ms) for r in early.launch_log)
+    assert any("recycled" in w for w in early.warnings)
     assert st2.total_ms == 0
 
 

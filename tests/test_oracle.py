@@ -112,10 +112,31 @@ def test_validate_graph(orc):
     assert orc.validate_graph(3, [(0, 1), (2, 2)]) == ("self-loop", 1)
 
 
-def test_cpu_samples_run(orc):
+def test_c_generators_match_numpy_restatement(orc):
+    # the C generators (orc.c) against the numpy restatements of gen.py, on
+    # sizes / densities that force several rejection batches
+    for n, s in [(1, 0), (2, 5), (3, 1), (1000, 3), (65537, 9)]:
+        assert np.array_equal(orc.gen_list(n, s), orc.gen_list_np(n, s)), (n, s)
+    for n, d, s in [(2, 1.0, 0), (5, 1.0, 3), (40, 0.9, 1), (300, 0.3, 2), (5000, 0.001, 4)]:
+        assert np.array_equal(orc.gen_random_graph(n, d, s), orc.gen_random_graph_np(n, d, s)), (n, d, s)
+
+
+def test_generator_digests_match_reference(orc, hashes):
+    import hashlib
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+    assert sha(orc.gen_list(1 << 20, 0)) == hashes["gen_list_1048576_0"]
+    e = orc.gen_random_graph(1 << 16, (1 << 18) / ((1 << 16) * ((1 << 16) - 1) // 2), 0)
+    assert sha(e) == hashes["gen_random_graph_65536_262144_0"]
+    assert sha(orc.seq_components(1 << 16, e)) == hashes["seq_components_65536_262144_0"]
+
+
+def test_seq_rank_sampler(orc):
     succ = orc.gen_list(1 << 12, 0)
-    hops = orc.rank_walk_sample(succ, 100, 4)
-    assert 0 < hops <= 400
-    e = orc.gen_random_graph(1000, 0.01, 0)
-    used, tu, tl = orc.uf_sample(1000, e, 2)
-    assert used == (e.shape[0] + 1) // 2 and tu >= 0 and tl >= 0
+    smp = orc.SeqRankSampler(succ)
+    assert smp(100) == 100
+    assert smp(100) == 100          # a fresh epoch: nothing looks visited
+    assert smp(1 << 20) == (1 << 12) - 1   # the whole chain: n - 1 hops to the tail
+    assert np.array_equal(smp.rank, orc.seq_rank(succ))
