@@ -100,19 +100,31 @@ def sv_components(graph, p, backend="simulated", accounting="full", block_size=2
     return labels, stats
 
 
-RoundProfile = namedtuple("RoundProfile", ["rows", "hook_dominated"])
+RoundProfile = namedtuple("RoundProfile", ["rows", "sv23_read_dominated"])
+
+# global reads per item of each launch, the reference's counting rule
+# (concomp.py:249-271 sums ctx.read elements): a hook reads the stored edge
+# (2 ids) and both parents; the partition reads the edge; a shortcut or label
+# pass reads D[i] and D[D[i]]; collectives read nothing on the SMs
+_READS_PER_ITEM = {"cc_hook_uf": 4, "cc_hook_sv": 4, "cc_partition": 2, "cc_shortcut": 2, "cc_labels": 2}
 
 
 def round_profile(stats):
     """Per-launch table of a components run (concomp.py:249-271): round,
-    kernel, items and device ms; the flag says whether the hook sweeps
-    account for most of the device time."""
+    kernel, reads, writes, transactions (the reference's row keys; reads from
+    the per-item model above, writes and transactions live in ncu, 0 here),
+    plus items and device ms.  The flag says whether the hooking kernels
+    account for the majority of all global reads, as the reference's
+    ``sv23_read_dominated`` does for its SV2 + SV3."""
     rows = []
-    hook = other = 0.0
+    hook = other = 0
     for rec in stats.launch_log:
-        rows.append({"round": rec.round, "kernel": rec.kernel, "items": rec.counters.items, "ms": rec.ms})
+        c = rec.counters
+        reads = c.reads or _READS_PER_ITEM.get(rec.kernel, 0) * c.items
+        rows.append({"round": rec.round, "kernel": rec.kernel, "reads": reads, "writes": c.writes,
+                     "transactions": c.transactions, "items": c.items, "ms": rec.ms})
         if rec.kernel.startswith("cc_hook"):
-            hook += rec.ms
+            hook += reads
         else:
-            other += rec.ms
+            other += reads
     return RoundProfile(rows, hook > other)

@@ -583,8 +583,10 @@ __global__ void __launch_bounds__(MS_THREADS, TP_CTAS_PER_SM) k_cc_part_tiles(
     }
 }
 
-// hook of window k over the tile-sorted copy: CTAs take tiles in order and
-// hook the tile's k-th slice (HU edges per thread in flight)
+// hook of window k over the tile-sorted copy: one warp per tile slice (a
+// slice holds ~m/tiles * (2k+1)/P^2 edges -- 64 for the lowest window of a
+// G(n,m) graph at 8 windows -- so a CTA per slice would idle most lanes),
+// warps take tiles in order, HU edges per lane in flight
 template <bool kUF>
 __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_tiles(const uint2* __restrict__ edges,
                                                                 const uint32_t* __restrict__ toff,
@@ -592,16 +594,19 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_tiles(const uint2* __r
                                                                 unsigned long long* flags) {
     bool any = false;
     constexpr int HU = 2;
-    for (unsigned long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint32_t lane = lane_id();
+    const unsigned long long nw = (unsigned long long)gridDim.x * (HOOK_THREADS / 32);
+    for (unsigned long long t = (unsigned long long)blockIdx.x * (HOOK_THREADS / 32) + (threadIdx.x >> 5); t < ntiles;
+         t += nw) {
         const uint32_t lo = __ldg(toff + t * (MAX_PARTS + 1) + k), hi = __ldg(toff + t * (MAX_PARTS + 1) + k + 1);
         const uint2* te = edges + t * MS2_TILE;
-        for (uint32_t i = lo + threadIdx.x; i < hi; i += HU * HOOK_THREADS) {
+        for (uint32_t i = lo + lane; i < hi; i += HU * 32) {
             uint2 uv[HU];
             bool ok[HU];
 #pragma unroll
             for (int q = 0; q < HU; ++q) {
-                ok[q] = i + q * HOOK_THREADS < hi;
-                uv[q] = ok[q] ? __ldcs(te + i + q * HOOK_THREADS) : make_uint2(0, 0);
+                ok[q] = i + q * 32 < hi;
+                uv[q] = ok[q] ? __ldcs(te + i + q * 32) : make_uint2(0, 0);
             }
             uint32_t pu[HU], pv[HU];
 #pragma unroll
@@ -622,7 +627,7 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_tiles(const uint2* __r
             }
         }
     }
-    if (__any_sync(0xffffffffu, any) && lane_id() == 0) flags[0] = 1ull;
+    if (__any_sync(0xffffffffu, any) && lane == 0) flags[0] = 1ull;
 }
 
 // ---------------------------------------------------------------------------
@@ -664,8 +669,8 @@ __global__ void k_cc_apply_min(uint32_t* __restrict__ D, const uint32_t* __restr
 // ---------------------------------------------------------------------------
 // host side
 
-static uint32_t hook_grid(unsigned long long m) { return grid_for(m, HOOK_THREADS, 4, kSMs * 8); }
-static uint32_t vtx_grid(unsigned long long n) { return grid_for(n, COMP_THREADS, 1, kSMs * 8); }
+static uint32_t hook_grid(unsigned long long m) { return grid_for(m, HOOK_THREADS, 4, sm_count() * 8); }
+static uint32_t vtx_grid(unsigned long long n) { return grid_for(n, COMP_THREADS, 1, sm_count() * 8); }
 
 template <class E>
 static int launch_hook(E view, unsigned long long m, unsigned long long row0, unsigned long long n, uint32_t* D,
@@ -707,7 +712,7 @@ struct CcPlan {
 
 static CcPlan plan_cc(unsigned long long n, unsigned long long m) {
     CcPlan p;
-    const char* e = getenv("SG_CC_WBITS");
+    static const char* e = getenv("SG_CC_WBITS");  // experiment switch, read once
     uint32_t wbits = e && *e ? (uint32_t)atoi(e) : 23u;  // window of 2^23 vertices = 32 MiB of D
     if (wbits < 10) wbits = 10;
     if (wbits > 31) wbits = 31;
@@ -736,8 +741,11 @@ static unsigned long long part_tiles(unsigned long long m) { return (m + MS2_TIL
 
 // partition mode: 1 = one-pass tile sort (default), 0 = count + scatter (SG_CC_PART=2pass)
 static bool part_one_pass() {
-    const char* e = getenv("SG_CC_PART");
-    return !(e && strcmp(e, "2pass") == 0);
+    static const bool one = [] {
+        const char* e = getenv("SG_CC_PART");
+        return !(e && strcmp(e, "2pass") == 0);
+    }();
+    return one;
 }
 // the one-pass layout needs 16-B aligned input rows (bulk copies); a reused
 // partition (sg_cc_hook_part, reuse = 1) re-derives its layout from this
@@ -761,8 +769,8 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
         const size_t smem = (size_t)MS2_TILE * E::kBytes + (size_t)MS2_TILE * 8;
         SG_CUDA(set_smem_max(kt, smem));
         const unsigned long long ntile = part_tiles(m);
-        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * TP_CTAS_PER_SM ? ntile
-                                                                                         : kSMs * TP_CTAS_PER_SM);
+        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)sm_count() * TP_CTAS_PER_SM ? ntile
+                                                                                         : sm_count() * TP_CTAS_PER_SM);
         kt<<<ns, MS_THREADS, smem, s>>>(view, m, n, row0, p.shift, p.parts, b.toff, b.edges, flags);
         SG_LAUNCH_CHECK();
         b.tiled = true;
@@ -770,7 +778,7 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
     }
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
     SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * MAX_PARTS, s));
-    const uint32_t cg = nt < kSMs * 8 ? nt : kSMs * 8;
+    const uint32_t cg = nt < sm_count() * 8 ? nt : sm_count() * 8;
     int nbits = 0;
     while ((1 << nbits) < p.parts) ++nbits;
     const bool narrow = E::kBytes == 8 && n <= 0x80000000ull;  // (u32 ids are < 2^32 - 1 = n's cap anyway)
@@ -794,14 +802,14 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
                             : nbits == 3 ? k_cc_part_scatter2<E, 3, false> : k_cc_part_scatter2<E, 4, false>);
         SG_CUDA(set_smem_max(ks, smem));
         const unsigned long long ntile = (m + MS2_TILE - 1) / MS2_TILE;
-        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * PART2_CTAS_PER_SM ? ntile
-                                                                                            : kSMs * PART2_CTAS_PER_SM);
+        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)sm_count() * PART2_CTAS_PER_SM ? ntile
+                                                                                            : sm_count() * PART2_CTAS_PER_SM);
         ks<<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
     } else {
         const size_t smem = MsSmem::bytes((uint32_t)p.parts);
         SG_CUDA(set_smem_max(k_cc_part_scatter<E>, smem));
         const unsigned long long ntile = (m + MS_TILE - 1) / MS_TILE;
-        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)kSMs * 4 ? ntile : kSMs * 4);
+        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)sm_count() * 4 ? ntile : sm_count() * 4);
         k_cc_part_scatter<E><<<ns, MS_THREADS, smem, s>>>(view, m, n, p.shift, p.parts, b.off_part, b.cursor, b.edges);
     }
     SG_LAUNCH_CHECK();
@@ -823,7 +831,7 @@ static int hook_partitions(const CcPlan& p, const CcPartBufs& b, unsigned long l
                            uint32_t* D, int variant, unsigned long long* flags, cudaStream_t s) {
     if (b.tiled) {
         const unsigned long long nt = part_tiles(m);
-        const uint32_t g = (uint32_t)(nt < (unsigned long long)kSMs * 8 ? nt : kSMs * 8);
+        const uint32_t g = (uint32_t)(nt < (unsigned long long)sm_count() * 8 ? nt : sm_count() * 8);
         for (int k = 0; k < p.parts; ++k) {
             if (variant == SG_CC_UF)
                 k_cc_hook_tiles<true><<<g, HOOK_THREADS, 0, s>>>(b.edges, b.toff, nt, k, D, flags);

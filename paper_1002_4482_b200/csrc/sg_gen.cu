@@ -242,7 +242,7 @@ int sg_kiss_device(const uint64_t* states, uint64_t chunks, uint64_t chunk_len, 
 int sg_list_from_order(const int64_t* perm, uint64_t n, void* succ, int succ_dtype, void* stream) {
     if (n == 0) return SG_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    const uint32_t g = grid_for(n, 256, 1, kSMs * 8);
+    const uint32_t g = grid_for(n, 256, 1, sm_count() * 8);
     const long long* p = (const long long*)perm;
     switch (succ_dtype) {
         case SG_U32: k_list_from_order<uint32_t><<<g, 256, 0, s>>>(p, n, (uint32_t*)succ); break;
@@ -257,7 +257,7 @@ int sg_list_from_order(const int64_t* perm, uint64_t n, void* succ, int succ_dty
 int sg_edge_keys(const uint64_t* draws, uint64_t pairs, uint64_t n, int64_t* keys, void* stream) {
     if (pairs == 0) return SG_OK;
     if (n == 0) return SG_ERR_VALUE;
-    k_edge_keys<<<grid_for(pairs, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+    k_edge_keys<<<grid_for(pairs, 256, 1, sm_count() * 8), 256, 0, (cudaStream_t)stream>>>(
         (const unsigned long long*)draws, pairs, n, (long long*)keys);
     SG_LAUNCH_CHECK();
     return SG_OK;
@@ -266,7 +266,7 @@ int sg_edge_keys(const uint64_t* draws, uint64_t pairs, uint64_t n, int64_t* key
 int sg_edges_from_keys(const int64_t* keys, uint64_t m, uint64_t n, int64_t* edges, void* stream) {
     if (m == 0) return SG_OK;
     if (n == 0) return SG_ERR_VALUE;
-    k_edges_from_keys<<<grid_for(m, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+    k_edges_from_keys<<<grid_for(m, 256, 1, sm_count() * 8), 256, 0, (cudaStream_t)stream>>>(
         (const long long*)keys, m, n, (long long*)edges);
     SG_LAUNCH_CHECK();
     return SG_OK;
@@ -313,7 +313,7 @@ int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t
 
 int sg_gather_i64(const int64_t* src, const int64_t* idx, uint64_t k, int64_t* out, void* stream) {
     if (k == 0) return SG_OK;
-    k_gather_i64<<<grid_for(k, 256, 1, kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+    k_gather_i64<<<grid_for(k, 256, 1, sm_count() * 8), 256, 0, (cudaStream_t)stream>>>(
         (const long long*)src, (const long long*)idx, k, (long long*)out);
     SG_LAUNCH_CHECK();
     return SG_OK;

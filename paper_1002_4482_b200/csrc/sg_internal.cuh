@@ -21,7 +21,9 @@ namespace sg {
 
 constexpr uint32_t NIL = 0xFFFFFFFFu;
 constexpr unsigned long long NONE64 = ~0ull;
-constexpr int kSMs = 148;
+// SMs of the current device (148 on a B200), queried once per device; every
+// persistent grid is sized from it
+int sm_count();
 
 // Kernel ids; names are returned by sg_kernel_name().  Names follow the
 // reference's phase names where a kernel does that phase's job

@@ -38,6 +38,8 @@
 #include <type_traits>
 #include <string.h>
 
+#include <atomic>
+
 #include "sg_internal.cuh"
 #include "sg_msplit.cuh"
 
@@ -355,6 +357,12 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
 // locally shuffled layouts) are contracted tile by tile in shared memory
 // (k_rs_contract); scattered lists take the ruling-set record walk.
 __device__ __forceinline__ bool layout_local(const ListStatus* st) { return st->local != 0; }
+// the top level has found the list invalid (set before any rank is written):
+// the passes that write ranks skip, so an aliased successor array
+// (reuse_succ) survives for the host's violation report
+__device__ __forceinline__ bool ranks_invalid(const ListStatus* st) {
+    return st->overflow || st->bad || !st->head_ok || st->head_sum != st->R[0];
+}
 
 // Single-CTA exclusive scan of per-tile counts, in place, chunk by chunk
 // with coalesced (transposed) loads and stores.  Returns the total.
@@ -1032,7 +1040,7 @@ template <class OutT>
 __global__ void __launch_bounds__(256) k_rs_rec_scatter(const unsigned long long* __restrict__ pairs,
                                                                OutT* __restrict__ rank, unsigned long long n,
                                                                uint32_t fshift, const ListStatus* st, int vec) {
-    if (layout_local(st) || st->overflow) return;
+    if (layout_local(st) || ranks_invalid(st)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     OutT* win = reinterpret_cast<OutT*>(smem_raw);
     const unsigned long long w0 = (unsigned long long)blockIdx.x << fshift;
@@ -1246,7 +1254,7 @@ __global__ void __launch_bounds__(256) k_rs_expand_k(const unsigned long long* _
 template <class OutT>
 __global__ void k_rs_expand_direct(const uint32_t* __restrict__ IS0, OutT* __restrict__ rank, unsigned long long n,
                                    const ListStatus* st) {
-    if (st->overflow) return;
+    if (ranks_invalid(st)) return;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         rank[i] = (OutT)(IS0[i] - 1u);
@@ -1620,7 +1628,7 @@ __global__ void __launch_bounds__(256) k_rs_contract_expand(const uint32_t* __re
                                                             const uint2* __restrict__ lvl1,
                                                             const uint32_t* __restrict__ IS1, OutT* __restrict__ rank,
                                                             const ListStatus* st) {
-    if (!layout_local(st) || st->overflow || st->bad) return;
+    if (!layout_local(st) || ranks_invalid(st)) return;
     const unsigned long long N = st->R[0];
     const unsigned long long R1 = st->R[1];
     auto rank_of = [&](unsigned long long i, uint32_t w) -> uint32_t {
@@ -1682,7 +1690,7 @@ struct RsPlan {
     uint32_t cshift = 20;                        // coarse window = 2^cshift nodes
     uint32_t cbins = 1;                          // number of coarse windows
     unsigned long long nwin = 1;                 // number of fine windows
-    uint32_t walk_grid = kSMs * (2048 / WALK_THREADS);
+    uint32_t walk_grid = sm_count() * (2048 / WALK_THREADS);
     bool rec_ok = true;                          // fine windows fit shared memory
     int contract = 1;                            // allow the tile contraction for local layouts
     bool packed = false;                         // level-0 records packed into one u64
@@ -1704,6 +1712,31 @@ static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t h
     return (uint32_t)v;
 }
 
+// experiment switches (SG_RS_* environment variables), read once per process:
+// the defaults are the measured configuration, the switches only exist to
+// re-run the comparisons DESIGN.md records
+struct RsTuning {
+    uint32_t win_kb, kb0, kb1, fin, walk_cap, load_mode, contract, coop, topn, packed, fused;
+};
+static const RsTuning& rs_tuning() {
+    static const RsTuning t = [] {
+        RsTuning v;
+        v.win_kb = env_u32("SG_RS_WIN_KB", 64, 8, 128);  // fine window: KiB of shared memory in rs5_scatter
+        v.kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);
+        v.kb1 = env_u32("SG_RS_KBITS", 3, 1, 16);  // upper levels: short chains, the walk tail is latency-bound
+        v.fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
+        v.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
+        v.load_mode = env_u32("SG_WALK_LOAD", 0, 0, 3);
+        v.contract = env_u32("SG_RS_CONTRACT", 1, 0, 1);
+        v.coop = env_u32("SG_RS_COOP", 1, 0, 1);
+        v.topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
+        v.packed = env_u32("SG_RS_PACKED", 1, 0, 1);
+        v.fused = env_u32("SG_RS_FUSED", 1, 0, 1);
+        return v;
+    }();
+    return t;
+}
+
 static uint32_t mix32(uint64_t x) {
     x ^= x >> 33;
     x *= 0xff51afd7ed558ccdull;
@@ -1715,10 +1748,10 @@ static uint32_t mix32(uint64_t x) {
 
 static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     RsPlan p;
-    // a fine window fills 32 KiB of shared memory in rs5_scatter; coarse
-    // windows: few enough bins for one multisplit, >= 64 pairs per bin per tile
-    // a fine window fills SG_RS_WIN_KB (default 64) KiB of shared memory in rs5_scatter
-    const uint32_t win_kb = env_u32("SG_RS_WIN_KB", 64, 8, 128);
+    // a fine window fills win_kb (64) KiB of shared memory in rs5_scatter;
+    // coarse windows: few enough bins for one multisplit
+    const RsTuning& tu = rs_tuning();
+    const uint32_t win_kb = tu.win_kb;
     p.fshift = 10;
     while (((size_t)out_bytes << (p.fshift + 1)) <= ((size_t)win_kb << 10)) ++p.fshift;
     uint32_t cs = p.fshift + 1;
@@ -1731,23 +1764,23 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.nwin = (unsigned long long)p.cbins << (cs - p.fshift);
     // one lane per ruler is plenty; every warp that walks may leave one partial chunk
     unsigned long long wg = ((n >> 5) + 2 * WALK_THREADS - 1) / (2 * WALK_THREADS);
-    if (wg < (unsigned long long)kSMs) wg = kSMs;
-    if (wg > (unsigned long long)kSMs * (2048 / WALK_THREADS)) wg = kSMs * (2048 / WALK_THREADS);
+    if (wg < (unsigned long long)sm_count()) wg = sm_count();
+    if (wg > (unsigned long long)sm_count() * (2048 / WALK_THREADS)) wg = sm_count() * (2048 / WALK_THREADS);
     p.walk_grid = (uint32_t)wg;
     const unsigned long long warps = wg * (WALK_THREADS / 32);
     p.maxchunks = n / (REC_CH - 32) + warps + 2;
-    const uint32_t kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);
-    const uint32_t kb1 = env_u32("SG_RS_KBITS", 3, 1, 16);  // upper levels: short chains, the walk tail is latency-bound
-    const uint32_t fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
-    p.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
-    p.load_mode = (int)env_u32("SG_WALK_LOAD", 0, 0, 3);
-    p.contract = (int)env_u32("SG_RS_CONTRACT", 1, 0, 1);
-    p.coop_top = env_u32("SG_RS_COOP", 1, 0, 1) != 0;
+    const uint32_t kb0 = tu.kb0;
+    const uint32_t kb1 = tu.kb1;
+    const uint32_t fin = tu.fin;
+    p.walk_cap = tu.walk_cap;
+    p.load_mode = (int)tu.load_mode;
+    p.contract = (int)tu.contract;
+    p.coop_top = tu.coop != 0;
 
     p.cap[0] = n;
     // a ruler list of at most SG_RS_TOPN (> FINAL_CAP) nodes above level 0 is
     // ranked by multi-CTA pointer jumping (k_rs_top_jump) instead of more walks
-    const unsigned long long topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
+    const unsigned long long topn = tu.topn;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1 && !(p.levels >= 1 && N <= topn)) {
         const uint32_t kb = p.levels == 0 ? kb0 : kb1;
@@ -1760,7 +1793,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
         p.cap[p.levels] = cap;
         N = exp;
     }
-    if (p.levels > 0 && env_u32("SG_RS_PACKED", 1, 0, 1)) {
+    if (p.levels > 0 && tu.packed) {
         // field widths: cur needs ceil(log2 n) bits; sid needs room for cap[1]
         // ids plus an all-ones pad value that is never an id
         uint32_t cb = 1, sbits = 1;
@@ -1772,7 +1805,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
             p.rec_sb = 64 - cb;
             const unsigned long long lmax = p.rec_lb >= 32 ? 0xFFFFFFFFull : ((1ull << p.rec_lb) - 1);
             if (p.walk_cap > lmax) p.walk_cap = (uint32_t)lmax;  // longer chains: Wyllie fallback
-            p.fused = p.cbins <= WB_MAXBINS && env_u32("SG_RS_FUSED", 1, 0, 1) != 0;
+            p.fused = p.cbins <= WB_MAXBINS && tu.fused != 0;
         }
     }
     return p;
@@ -1859,7 +1892,7 @@ static int wyllie_run(const SuccT* succ, OutT* rank, uint64_t n, int variant, Li
         SG_LAUNCH_CHECK();
         return SG_OK;
     }
-    const uint32_t grid = grid_for(n, JUMP_THREADS, 1, kSMs * 8);
+    const uint32_t grid = grid_for(n, JUMP_THREADS, 1, sm_count() * 8);
     rec.begin(K_WY_INIT, 0, grid, JUMP_THREADS, n);
     k_wy_init<SuccT><<<grid, JUMP_THREADS, 0, s>>>(succ, word, n, st);
     rec.end();
@@ -1910,7 +1943,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         k_rs_final<Level0<SuccT>><<<1, 1024, 0, s>>>(Level0<SuccT>{succ, p.load_mode}, b.fa, b.fb, b.IS[0], b.st, 0);
         rec.end();
         SG_LAUNCH_CHECK();
-        const uint32_t g = grid_for(n, 256, 1, kSMs * 8);
+        const uint32_t g = grid_for(n, 256, 1, sm_count() * 8);
         rec.begin(K_RS5_EXPAND, 0, g, 256, n);
         k_rs_expand_direct<OutT><<<g, 256, 0, s>>>(b.IS[0], rank, n, b.st);
         rec.end();
@@ -1926,7 +1959,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         uint32_t* tk = k == 0 ? b.tiles : b.tiles_up;
         if (k == 0) {
             const uint32_t cw = (nt + TILE_THREADS / 32 - 1) / (TILE_THREADS / 32);  // one warp per tile
-            const uint32_t cg = cw < kSMs * 8 ? cw : kSMs * 8;
+            const uint32_t cg = cw < sm_count() * 8 ? cw : sm_count() * 8;
             rec.begin(K_RS_COUNT, 0, cg, TILE_THREADS, capN);
             const bool narrow = sizeof(SuccT) == 4 && n <= 0x80000000ull;
             const bool vec = ((uintptr_t)succ & 15) == 0;
@@ -1947,7 +1980,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
         rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
-        k_rs_select<false><<<nt < kSMs * 8 ? nt : kSMs * 8, TILE_THREADS, 0, s>>>(tk, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
+        k_rs_select<false><<<nt < sm_count() * 8 ? nt : sm_count() * 8, TILE_THREADS, 0, s>>>(tk, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
                                                         k == 0 ? b.rgrp : nullptr);
         rec.end();
         SG_LAUNCH_CHECK();
@@ -1962,8 +1995,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
                 auto kern = k_rs_walk_bin<SuccT, WB_T, WB_C, WB_S>;
                 const size_t smem = (size_t)p.cbins * WB_S * sizeof(unsigned long long);
                 SG_CUDA(set_smem_max(kern, smem));
-                rec.begin(K_RS3_WALK, 0, kSMs * WB_C, WB_T, capN);
-                kern<<<kSMs * WB_C, WB_T, smem, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.cursor, b.pairs, b.st,
+                rec.begin(K_RS3_WALK, 0, sm_count() * WB_C, WB_T, capN);
+                kern<<<sm_count() * WB_C, WB_T, smem, s>>>(succ, b.rgrp, b.spl[0], b.lvl[1], b.cursor, b.pairs, b.st,
                                                      p.kbits[0], p.salt[0], p.walk_cap, p.load_mode, p.rec_sb, p.rec_lb,
                                                      p.cshift, p.cbins);
             } else {
@@ -1979,14 +2012,14 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             }
             rec.end();
             SG_LAUNCH_CHECK();
-            const uint32_t cg = nt < kSMs * CT_CTAS_PER_SM ? nt : kSMs * CT_CTAS_PER_SM;
+            const uint32_t cg = nt < sm_count() * CT_CTAS_PER_SM ? nt : sm_count() * CT_CTAS_PER_SM;
             rec.begin(K_RS_CONTRACT, 0, cg, TILE_THREADS, capN);
             const int rc = launch_contract<SuccT>(cg, s, succ, b.st, b.tiles, b.rid, b.spl[0], b.IS[1], b.lvl[1],
                                                   reinterpret_cast<uint32_t*>(b.word0));
             if (rc != SG_OK) return rc;
             rec.end();
             SG_LAUNCH_CHECK();
-            const uint32_t lg = grid_for(capR, 256, 1, kSMs * 8);
+            const uint32_t lg = grid_for(capR, 256, 1, sm_count() * 8);
             rec.begin(K_RS_CONTRACT_LINK, 0, lg, 256, capR);
             k_rs_contract_link<<<lg, 256, 0, s>>>(b.rid, b.spl[0], b.IS[1], b.lvl[1], b.st);
         } else {
@@ -2006,11 +2039,20 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     const int L = p.levels;
     bool coop_done = false;
     if (p.cap[L] > FINAL_CAP && p.coop_top) {
-        static int coop_blocks = -1;  // resident 512-thread CTAs per SM for the cooperative launch
+        // resident 512-thread CTAs per SM for the cooperative launch, per device
+        static std::atomic<int> coop_cache[64];  // 0: unknown, else blocks + 1
+        int cdev = 0;
+        cudaGetDevice(&cdev);
+        std::atomic<int>& slot = coop_cache[cdev >= 0 && cdev < 64 ? cdev : 0];
+        int coop_blocks = slot.load(std::memory_order_relaxed) - 1;
         if (coop_blocks < 0) {
             int nb = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rs_top_coop<LevelK>, 512, 0) != cudaSuccess) nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rs_top_coop<LevelK>, 512, 0) != cudaSuccess) {
+                cudaGetLastError();
+                nb = 0;
+            }
             coop_blocks = nb;
+            slot.store(nb + 1, std::memory_order_relaxed);
         }
         if (coop_blocks > 0) {
             LevelK view{b.lvl[L]};
@@ -2020,7 +2062,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             uint32_t* isp = b.IS[L];
             int rounds = jump_rounds(p.cap[L]) + 1;
             void* args[] = {&view, &A, &stp, &lv, &isp, &rounds};
-            const uint32_t g = (uint32_t)(kSMs * (coop_blocks < 2 ? coop_blocks : 2));
+            const uint32_t g = (uint32_t)(sm_count() * (coop_blocks < 2 ? coop_blocks : 2));
             rec.begin(K_RS4_RANK, L, g, 512, p.cap[L]);
             const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_rs_top_coop<LevelK>, g, 512, args, 0, s);
             rec.end();
@@ -2033,7 +2075,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     if (coop_done) {
     } else if (p.cap[L] > FINAL_CAP) {
-        const uint32_t g = grid_for(p.cap[L], 256, 4, kSMs * 8);
+        const uint32_t g = grid_for(p.cap[L], 256, 4, sm_count() * 8);
         rec.begin(K_RS4_RANK, L, g, 256, p.cap[L]);
         k_rs_top_init<LevelK><<<g, 256, 0, s>>>(LevelK{b.lvl[L]}, b.fa, b.st, L);
         rec.end();
@@ -2053,7 +2095,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     // upward: expand
     for (int k = L - 1; k >= 1; --k) {
-        const uint32_t g = grid_for(p.cap[k], 256, 1, kSMs * 8);
+        const uint32_t g = grid_for(p.cap[k], 256, 1, sm_count() * 8);
         rec.begin(K_RS4_EXPAND, k, g, 256, p.cap[k]);
         k_rs_expand_k<<<g, 256, 0, s>>>(b.word[k], b.IS[k + 1], b.IS[k], b.st, k);
         rec.end();
@@ -2061,7 +2103,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     {  // local layouts: expand the contraction
         const uint32_t nt = (uint32_t)((n + TILE - 1) / TILE);
-        const uint32_t eg = grid_for(n / 4 + 1, 256, 1, kSMs * 8);
+        const uint32_t eg = grid_for(n / 4 + 1, 256, 1, sm_count() * 8);
         rec.begin(K_RS5_EXPAND, 0, eg, 256, n);
         if (((uintptr_t)rank & 15) == 0)
             k_rs_contract_expand<OutT, true><<<eg, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(b.word0), b.tiles,
@@ -2074,7 +2116,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     // scattered layouts: rank the records, bucket them by window, scatter
     constexpr uint32_t tile2 = MS_THREADS * MS2_ITEMS;
-    const uint32_t persist2 = kSMs * 2;
+    const uint32_t persist2 = sm_count() * 2;
     const size_t sm_ref2 = (size_t)tile2 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), tile2);
     if (!p.fused) {
         SG_CUDA(cudaMemsetAsync(b.cursor, 0, sizeof(unsigned long long) * (size_t)(p.cbins + p.nwin), s));
@@ -2094,8 +2136,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         auto kr = fbits <= 4 ? k_rs_rec_refine2<8, 1, 4>
                              : (fbits <= 6 ? k_rs_rec_refine2<8, 1, 6> : k_rs_rec_refine2<8, 1, 8>);
         SG_CUDA(set_smem_max(kr, sm8));
-        rec.begin(K_RS5_REFINE, 0, kSMs * 3, MS_THREADS, n);
-        kr<<<kSMs * 3, MS_THREADS, sm8, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
+        rec.begin(K_RS5_REFINE, 0, sm_count() * 3, MS_THREADS, n);
+        kr<<<sm_count() * 3, MS_THREADS, sm8, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
                                              b.IS[1], p.rec_sb, p.rec_lb);
     } else {
         auto kr = k_rs_rec_refine2<MS2_ITEMS, 0>;

@@ -28,12 +28,17 @@ constexpr int MS_MAXB = 1024;
 // peer ranking: 0 match.any, 1 ballots, 2 alternate per item (SG_MS_PEERS)
 static __constant__ int g_ms_peers = 1;
 
+// once per device and host thread, only when the switch is set
 static inline void ms_configure() {
-    const char* e = getenv("SG_MS_PEERS");
-    if (e && *e) {
-        const int v = atoi(e);
-        cudaMemcpyToSymbol(g_ms_peers, &v, sizeof(int));
-    }
+    static const char* e = getenv("SG_MS_PEERS");
+    if (!(e && *e)) return;
+    static thread_local unsigned long long done = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && (done >> dev & 1ull)) return;
+    if (dev < 64) done |= 1ull << dev;
+    const int v = atoi(e);
+    cudaMemcpyToSymbol(g_ms_peers, &v, sizeof(int));
 }
 
 // dynamic shared memory layout for nb bins

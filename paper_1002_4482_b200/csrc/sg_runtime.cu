@@ -7,6 +7,8 @@
 #include <mutex>
 #include <string>
 
+#include <atomic>
+
 #include "sg_internal.cuh"
 
 namespace sg {
@@ -148,6 +150,22 @@ namespace sg {
 
 // Optional device tuning from the environment, applied once per process and
 // device: SG_L2_FETCH=<bytes> sets cudaLimitMaxL2FetchGranularity (a hint).
+int sm_count() {
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> cache[kMaxDev];  // 0: not queried yet
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) dev = 0;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        v = 148;
+    }
+    cache[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+
 void apply_tuning() {
     static thread_local int done_mask = 0;
     int dev = 0;

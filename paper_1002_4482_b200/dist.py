@@ -236,16 +236,19 @@ def sharded_components(n, edges, row0, comm, ops, variant="uf", round_bound=None
 
 
 def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", accounting="full",
-                       block_size=256, seed=0, workers=None, shard=None):
+                       block_size=256, seed=0, workers=None, shard=None, comm=None, sparse_cap=None):
     """Edge-sharded ``sv_components`` across the ranks of `group`.
 
     Every rank calls it with the same graph (host or its own device copy) --
     or with its own block of rows via ``shard=(row0, edges_block)`` -- and
-    gets the full int64 label array (replicated) plus ExecStats.
+    gets the full int64 label array (replicated) plus ExecStats.  `comm`
+    replaces the group's collectives (any object with TorchDistComm's
+    methods); `sparse_cap` overrides the changed-entry exchange's per-rank
+    cap (default n/8/G).
     """
     if graph is not None and graph.n <= 0:
         raise InvalidGraphError("graph needs at least one vertex")
-    comm = TorchDistComm(group)
+    comm = comm or TorchDistComm(group)
     dev = _device.require_cuda()
     n = graph.n
     if shard is None:
@@ -264,7 +267,7 @@ def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", 
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record()
-    D, info = sharded_components(n, edges, int(row0), comm, ops, variant=variant, trace=trace)
+    D, info = sharded_components(n, edges, int(row0), comm, ops, variant=variant, trace=trace, sparse_cap=sparse_cap)
     stop.record()
     stop.synchronize()
     labels = D[:n].to(torch.int64)
@@ -278,7 +281,8 @@ def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", 
     stats.meta.update(n=n, p=int(p), m_stored=graph.m, oriented_m=2 * graph.m, rounds=info["rounds"],
                       round_bound=sv_round_bound(n), roots_per_round=info["roots_per_round"], variant=variant,
                       edge_sweeps=info["edge_sweeps"], vertex_sweeps=info["vertex_sweeps"], world=comm.world,
-                      allreduce_bytes=info["allreduce_bytes"], allgather_bytes=info["allgather_bytes"])
+                      allreduce_bytes=info["allreduce_bytes"], allgather_bytes=info["allgather_bytes"],
+                      sparse_rounds=info.get("sparse_rounds", 0))
     if isinstance(graph.edges, torch.Tensor) and graph.edges.is_cuda:
         return labels, stats
     return labels.cpu().numpy(), stats

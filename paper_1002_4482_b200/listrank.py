@@ -210,13 +210,25 @@ def wyllie_rank(sl, p, variant="multi_kernel", backend="simulated", accounting="
 # ---------------------------------------------------------------------------
 # ruling set
 
+# draws and device index copies are cached only up to this many splitters
+# (64 cached entries x 512 KiB at most, host and HBM); larger p is redrawn
+_CACHE_MAX_R = 1 << 16
+
+
 def _draw_splitters(n, r, seed):
-    """Cached copy of the reference's splitter draw (deterministic in its arguments)."""
+    """Copy of the reference's splitter draw (deterministic in its
+    arguments; cached for r <= _CACHE_MAX_R)."""
+    if int(r) > _CACHE_MAX_R:
+        return _draw_splitters_uncached(int(n), int(r), int(seed))
     return _draw_splitters_cached(int(n), int(r), int(seed)).copy()
 
 
 @functools.lru_cache(maxsize=64)
 def _draw_splitters_cached(n, r, seed):
+    return _draw_splitters_uncached(n, r, seed)
+
+
+def _draw_splitters_uncached(n, r, seed):
     """Head plus r-1 distinct random interior nodes, reproducible by seed
     (listrank.py:211-231): KISS rejection sampling in batches, or a random
     ordering of all interior nodes when more than half of them are needed."""
@@ -246,7 +258,7 @@ _IDX_CACHE = {}
 def _device_index(spl_nodes, dev, key):
     """Device copy of a splitter-node array; cached when `key` names a
     deterministic draw (n, p, seed)."""
-    if key is None:
+    if key is None or len(spl_nodes) > _CACHE_MAX_R:
         return torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
     key = (str(dev),) + tuple(key)
     t = _IDX_CACHE.get(key)
@@ -297,6 +309,11 @@ def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_su
     if p > 1 and p * math.log2(p) > n:
         stats.warnings.append("super-linear work regime: p*lg(p) > n")
         stats.meta["superlinear"] = True
+    if p > block_size:
+        # the reference's reduced list is wider than one block, so its RS4
+        # runs one launch per jump round (listrank.py:343-346); the device
+        # ranks its own ruler levels either way, the flag keeps the meta
+        stats.meta["rs4_fallback"] = True
     if even:
         # perfect splitters every n/p chain positions (listrank.py:431-436):
         # node at chain position k has rank n-1-k

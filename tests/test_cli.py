@@ -105,3 +105,14 @@ def test_plot_data(cuda, tmp_path):
                  "--out", str(out), "--plot-data", str(plot)]) == 0
     rows = _read(plot)
     assert len(rows) == 2 and float(rows[0]["speedup"]) == 1.0
+
+
+def test_host_expectations_match_reference_examples():
+    # test_core.py:46-59 known answers, and a labelling that merges two
+    # components is caught (the host check is the component minimum)
+    assert cli._host_ranks(np.array([1, 2, 2])).tolist() == [2, 1, 0]
+    assert cli._host_ranks(np.array([3, 4, 2, 1, 2])).tolist() == [4, 2, 0, 3, 1]
+    lab = cli._host_labels(6, np.array([[0, 3], [3, 5], [2, 4]]))
+    assert lab.tolist() == [0, 1, 2, 0, 2, 0]
+    from paper_1002_4482_b200.core import compare_arrays
+    assert compare_arrays(lab, np.zeros(6, dtype=np.int64)) == 1

@@ -1,0 +1,44 @@
+"""Small-size driver for compute-sanitizer (tools/sanitize.sh): every libsg
+kernel family once, at sizes the sanitizers finish in minutes.
+
+    list ranking: rs_rank on random (ruling-set walk + binned records,
+      refine, scatter, levels >= 1, cooperative top) and ordered lists
+      (tile contraction), wyllie_rank both variants;
+    components: uf and sv, with and without the window partition
+      (SG_CC_WBITS=12 forces several windows at small n).
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1002_4482_b200 as g  # noqa: E402
+
+
+def main():
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    dev = torch.device("cuda", 0)
+    n = int(os.environ.get("SAN_N", 1 << 18))
+    if which in ("all", "list"):
+        sl = g.gen_list(n, seed=1, device=dev)
+        r, st = g.rs_rank(sl, 1024)
+        print("rs random", st.meta["path"], st.meta["levels"], int(r.max()))
+        # enough levels for the multi-CTA top (cooperative) at this size
+        o = g.SuccessorList(torch.cat([torch.arange(1, n, device=dev), torch.tensor([n - 1], device=dev)]).to(torch.int32))
+        r, st = g.rs_rank(o, 1024)
+        print("rs ordered", st.meta["path"], int(r[0]))
+        r, _ = g.wyllie_rank(g.gen_list(1 << 14, seed=2, device=dev), 64)
+        r, _ = g.wyllie_rank(g.gen_list(200, seed=3, device=dev), 128, variant="single_block")
+        print("wyllie ok")
+    if which in ("all", "cc"):
+        gr = g.gen_random_graph(n, 4.0 * n / (n * (n - 1) // 2) * 2, seed=0, device=dev)
+        for variant in ("uf", "sv"):
+            lab, st = g.sv_components(gr, 64, variant=variant)
+            print("cc", variant, st.meta["rounds"], int(lab.max()))
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
