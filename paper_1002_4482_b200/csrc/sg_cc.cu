@@ -712,7 +712,7 @@ struct CcPlan {
 
 static CcPlan plan_cc(unsigned long long n, unsigned long long m) {
     CcPlan p;
-    static const char* e = getenv("SG_CC_WBITS");  // experiment switch, read once
+    const char* e = getenv("SG_CC_WBITS");  // window width switch (tests force small windows with it)
     uint32_t wbits = e && *e ? (uint32_t)atoi(e) : 23u;  // window of 2^23 vertices = 32 MiB of D
     if (wbits < 10) wbits = 10;
     if (wbits > 31) wbits = 31;
@@ -739,11 +739,13 @@ struct CcPartBufs {
 
 static unsigned long long part_tiles(unsigned long long m) { return (m + MS2_TILE - 1) / MS2_TILE; }
 
-// partition mode: 1 = one-pass tile sort (default), 0 = count + scatter (SG_CC_PART=2pass)
+// partition mode: count + scatter (default), or the one-pass tile sort
+// (SG_CC_PART=tiles): the tile sort moves 0.5 ms less data at C5, but hooking
+// the per-tile slices costs 1.1 ms more (profiles/r02_cc_partition.txt)
 static bool part_one_pass() {
     static const bool one = [] {
         const char* e = getenv("SG_CC_PART");
-        return !(e && strcmp(e, "2pass") == 0);
+        return e && strcmp(e, "tiles") == 0;
     }();
     return one;
 }

@@ -1034,6 +1034,201 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
     if (over) st->bad = 1;
 }
 
+// rs5_refine, counter-ranked (default for <= 64 fine bins).  Same job as
+// k_rs_rec_refine2<.., 1, ..> -- coarse-window records -> {cur, rank} pairs
+// split by fine window -- with the tile ranked by per-thread counters instead
+// of warp ballots (the radix-rank scheme of a block radix sort):
+//   1. every thread counts its RF_IT records per bin in its own column of a
+//      [bin/2][thread] array of packed 16-bit counters (no atomics, no bank
+//      conflicts: a thread only touches its own column),
+//   2. one raking exclusive scan of the packed array gives every (bin,
+//      thread) its first slot in the bin-sorted tile (low halves = even bins
+//      first, then the odd bins: every bin is still one contiguous run),
+//   3. records go to their slot in shared memory; one global atomic per
+//      (tile, bin) claims the run's slots in the fine window; runs leave the
+//      SM as coalesced 8-B stores.
+// All slot arithmetic is 32-bit (a tile holds RF_TILE records).  The next
+// tile streams in (cp.async.bulk) while the current one is ranked; the
+// IS_1[sid] gathers are issued before the counting and first used at the
+// placement.
+constexpr int RF_THREADS = 256;
+constexpr int RF_IT = 16;
+constexpr int RF_TILE = RF_THREADS * RF_IT;  // 4096 records
+constexpr int RF_MAXB = 64;                  // fine bins per coarse window handled here
+constexpr int RF_CTAS_PER_SM = 2;
+
+__device__ __forceinline__ uint32_t rf_pad(uint32_t i) { return i + (i >> 5); }  // one pad word per 32
+
+static size_t rf_smem_bytes(uint32_t nb) {
+    const uint32_t words = (nb + 1) / 2 * RF_THREADS;
+    return (size_t)RF_TILE * 8 * 2 + (size_t)(words + (words >> 5)) * 4 + 16;
+}
+
+template <int kMode>  // 1: packed walk records in (ranked here); 0: {cur, rank} pairs in
+__global__ void __launch_bounds__(RF_THREADS, RF_CTAS_PER_SM) k_rs_refine_cnt(
+    const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
+    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
+    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
+    if (layout_local(st) || st->overflow) return;
+    const uint32_t fb = 1u << (cshift - fshift);  // <= RF_MAXB
+    const uint32_t W = (fb + 1) / 2;              // counter words per thread
+    extern __shared__ __align__(128) unsigned char rf_raw[];
+    unsigned long long* s_in = reinterpret_cast<unsigned long long*>(rf_raw);
+    unsigned long long* s_sort = s_in + RF_TILE;
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_sort + RF_TILE);
+    __shared__ unsigned long long bar;
+    __shared__ uint32_t s_wsum[RF_THREADS / 32];
+    __shared__ uint32_t s_base[RF_MAXB], s_lim[RF_MAXB];
+    __shared__ uint32_t s_total;
+    const uint32_t t = threadIdx.x;
+    const uint32_t lane = lane_id(), warp = t >> 5;
+    const unsigned long long ntiles = (n + RF_TILE - 1) / RF_TILE;
+    const unsigned long long R1 = st->R[1];
+    const unsigned long long pol_last = l2_evict_last();
+    const uint32_t fmask = fb - 1;
+    const uint32_t lmask = lb >= 32 ? 0xFFFFFFFFu : ((1u << lb) - 1u);
+    const unsigned long long smask = (1ull << (sb - lb)) - 1;
+    if (t == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    auto issue = [&](unsigned long long tile) {
+        if (t == 0 && tile < ntiles) {
+            const unsigned long long e0 = tile * RF_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)RF_TILE, n - e0);
+            const uint32_t bytes = (cnt * 8u + 15u) & ~15u;  // the buffer is padded to whole windows
+            mbar_expect_tx(&bar, bytes);
+            bulk_g2s_hint(s_in, in + e0, bytes, &bar, l2_evict_first());
+        }
+    };
+    bool over = false;
+    uint32_t phase = 0;
+    issue(blockIdx.x);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long e0 = tile * RF_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)RF_TILE, n - e0);
+        const unsigned long long c = e0 >> cshift;  // tiles never straddle a coarse window
+        // zero this thread's counter column while the tile lands
+        for (uint32_t w = 0; w < W; ++w) s_cnt[rf_pad(w * RF_THREADS + t)] = 0u;
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        unsigned long long rec[RF_IT];
+        uint32_t gv[RF_IT];
+        uint32_t loc[RF_IT];  // bin (low 8 bits, 0xFF = skip) | rank among this thread's records of the bin << 8
+#pragma unroll
+        for (int g = 0; g < RF_IT / 2; ++g) {
+            const uint32_t e = (g * RF_THREADS + t) * 2;
+            const ulonglong2 v = e < cnt ? reinterpret_cast<const ulonglong2*>(s_in)[e >> 1] : make_ulonglong2(0, 0);
+            rec[2 * g] = v.x;
+            rec[2 * g + 1] = v.y;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const unsigned long long r = q ? v.y : v.x;
+                const unsigned long long cur = kMode == 1 ? (r >> sb) : (r >> 32);
+                if (kMode == 1) {
+                    const unsigned long long o = (r >> lb) & smask;
+                    gv[2 * g + q] = ld_hint(IS1 + (o < R1 ? o : 0), pol_last);
+                }
+                loc[2 * g + q] = (e + q < cnt && (cur >> cshift) == c) ? ((uint32_t)cur >> fshift) & fmask : 0xFFu;
+            }
+        }
+        __syncthreads();  // staging consumed, counters zeroed
+        issue(tile + gridDim.x);
+        // 1. count: own column, packed 16-bit halves
+#pragma unroll
+        for (int j = 0; j < RF_IT; ++j) {
+            const uint32_t d = loc[j];
+            if (d != 0xFFu) {
+                const uint32_t a = rf_pad((d >> 1) * RF_THREADS + t);
+                const uint32_t sh = (d & 1u) << 4;
+                const uint32_t v = s_cnt[a];
+                s_cnt[a] = v + (1u << sh);
+                loc[j] = d | (((v >> sh) & 0xFFFFu) << 8);
+            }
+        }
+        __syncthreads();
+        // 2. raking exclusive scan over the packed array, logical order [word][thread]
+        {
+            const uint32_t i0 = t * W;
+            uint32_t sum = 0;
+            for (uint32_t k = 0; k < W; ++k) sum += s_cnt[rf_pad(i0 + k)];
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += y;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            uint32_t run = incl - sum;
+#pragma unroll
+            for (int k = 0; k < RF_THREADS / 32; ++k)
+                if (k < (int)warp) run += s_wsum[k];
+            if (t == RF_THREADS - 1) s_total = run + sum;  // packed grand total
+            for (uint32_t k = 0; k < W; ++k) {
+                const uint32_t a = rf_pad(i0 + k);
+                const uint32_t v = s_cnt[a];
+                s_cnt[a] = run;
+                run += v;
+            }
+        }
+        __syncthreads();
+        const uint32_t tot = s_total;
+        const uint32_t tot_lo = tot & 0xFFFFu;  // records in even bins: the odd bins follow them
+        auto bin_start = [&](uint32_t d) {      // first slot of bin d in the sorted tile
+            const uint32_t v = s_cnt[rf_pad((d >> 1) * RF_THREADS)];
+            return (d & 1u) ? (v >> 16) + tot_lo : (v & 0xFFFFu);
+        };
+        // bins: start, size, global claim (one atomic per non-empty bin and tile)
+        if (t < fb) {
+            const uint32_t d = t;
+            const uint32_t s0 = bin_start(d);
+            uint32_t s1;
+            if (d + 2 < fb)
+                s1 = bin_start(d + 2);
+            else if (!(d & 1u) && fb > 1)
+                s1 = tot_lo;  // last even bin ends where the odd bins start
+            else
+                s1 = tot_lo + (tot >> 16);
+            const uint32_t sz = s1 - s0;
+            uint32_t base = 0;
+            if (sz) base = (uint32_t)atomicAdd(cursor + c * fb + d, (unsigned long long)sz);
+            const uint32_t cap = 1u << fshift;
+            const uint32_t room = base < cap ? cap - base : 0u;
+            s_base[d] = base - s0;                   // slot in window = s_base + tile position
+            s_lim[d] = s0 + (sz < room ? sz : room);  // tile positions past this overflow
+        }
+        // 3. place: slot = scanned prefix of (bin, thread) + rank within the thread
+#pragma unroll
+        for (int j = 0; j < RF_IT; ++j) {
+            const uint32_t d = loc[j] & 0xFFu;
+            if (d != 0xFFu) {
+                const uint32_t v = s_cnt[rf_pad((d >> 1) * RF_THREADS + t)];
+                const uint32_t pos = ((d & 1u) ? (v >> 16) + tot_lo : (v & 0xFFFFu)) + (loc[j] >> 8);
+                unsigned long long pr = rec[j];
+                if (kMode == 1) {
+                    const unsigned long long cur = pr >> sb;
+                    // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
+                    pr = (cur << 32) | (uint32_t)(gv[j] - ((uint32_t)pr & lmask) - 1u);
+                }
+                s_sort[pos] = pr;
+            }
+        }
+        __syncthreads();
+        // 4. write the runs: tile position i of bin d -> window slot s_base[d] + i
+        const uint32_t total = tot_lo + (tot >> 16);
+        unsigned long long* wout = out + (c * fb << fshift);
+        for (uint32_t i = t; i < total; i += RF_THREADS) {
+            const unsigned long long p = s_sort[i];
+            const uint32_t d = (uint32_t)(p >> 32 >> fshift) & fmask;
+            if (i < s_lim[d])
+                __stcs(wout + ((unsigned long long)d << fshift) + (s_base[d] + i), p);
+            else
+                over = true;
+        }
+        __syncthreads();  // s_sort, s_cnt and the bin tables are reused by the next tile
+    }
+    if (over) st->bad = 1;
+}
+
 // one CTA per fine window: scatter its pairs into shared memory, then store
 // the window coalesced
 template <class OutT>
@@ -1716,7 +1911,7 @@ static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t h
 // the defaults are the measured configuration, the switches only exist to
 // re-run the comparisons DESIGN.md records
 struct RsTuning {
-    uint32_t win_kb, kb0, kb1, fin, walk_cap, load_mode, contract, coop, topn, packed, fused;
+    uint32_t win_kb, kb0, kb1, fin, walk_cap, load_mode, contract, coop, topn, packed, fused, refine_cnt;
 };
 static const RsTuning& rs_tuning() {
     static const RsTuning t = [] {
@@ -1732,6 +1927,7 @@ static const RsTuning& rs_tuning() {
         v.topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
         v.packed = env_u32("SG_RS_PACKED", 1, 0, 1);
         v.fused = env_u32("SG_RS_FUSED", 1, 0, 1);
+        v.refine_cnt = env_u32("SG_RS_REFINE_CNT", 1, 0, 1);  // 0: the ballot-ranked refine
         return v;
     }();
     return t;
@@ -2129,7 +2325,15 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
     }
-    if (p.fused) {  // 8 records per thread, 3 CTAs per SM: more warps to hide the IS_1 gathers
+    const uint32_t fbits_r = p.cshift - p.fshift;
+    if (p.fused && (1u << fbits_r) <= (uint32_t)RF_MAXB && rs_tuning().refine_cnt) {
+        const size_t smr = rf_smem_bytes(1u << fbits_r);
+        SG_CUDA(set_smem_max(k_rs_refine_cnt<1>, smr));
+        const uint32_t g = sm_count() * RF_CTAS_PER_SM;
+        rec.begin(K_RS5_REFINE, 0, g, RF_THREADS, n);
+        k_rs_refine_cnt<1><<<g, RF_THREADS, smr, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
+                                                     p.fshift, b.IS[1], p.rec_sb, p.rec_lb);
+    } else if (p.fused) {  // 8 records per thread, 3 CTAs per SM: more warps to hide the IS_1 gathers
         constexpr uint32_t t8 = MS_THREADS * 8;
         const size_t sm8 = (size_t)t8 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), t8);
         const uint32_t fbits = p.cshift - p.fshift;  // ballots per element in the split

@@ -7,7 +7,7 @@ O=gpurun_out/$TAG
 mkdir -p $O
 CS=/usr/local/cuda/bin/compute-sanitizer
 F="--kernel-name kns=sg:: --print-limit 50"
-for tool in memcheck racecheck synccheck initcheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   for part in list cc; do
     extra=""
     [ "$part" = cc ] && export SG_CC_WBITS=12 || unset SG_CC_WBITS

@@ -21,19 +21,24 @@ def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     dev = torch.device("cuda", 0)
     n = int(os.environ.get("SAN_N", 1 << 18))
+    # inputs are generated on the host and copied in: initcheck tracks every
+    # byte, and torch's device sort (the device generators) copies scratch
+    # it never initialised
     if which in ("all", "list"):
-        sl = g.gen_list(n, seed=1, device=dev)
+        sl = g.SuccessorList(torch.from_numpy(g.gen_list(n, seed=1).succ).to(dev))
         r, st = g.rs_rank(sl, 1024)
         print("rs random", st.meta["path"], st.meta["levels"], int(r.max()))
         # enough levels for the multi-CTA top (cooperative) at this size
         o = g.SuccessorList(torch.cat([torch.arange(1, n, device=dev), torch.tensor([n - 1], device=dev)]).to(torch.int32))
         r, st = g.rs_rank(o, 1024)
         print("rs ordered", st.meta["path"], int(r[0]))
-        r, _ = g.wyllie_rank(g.gen_list(1 << 14, seed=2, device=dev), 64)
-        r, _ = g.wyllie_rank(g.gen_list(200, seed=3, device=dev), 128, variant="single_block")
+        r, _ = g.wyllie_rank(g.SuccessorList(torch.from_numpy(g.gen_list(1 << 14, seed=2).succ).to(dev)), 64)
+        r, _ = g.wyllie_rank(g.SuccessorList(torch.from_numpy(g.gen_list(200, seed=3).succ).to(dev)), 128,
+                             variant="single_block")
         print("wyllie ok")
     if which in ("all", "cc"):
-        gr = g.gen_random_graph(n, 4.0 * n / (n * (n - 1) // 2) * 2, seed=0, device=dev)
+        h = g.gen_random_graph(n, 8.0 * n / (n * (n - 1) // 2), seed=0)
+        gr = g.EdgeGraph(n, torch.from_numpy(h.edges).to(dev))
         for variant in ("uf", "sv"):
             lab, st = g.sv_components(gr, 64, variant=variant)
             print("cc", variant, st.meta["rounds"], int(lab.max()))
