@@ -121,6 +121,10 @@ typedef struct sg_violation {
 const char* sg_strerror(int status);
 const char* sg_kernel_name(int kernel_id);
 int sg_version(void);
+/* Re-read the SG_* experiment switches from the environment (they are
+ * otherwise parsed once per process; defaults = the measured configuration).
+ * Not a reference interface: tests use it to force rare paths. */
+int sg_tuning_reload(void);
 /* sha256 (hex, ';'-terminated) of the sources, headers and nvcc flags this
  * library was built from (paper_1002_4482_b200/build.py). */
 const char* sg_source_hash(void);

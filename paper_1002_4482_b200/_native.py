@@ -33,7 +33,7 @@ SG_MAX_LEVELS = 8
 
 # every symbol include/sg.h declares (tests check the export table)
 EXPORTS = (
-    "sg_strerror", "sg_kernel_name", "sg_version", "sg_source_hash", "sg_last_cuda_error", "sg_stats_resolve",
+    "sg_strerror", "sg_kernel_name", "sg_version", "sg_tuning_reload", "sg_source_hash", "sg_last_cuda_error", "sg_stats_resolve",
     "sg_wyllie_workspace_bytes", "sg_rs_workspace_bytes", "sg_wyllie_rank", "sg_rs_rank",
     "sg_gather_i64", "sg_cc_workspace_bytes", "sg_cc", "sg_cc_init", "sg_cc_hook",
     "sg_cc_hook_workspace_bytes", "sg_cc_hook_part", "sg_splitter_meta_workspace_bytes", "sg_splitter_meta",
@@ -73,6 +73,7 @@ _SIGS = {
     "sg_strerror": (ctypes.c_char_p, [_I]),
     "sg_kernel_name": (ctypes.c_char_p, [_I]),
     "sg_version": (_I, []),
+    "sg_tuning_reload": (_I, []),
     "sg_source_hash": (ctypes.c_char_p, []),
     "sg_last_cuda_error": (ctypes.c_char_p, []),
     "sg_stats_resolve": (_I, [ctypes.POINTER(Stats)]),

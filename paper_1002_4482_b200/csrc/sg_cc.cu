@@ -712,8 +712,8 @@ struct CcPlan {
 
 static CcPlan plan_cc(unsigned long long n, unsigned long long m) {
     CcPlan p;
-    const char* e = getenv("SG_CC_WBITS");  // window width switch (tests force small windows with it)
-    uint32_t wbits = e && *e ? (uint32_t)atoi(e) : 23u;  // window of 2^23 vertices = 32 MiB of D
+    const uint32_t tw = tuning().cc_wbits;  // tests force small windows with SG_CC_WBITS
+    uint32_t wbits = tw ? tw : 23u;         // window of 2^23 vertices = 32 MiB of D
     if (wbits < 10) wbits = 10;
     if (wbits > 31) wbits = 31;
     unsigned long long parts = (n + (1ull << wbits) - 1) >> wbits;
@@ -742,13 +742,7 @@ static unsigned long long part_tiles(unsigned long long m) { return (m + MS2_TIL
 // partition mode: count + scatter (default), or the one-pass tile sort
 // (SG_CC_PART=tiles): the tile sort moves 0.5 ms less data at C5, but hooking
 // the per-tile slices costs 1.1 ms more (profiles/r02_cc_partition.txt)
-static bool part_one_pass() {
-    static const bool one = [] {
-        const char* e = getenv("SG_CC_PART");
-        return e && strcmp(e, "tiles") == 0;
-    }();
-    return one;
-}
+static bool part_one_pass() { return tuning().cc_part_tiles != 0; }
 // the one-pass layout needs 16-B aligned input rows (bulk copies); a reused
 // partition (sg_cc_hook_part, reuse = 1) re-derives its layout from this
 static bool use_tiles(const void* edges) { return part_one_pass() && ((uintptr_t)edges & 15) == 0; }

@@ -25,6 +25,23 @@ constexpr unsigned long long NONE64 = ~0ull;
 // persistent grid is sized from it
 int sm_count();
 
+// Experiment switches (SG_* environment variables).  The defaults are the
+// measured configuration; the switches exist to re-run the comparisons
+// DESIGN.md records and to force rare paths in tests.  They are parsed once
+// and again only when sg_tuning_reload() is called (tests do, after
+// changing the environment), never per call.
+struct Tuning {
+    // list ranking (sg_list.cu)
+    uint32_t rs_win_kb, rs_kb0, rs_kb1, rs_fin, rs_walk_cap, rs_load_mode, rs_contract, rs_coop, rs_topn,
+        rs_packed, rs_fused, rs_refine;
+    // components (sg_cc.cu): window bits (0 = default), one-pass tile partition
+    uint32_t cc_wbits, cc_part_tiles;
+    // block multisplit peer ranking (sg_msplit.cuh): 0 match.any, 1 ballots, 2 alternate
+    uint32_t ms_peers;
+    uint32_t generation;  // bumped by every reload
+};
+Tuning tuning();
+
 // Kernel ids; names are returned by sg_kernel_name().  Names follow the
 // reference's phase names where a kernel does that phase's job
 // (listrank.py:197-382, concomp.py:69-205).

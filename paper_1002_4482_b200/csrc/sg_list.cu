@@ -1034,66 +1034,60 @@ __global__ void __launch_bounds__(MS_THREADS, IT >= 16 ? 2 : 3) k_rs_rec_refine2
     if (over) st->bad = 1;
 }
 
-// rs5_refine, counter-ranked (default for <= 64 fine bins).  Same job as
+// rs5_refine, lean (default for <= 64 fine bins).  Same job as
 // k_rs_rec_refine2<.., 1, ..> -- coarse-window records -> {cur, rank} pairs
-// split by fine window -- with the tile ranked by per-thread counters instead
-// of warp ballots (the radix-rank scheme of a block radix sort):
-//   1. every thread counts its RF_IT records per bin in its own column of a
-//      [bin/2][thread] array of packed 16-bit counters (no atomics, no bank
-//      conflicts: a thread only touches its own column),
-//   2. one raking exclusive scan of the packed array gives every (bin,
-//      thread) its first slot in the bin-sorted tile (low halves = even bins
-//      first, then the odd bins: every bin is still one contiguous run),
-//   3. records go to their slot in shared memory; one global atomic per
-//      (tile, bin) claims the run's slots in the fine window; runs leave the
-//      SM as coalesced 8-B stores.
-// All slot arithmetic is 32-bit (a tile holds RF_TILE records).  The next
-// tile streams in (cp.async.bulk) while the current one is ranked; the
-// IS_1[sid] gathers are issued before the counting and first used at the
-// placement.
-constexpr int RF_THREADS = 256;
-constexpr int RF_IT = 16;
-constexpr int RF_TILE = RF_THREADS * RF_IT;  // 4096 records
-constexpr int RF_MAXB = 64;                  // fine bins per coarse window handled here
-constexpr int RF_CTAS_PER_SM = 2;
+// split by fine window (rank = IS_1[sid] - local - 1, listrank.py:375-379) --
+// written for the issue slots and the L1TEX pipe, which the IS_1 gathers
+// already load to ~1 wavefront per record (tools/ubench_l2.cu: ~288 G random
+// L2 sectors/s per GPU, 0.93 ms for 2^28 gathers):
+//   * 32-bit slot and node arithmetic (a tile holds RL_TILE records; node
+//     ids and window slots are < 2^32),
+//   * peer ranking by ballots over the NB bin bits (or match.any, kPeers),
+//     warp counters in shared memory touched by the group leaders only,
+//   * one small pass turns the (warp, bin) counts into absolute tile slots,
+//     so placing a record is one shared load and one shared store,
+//   * runs leave the SM warp by warp, bin by bin (no per-record bin lookup).
+// Persistent, 2 CTAs of 512 threads per SM; the next tile streams in
+// (cp.async.bulk, evict-first) while the current one is split.
+constexpr int RL_THREADS = 512;
+constexpr int RL_WARPS = RL_THREADS / 32;
+constexpr int RL_IT = 8;
+constexpr int RL_TILE = RL_THREADS * RL_IT;  // 4096 records (2^cshift is a multiple)
+constexpr int RL_MAXB = 64;                  // fine bins per coarse window handled here
+constexpr int RL_CTAS_PER_SM = 2;
 
-__device__ __forceinline__ uint32_t rf_pad(uint32_t i) { return i + (i >> 5); }  // one pad word per 32
+static size_t rl_smem_bytes() { return (size_t)RL_TILE * 8 * 2; }
 
-static size_t rf_smem_bytes(uint32_t nb) {
-    const uint32_t words = (nb + 1) / 2 * RF_THREADS;
-    return (size_t)RF_TILE * 8 * 2 + (size_t)(words + (words >> 5)) * 4 + 16;
-}
-
-template <int kMode>  // 1: packed walk records in (ranked here); 0: {cur, rank} pairs in
-__global__ void __launch_bounds__(RF_THREADS, RF_CTAS_PER_SM) k_rs_refine_cnt(
+template <int NB, int kPeers>  // NB: bin bits (fb <= 2^NB <= 64); kPeers: 1 ballots, 0 match.any, 2 alternate
+__global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
     unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
     const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
     if (layout_local(st) || st->overflow) return;
-    const uint32_t fb = 1u << (cshift - fshift);  // <= RF_MAXB
-    const uint32_t W = (fb + 1) / 2;              // counter words per thread
-    extern __shared__ __align__(128) unsigned char rf_raw[];
-    unsigned long long* s_in = reinterpret_cast<unsigned long long*>(rf_raw);
-    unsigned long long* s_sort = s_in + RF_TILE;
-    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_sort + RF_TILE);
+    const uint32_t fb = 1u << (cshift - fshift);  // <= 2^NB
+    extern __shared__ __align__(128) unsigned char rl_raw[];
+    unsigned long long* s_in = reinterpret_cast<unsigned long long*>(rl_raw);
+    unsigned long long* s_sort = s_in + RL_TILE;
     __shared__ unsigned long long bar;
-    __shared__ uint32_t s_wsum[RF_THREADS / 32];
-    __shared__ uint32_t s_base[RF_MAXB], s_lim[RF_MAXB];
-    __shared__ uint32_t s_total;
-    const uint32_t t = threadIdx.x;
-    const uint32_t lane = lane_id(), warp = t >> 5;
-    const unsigned long long ntiles = (n + RF_TILE - 1) / RF_TILE;
-    const unsigned long long R1 = st->R[1];
+    __shared__ uint32_t s_w[RL_WARPS][RL_MAXB];  // per-warp bin counts -> absolute tile slots
+    __shared__ uint32_t s_bs[RL_MAXB + 1];         // bin starts in the sorted tile
+    __shared__ uint32_t s_gb[RL_MAXB];             // window slot of the bin's first tile record
+    __shared__ uint32_t s_ge[RL_MAXB];             // tile end of the bin's writable run
+    __shared__ uint32_t s_half;
+    const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned long long ntiles = (n + RL_TILE - 1) / RL_TILE;
+    const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
     const unsigned long long pol_last = l2_evict_last();
     const uint32_t fmask = fb - 1;
-    const uint32_t lmask = lb >= 32 ? 0xFFFFFFFFu : ((1u << lb) - 1u);
-    const unsigned long long smask = (1ull << (sb - lb)) - 1;
+    const uint32_t lmask = (1u << lb) - 1u;            // lb < 32 (host-checked)
+    const uint32_t smask = (uint32_t)((1ull << (sb - lb)) - 1);
     if (t == 0) mbar_init(&bar, 1);
     __syncthreads();
     auto issue = [&](unsigned long long tile) {
         if (t == 0 && tile < ntiles) {
-            const unsigned long long e0 = tile * RF_TILE;
-            const uint32_t cnt = (uint32_t)min((unsigned long long)RF_TILE, n - e0);
+            const unsigned long long e0 = tile * RL_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)RL_TILE, n - e0);
             const uint32_t bytes = (cnt * 8u + 15u) & ~15u;  // the buffer is padded to whole windows
             mbar_expect_tx(&bar, bytes);
             bulk_g2s_hint(s_in, in + e0, bytes, &bar, l2_evict_first());
@@ -1103,128 +1097,114 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS_PER_SM) k_rs_refine_cnt(
     uint32_t phase = 0;
     issue(blockIdx.x);
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const unsigned long long e0 = tile * RF_TILE;
-        const uint32_t cnt = (uint32_t)min((unsigned long long)RF_TILE, n - e0);
-        const unsigned long long c = e0 >> cshift;  // tiles never straddle a coarse window
-        // zero this thread's counter column while the tile lands
-        for (uint32_t w = 0; w < W; ++w) s_cnt[rf_pad(w * RF_THREADS + t)] = 0u;
+        const unsigned long long e0 = tile * RL_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)RL_TILE, n - e0);
+        const uint32_t c = (uint32_t)(e0 >> cshift);  // tiles never straddle a coarse window
+        if (lane < (uint32_t)RL_MAXB / 2) {         // this warp's counters
+            s_w[warp][lane] = 0u;
+            s_w[warp][lane + RL_MAXB / 2] = 0u;
+        }
         mbar_wait(&bar, phase);
         phase ^= 1u;
-        unsigned long long rec[RF_IT];
-        uint32_t gv[RF_IT];
-        uint32_t loc[RF_IT];  // bin (low 8 bits, 0xFF = skip) | rank among this thread's records of the bin << 8
+        uint32_t cur[RL_IT], gv[RL_IT], loc[RL_IT], bn[RL_IT];
 #pragma unroll
-        for (int g = 0; g < RF_IT / 2; ++g) {
-            const uint32_t e = (g * RF_THREADS + t) * 2;
+        for (int g = 0; g < RL_IT / 2; ++g) {
+            const uint32_t e = (g * RL_THREADS + t) * 2;
             const ulonglong2 v = e < cnt ? reinterpret_cast<const ulonglong2*>(s_in)[e >> 1] : make_ulonglong2(0, 0);
-            rec[2 * g] = v.x;
-            rec[2 * g + 1] = v.y;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const unsigned long long r = q ? v.y : v.x;
-                const unsigned long long cur = kMode == 1 ? (r >> sb) : (r >> 32);
-                if (kMode == 1) {
-                    const unsigned long long o = (r >> lb) & smask;
-                    gv[2 * g + q] = ld_hint(IS1 + (o < R1 ? o : 0), pol_last);
-                }
-                loc[2 * g + q] = (e + q < cnt && (cur >> cshift) == c) ? ((uint32_t)cur >> fshift) & fmask : 0xFFu;
+                const int j = 2 * g + q;
+                cur[j] = (uint32_t)(r >> sb);
+                const uint32_t sid = (uint32_t)(r >> lb) & smask;
+                loc[j] = (uint32_t)r & lmask;
+                // issued now, first used at the placement: the gathers fly while the tile is ranked
+                gv[j] = ld_hint(IS1 + (sid < R1 ? sid : 0u), pol_last);
+                bn[j] = (e + q < cnt && (cur[j] >> cshift) == c) ? (cur[j] >> fshift) & fmask : 0xFFu;
             }
         }
         __syncthreads();  // staging consumed, counters zeroed
         issue(tile + gridDim.x);
-        // 1. count: own column, packed 16-bit halves
+        // rank among the warp's records of the same bin: rk = warp counter before + peers below
 #pragma unroll
-        for (int j = 0; j < RF_IT; ++j) {
-            const uint32_t d = loc[j];
-            if (d != 0xFFu) {
-                const uint32_t a = rf_pad((d >> 1) * RF_THREADS + t);
-                const uint32_t sh = (d & 1u) << 4;
-                const uint32_t v = s_cnt[a];
-                s_cnt[a] = v + (1u << sh);
-                loc[j] = d | (((v >> sh) & 0xFFFFu) << 8);
+        for (int j = 0; j < RL_IT; ++j) {
+            unsigned peers;
+            if (kPeers == 0 || (kPeers == 2 && (j & 1))) {
+                peers = __match_any_sync(0xffffffffu, bn[j]);
+            } else {
+                const bool valid = bn[j] != 0xFFu;
+                const unsigned vb = __ballot_sync(0xffffffffu, valid);
+                peers = valid ? vb : ~vb;
+#pragma unroll
+                for (int k = 0; k < NB; ++k) {
+                    const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
+                    peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+                }
             }
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (bn[j] != 0xFFu && (int)lane == leader) {
+                old = s_w[warp][bn[j]];
+                s_w[warp][bn[j]] = old + __popc(peers);
+            }
+            loc[j] |= (__shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt)) << 20;  // local < 2^12
         }
         __syncthreads();
-        // 2. raking exclusive scan over the packed array, logical order [word][thread]
-        {
-            const uint32_t i0 = t * W;
-            uint32_t sum = 0;
-            for (uint32_t k = 0; k < W; ++k) sum += s_cnt[rf_pad(i0 + k)];
-            uint32_t incl = sum;
+        // (warp, bin) counts -> absolute slots of the bin-sorted tile; one
+        // atomic per non-empty bin claims the bin's run in its fine window
+        if (t < 64) {
+            const uint32_t d = t;
+            uint32_t tot = 0;
+            if (d < fb) {
+#pragma unroll
+                for (int w = 0; w < RL_WARPS; ++w) {
+                    const uint32_t x = s_w[w][d];
+                    s_w[w][d] = tot;
+                    tot += x;
+                }
+            }
+            uint32_t incl = tot;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if ((int)lane >= o) incl += y;
             }
-            if (lane == 31) s_wsum[warp] = incl;
-            __syncthreads();
-            uint32_t run = incl - sum;
+            if (t == 31) s_half = incl;
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            const uint32_t start = incl - tot + (t >= 32 ? s_half : 0u);
+            if (d < fb) {
 #pragma unroll
-            for (int k = 0; k < RF_THREADS / 32; ++k)
-                if (k < (int)warp) run += s_wsum[k];
-            if (t == RF_THREADS - 1) s_total = run + sum;  // packed grand total
-            for (uint32_t k = 0; k < W; ++k) {
-                const uint32_t a = rf_pad(i0 + k);
-                const uint32_t v = s_cnt[a];
-                s_cnt[a] = run;
-                run += v;
+                for (int w = 0; w < RL_WARPS; ++w) s_w[w][d] += start;
+                uint32_t base = 0;
+                if (tot) base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot);
+                const uint32_t cap = 1u << fshift;
+                const uint32_t room = base < cap ? cap - base : 0u;
+                s_bs[d] = start;
+                s_gb[d] = base;
+                s_ge[d] = start + (tot < room ? tot : room);
+                if (d == fb - 1) s_bs[fb] = start + tot;
             }
         }
         __syncthreads();
-        const uint32_t tot = s_total;
-        const uint32_t tot_lo = tot & 0xFFFFu;  // records in even bins: the odd bins follow them
-        auto bin_start = [&](uint32_t d) {      // first slot of bin d in the sorted tile
-            const uint32_t v = s_cnt[rf_pad((d >> 1) * RF_THREADS)];
-            return (d & 1u) ? (v >> 16) + tot_lo : (v & 0xFFFFu);
-        };
-        // bins: start, size, global claim (one atomic per non-empty bin and tile)
-        if (t < fb) {
-            const uint32_t d = t;
-            const uint32_t s0 = bin_start(d);
-            uint32_t s1;
-            if (d + 2 < fb)
-                s1 = bin_start(d + 2);
-            else if (!(d & 1u) && fb > 1)
-                s1 = tot_lo;  // last even bin ends where the odd bins start
-            else
-                s1 = tot_lo + (tot >> 16);
-            const uint32_t sz = s1 - s0;
-            uint32_t base = 0;
-            if (sz) base = (uint32_t)atomicAdd(cursor + c * fb + d, (unsigned long long)sz);
-            const uint32_t cap = 1u << fshift;
-            const uint32_t room = base < cap ? cap - base : 0u;
-            s_base[d] = base - s0;                   // slot in window = s_base + tile position
-            s_lim[d] = s0 + (sz < room ? sz : room);  // tile positions past this overflow
-        }
-        // 3. place: slot = scanned prefix of (bin, thread) + rank within the thread
+        // place: slot = absolute (warp, bin) slot + rank within the warp
 #pragma unroll
-        for (int j = 0; j < RF_IT; ++j) {
-            const uint32_t d = loc[j] & 0xFFu;
-            if (d != 0xFFu) {
-                const uint32_t v = s_cnt[rf_pad((d >> 1) * RF_THREADS + t)];
-                const uint32_t pos = ((d & 1u) ? (v >> 16) + tot_lo : (v & 0xFFFFu)) + (loc[j] >> 8);
-                unsigned long long pr = rec[j];
-                if (kMode == 1) {
-                    const unsigned long long cur = pr >> sb;
-                    // rank = IS_1[sid] - local - 1 (listrank.py:375-379)
-                    pr = (cur << 32) | (uint32_t)(gv[j] - ((uint32_t)pr & lmask) - 1u);
-                }
-                s_sort[pos] = pr;
+        for (int j = 0; j < RL_IT; ++j) {
+            if (bn[j] != 0xFFu) {
+                const uint32_t pos = s_w[warp][bn[j]] + (loc[j] >> 20);
+                const uint32_t rank = gv[j] - (loc[j] & 0xFFFFFu) - 1u;
+                s_sort[pos] = ((unsigned long long)cur[j] << 32) | rank;
             }
         }
         __syncthreads();
-        // 4. write the runs: tile position i of bin d -> window slot s_base[d] + i
-        const uint32_t total = tot_lo + (tot >> 16);
-        unsigned long long* wout = out + (c * fb << fshift);
-        for (uint32_t i = t; i < total; i += RF_THREADS) {
-            const unsigned long long p = s_sort[i];
-            const uint32_t d = (uint32_t)(p >> 32 >> fshift) & fmask;
-            if (i < s_lim[d])
-                __stcs(wout + ((unsigned long long)d << fshift) + (s_base[d] + i), p);
-            else
-                over = true;
+        // write out: warp w copies the runs of bins w, w + RL_WARPS, ...
+        unsigned long long* wout = out + ((unsigned long long)c * fb << fshift);
+        for (uint32_t d = warp; d < fb; d += RL_WARPS) {
+            const uint32_t s0 = s_bs[d], s1 = s_bs[d + 1], se = s_ge[d];
+            unsigned long long* dst = wout + ((unsigned long long)d << fshift) + s_gb[d];
+            for (uint32_t i = s0 + lane; i < se; i += 32) __stcs(dst + (i - s0), s_sort[i]);
+            if (se < s1) over = true;
         }
-        __syncthreads();  // s_sort, s_cnt and the bin tables are reused by the next tile
+        __syncthreads();  // s_sort and the tables are reused by the next tile
     }
     if (over) st->bad = 1;
 }
@@ -1898,41 +1878,6 @@ struct RsPlan {
     unsigned long long cap[SG_MAX_LEVELS + 1] = {};  // node capacity per level
 };
 
-static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t hi) {
-    const char* s = getenv(name);
-    if (!s || !*s) return dflt;
-    long v = strtol(s, nullptr, 10);
-    if (v < (long)lo) v = lo;
-    if (v > (long)hi) v = hi;
-    return (uint32_t)v;
-}
-
-// experiment switches (SG_RS_* environment variables), read once per process:
-// the defaults are the measured configuration, the switches only exist to
-// re-run the comparisons DESIGN.md records
-struct RsTuning {
-    uint32_t win_kb, kb0, kb1, fin, walk_cap, load_mode, contract, coop, topn, packed, fused, refine_cnt;
-};
-static const RsTuning& rs_tuning() {
-    static const RsTuning t = [] {
-        RsTuning v;
-        v.win_kb = env_u32("SG_RS_WIN_KB", 64, 8, 128);  // fine window: KiB of shared memory in rs5_scatter
-        v.kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);
-        v.kb1 = env_u32("SG_RS_KBITS", 3, 1, 16);  // upper levels: short chains, the walk tail is latency-bound
-        v.fin = env_u32("SG_RS_FINAL", FINAL_CAP, 64, 1u << 20);
-        v.walk_cap = env_u32("SG_RS_WALK_CAP", WALK_CAP_HOPS, 1, 0x7FFFFFFF);
-        v.load_mode = env_u32("SG_WALK_LOAD", 0, 0, 3);
-        v.contract = env_u32("SG_RS_CONTRACT", 1, 0, 1);
-        v.coop = env_u32("SG_RS_COOP", 1, 0, 1);
-        v.topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
-        v.packed = env_u32("SG_RS_PACKED", 1, 0, 1);
-        v.fused = env_u32("SG_RS_FUSED", 1, 0, 1);
-        v.refine_cnt = env_u32("SG_RS_REFINE_CNT", 1, 0, 1);  // 0: the ballot-ranked refine
-        return v;
-    }();
-    return t;
-}
-
 static uint32_t mix32(uint64_t x) {
     x ^= x >> 33;
     x *= 0xff51afd7ed558ccdull;
@@ -1946,8 +1891,8 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     RsPlan p;
     // a fine window fills win_kb (64) KiB of shared memory in rs5_scatter;
     // coarse windows: few enough bins for one multisplit
-    const RsTuning& tu = rs_tuning();
-    const uint32_t win_kb = tu.win_kb;
+    const Tuning tu = tuning();
+    const uint32_t win_kb = tu.rs_win_kb;
     p.fshift = 10;
     while (((size_t)out_bytes << (p.fshift + 1)) <= ((size_t)win_kb << 10)) ++p.fshift;
     uint32_t cs = p.fshift + 1;
@@ -1965,18 +1910,18 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
     p.walk_grid = (uint32_t)wg;
     const unsigned long long warps = wg * (WALK_THREADS / 32);
     p.maxchunks = n / (REC_CH - 32) + warps + 2;
-    const uint32_t kb0 = tu.kb0;
-    const uint32_t kb1 = tu.kb1;
-    const uint32_t fin = tu.fin;
-    p.walk_cap = tu.walk_cap;
-    p.load_mode = (int)tu.load_mode;
-    p.contract = (int)tu.contract;
-    p.coop_top = tu.coop != 0;
+    const uint32_t kb0 = tu.rs_kb0;
+    const uint32_t kb1 = tu.rs_kb1;
+    const uint32_t fin = tu.rs_fin;
+    p.walk_cap = tu.rs_walk_cap;
+    p.load_mode = (int)tu.rs_load_mode;
+    p.contract = (int)tu.rs_contract;
+    p.coop_top = tu.rs_coop != 0;
 
     p.cap[0] = n;
     // a ruler list of at most SG_RS_TOPN (> FINAL_CAP) nodes above level 0 is
     // ranked by multi-CTA pointer jumping (k_rs_top_jump) instead of more walks
-    const unsigned long long topn = tu.topn;
+    const unsigned long long topn = tu.rs_topn;
     unsigned long long N = n;
     while (N > fin && p.levels < SG_MAX_LEVELS - 1 && !(p.levels >= 1 && N <= topn)) {
         const uint32_t kb = p.levels == 0 ? kb0 : kb1;
@@ -1989,7 +1934,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
         p.cap[p.levels] = cap;
         N = exp;
     }
-    if (p.levels > 0 && tu.packed) {
+    if (p.levels > 0 && tu.rs_packed) {
         // field widths: cur needs ceil(log2 n) bits; sid needs room for cap[1]
         // ids plus an all-ones pad value that is never an id
         uint32_t cb = 1, sbits = 1;
@@ -2001,7 +1946,7 @@ static RsPlan plan_rs(uint64_t n, uint64_t seed, int out_bytes) {
             p.rec_sb = 64 - cb;
             const unsigned long long lmax = p.rec_lb >= 32 ? 0xFFFFFFFFull : ((1ull << p.rec_lb) - 1);
             if (p.walk_cap > lmax) p.walk_cap = (uint32_t)lmax;  // longer chains: Wyllie fallback
-            p.fused = p.cbins <= WB_MAXBINS && tu.fused != 0;
+            p.fused = p.cbins <= WB_MAXBINS && tu.rs_fused != 0;
         }
     }
     return p;
@@ -2298,7 +2243,6 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         SG_LAUNCH_CHECK();
     }
     {  // local layouts: expand the contraction
-        const uint32_t nt = (uint32_t)((n + TILE - 1) / TILE);
         const uint32_t eg = grid_for(n / 4 + 1, 256, 1, sm_count() * 8);
         rec.begin(K_RS5_EXPAND, 0, eg, 256, n);
         if (((uintptr_t)rank & 15) == 0)
@@ -2326,13 +2270,28 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         SG_LAUNCH_CHECK();
     }
     const uint32_t fbits_r = p.cshift - p.fshift;
-    if (p.fused && (1u << fbits_r) <= (uint32_t)RF_MAXB && rs_tuning().refine_cnt) {
-        const size_t smr = rf_smem_bytes(1u << fbits_r);
-        SG_CUDA(set_smem_max(k_rs_refine_cnt<1>, smr));
-        const uint32_t g = sm_count() * RF_CTAS_PER_SM;
-        rec.begin(K_RS5_REFINE, 0, g, RF_THREADS, n);
-        k_rs_refine_cnt<1><<<g, RF_THREADS, smr, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift,
-                                                     p.fshift, b.IS[1], p.rec_sb, p.rec_lb);
+    const Tuning tu_r = tuning();
+    // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
+    if (p.fused && fbits_r <= 6 && tu_r.rs_refine != 1 && p.rec_lb < 32 && p.walk_cap < (1u << 20)) {
+        // SG_RS_REFINE: 0 lean + ballots (default), 2 lean + match.any, 3 lean + alternate, 1 the
+        // ms_split_fn refine below
+        const int pm = tu_r.rs_refine == 2 ? 0 : (tu_r.rs_refine == 3 ? 2 : 1);
+        using KL = void (*)(const unsigned long long*, unsigned long long*, unsigned long long*, ListStatus*,
+                            unsigned long long, uint32_t, uint32_t, const uint32_t*, uint32_t, uint32_t);
+        KL kl;
+        if (pm == 0)
+            kl = k_rs_refine_lean<6, 0>;
+        else if (pm == 2)
+            kl = fbits_r <= 4 ? k_rs_refine_lean<4, 2> : k_rs_refine_lean<6, 2>;
+        else
+            kl = fbits_r <= 2 ? k_rs_refine_lean<2, 1>
+                              : (fbits_r <= 4 ? k_rs_refine_lean<4, 1> : k_rs_refine_lean<6, 1>);
+        const size_t smr = rl_smem_bytes();
+        SG_CUDA(set_smem_max(kl, smr));
+        const uint32_t g = sm_count() * RL_CTAS_PER_SM;
+        rec.begin(K_RS5_REFINE, 0, g, RL_THREADS, n);
+        kl<<<g, RL_THREADS, smr, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift, b.IS[1],
+                                      p.rec_sb, p.rec_lb);
     } else if (p.fused) {  // 8 records per thread, 3 CTAs per SM: more warps to hide the IS_1 gathers
         constexpr uint32_t t8 = MS_THREADS * 8;
         const size_t sm8 = (size_t)t8 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), t8);

@@ -28,16 +28,17 @@ constexpr int MS_MAXB = 1024;
 // peer ranking: 0 match.any, 1 ballots, 2 alternate per item (SG_MS_PEERS)
 static __constant__ int g_ms_peers = 1;
 
-// once per device and host thread, only when the switch is set
+// pushes the SG_MS_PEERS switch to the device: once per device and tuning
+// generation, and only when it differs from the default
 static inline void ms_configure() {
-    static const char* e = getenv("SG_MS_PEERS");
-    if (!(e && *e)) return;
-    static thread_local unsigned long long done = 0;
+    const Tuning tu = tuning();
+    if (tu.ms_peers == 1 && tu.generation == 1) return;
+    static thread_local uint32_t done_gen[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && (done >> dev & 1ull)) return;
-    if (dev < 64) done |= 1ull << dev;
-    const int v = atoi(e);
+    if (dev < 0 || dev >= 64 || done_gen[dev] == tu.generation) return;
+    done_gen[dev] = tu.generation;
+    const int v = (int)tu.ms_peers;
     cudaMemcpyToSymbol(g_ms_peers, &v, sizeof(int));
 }
 

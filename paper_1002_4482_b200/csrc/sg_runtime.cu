@@ -166,6 +166,50 @@ int sm_count() {
     return v;
 }
 
+static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t hi) {
+    const char* s = getenv(name);
+    if (!s || !*s) return dflt;
+    long v = strtol(s, nullptr, 10);
+    if (v < (long)lo) v = lo;
+    if (v > (long)hi) v = hi;
+    return (uint32_t)v;
+}
+
+static Tuning read_tuning(uint32_t generation) {
+    Tuning v;
+    v.rs_win_kb = env_u32("SG_RS_WIN_KB", 64, 8, 128);  // fine window: KiB of shared memory in rs5_scatter
+    v.rs_kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);        // level-0 ruler density 2^-kb0
+    v.rs_kb1 = env_u32("SG_RS_KBITS", 3, 1, 16);         // upper levels: short chains (latency-bound tail)
+    v.rs_fin = env_u32("SG_RS_FINAL", 8192, 64, 1u << 20);
+    v.rs_walk_cap = env_u32("SG_RS_WALK_CAP", 1u << 16, 1, 0x7FFFFFFF);  // longer walks -> Wyllie fallback
+    v.rs_load_mode = env_u32("SG_WALK_LOAD", 0, 0, 3);
+    v.rs_contract = env_u32("SG_RS_CONTRACT", 1, 0, 1);
+    v.rs_coop = env_u32("SG_RS_COOP", 1, 0, 1);
+    v.rs_topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
+    v.rs_packed = env_u32("SG_RS_PACKED", 1, 0, 1);
+    v.rs_fused = env_u32("SG_RS_FUSED", 1, 0, 1);
+    v.rs_refine = env_u32("SG_RS_REFINE", 0, 0, 3);  // rs5_refine variant (sg_list.cu)
+    v.cc_wbits = env_u32("SG_CC_WBITS", 0, 0, 31);
+    const char* part = getenv("SG_CC_PART");
+    v.cc_part_tiles = part && strcmp(part, "tiles") == 0;
+    v.ms_peers = env_u32("SG_MS_PEERS", 1, 0, 2);
+    v.generation = generation;
+    return v;
+}
+
+static std::mutex g_tuning_mu;
+static Tuning g_tuning;
+static bool g_tuning_ok = false;
+
+Tuning tuning() {
+    std::lock_guard<std::mutex> lk(g_tuning_mu);
+    if (!g_tuning_ok) {
+        g_tuning = read_tuning(1);
+        g_tuning_ok = true;
+    }
+    return g_tuning;
+}
+
 void apply_tuning() {
     static thread_local int done_mask = 0;
     int dev = 0;
@@ -218,6 +262,13 @@ const char* sg_kernel_name(int id) {
 }
 
 int sg_version(void) { return 1; }
+
+int sg_tuning_reload(void) {
+    std::lock_guard<std::mutex> lk(sg::g_tuning_mu);
+    sg::g_tuning = sg::read_tuning(sg::g_tuning_ok ? sg::g_tuning.generation + 1 : 1);
+    sg::g_tuning_ok = true;
+    return SG_OK;
+}
 
 #ifndef SG_SOURCE_HASH
 #define SG_SOURCE_HASH "unknown"

@@ -51,3 +51,20 @@ def cuda():
 
     _native.lib()
     return torch.device("cuda", 0)
+
+
+@pytest.fixture
+def sg_env(monkeypatch):
+    """Set SG_* experiment switches for one test: the library parses them
+    once, so every change is followed by sg_tuning_reload(), and the
+    defaults are restored (and reloaded) when the test ends."""
+    from paper_1002_4482_b200 import _native
+
+    def set_(**kv):
+        for k, v in kv.items():
+            monkeypatch.setenv(k, str(v))
+        _native.lib().sg_tuning_reload()
+
+    yield set_
+    monkeypatch.undo()
+    _native.lib().sg_tuning_reload()

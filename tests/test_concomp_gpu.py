@@ -206,10 +206,10 @@ def test_building_blocks_c_abi(cuda, orc):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_partitioned_path_small_windows(cuda, orc, monkeypatch, variant):
+def test_partitioned_path_small_windows(cuda, orc, sg_env, variant):
     """Force the windowed (partitioned-edge) hook on small graphs: windows of
     2^12 vertices -> up to 16 partitions."""
-    monkeypatch.setenv("SG_CC_WBITS", "12")
+    sg_env(SG_CC_WBITS="12")
     cases = [g.gen_random_graph(60_000, 5e-5, seed=4), g.gen_tree_graph(70_000, 3, seed=2),
              g.list_to_graph(g.gen_list(66_000, seed=1)), g.gen_random_graph(30_000, 2e-4, seed=9)]
     for gr in cases:
@@ -226,7 +226,7 @@ def test_partitioned_path_small_windows(cuda, orc, monkeypatch, variant):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_sharded_path_on_nccl_single_rank(cuda, orc, monkeypatch, tmp_path, variant):
+def test_sharded_path_on_nccl_single_rank(cuda, orc, sg_env, tmp_path, variant):
     """The edge-sharded product path (dist.sv_components_dist: partitioned
     per-rank hook via sg_cc_hook_part, NCCL min all-reduce, sharded
     shortcut + all-gather) on a one-rank NCCL group, windows forced small so
@@ -235,7 +235,7 @@ def test_sharded_path_on_nccl_single_rank(cuda, orc, monkeypatch, tmp_path, vari
 
     from paper_1002_4482_b200 import dist as sgdist
 
-    monkeypatch.setenv("SG_CC_WBITS", "12")
+    sg_env(SG_CC_WBITS="12")
     store = dist.FileStore(str(tmp_path / "store"), 1)
     dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=cuda)
     try:

@@ -81,11 +81,11 @@ def test_contraction_matches_oracle(cuda, orc, case, n):
     assert np.array_equal(d.cpu().numpy().astype(np.int64), want)
 
 
-def test_contraction_meta_matches_ruling_set(cuda, orc, monkeypatch):
+def test_contraction_meta_matches_ruling_set(cuda, orc, sg_env):
     """The splitter meta is path-independent (derived from the ranks)."""
     succ = block_shuffled(200_000, 50, 4)
     a, sa = g.rs_rank(g.SuccessorList(succ), 256, seed=5)
-    monkeypatch.setenv("SG_RS_CONTRACT", "0")
+    sg_env(SG_RS_CONTRACT="0")
     b, sb = g.rs_rank(g.SuccessorList(succ), 256, seed=5)
     assert sa.meta["path"] == "contract" and sb.meta["path"] == "ruling_set"
     assert np.array_equal(a, b)

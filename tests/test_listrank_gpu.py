@@ -389,9 +389,9 @@ def test_full_size_properties_2_26(cuda, kind):
     assert torch.equal(w, rank)
 
 
-def test_walk_cap_fallback(cuda, orc, monkeypatch):
+def test_walk_cap_fallback(cuda, orc, sg_env):
     """A walk that exceeds the hop cap falls back to pointer jumping."""
-    monkeypatch.setenv("SG_RS_WALK_CAP", "4")
+    sg_env(SG_RS_WALK_CAP="4")
     sl = g.gen_list(50_000, seed=8)
     rank, stats = g.rs_rank(sl, 32)
     assert stats.meta["fallback"] is True
@@ -400,21 +400,21 @@ def test_walk_cap_fallback(cuda, orc, monkeypatch):
 
 @pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("n", [5_000, 300_001, 3_000_017])
-def test_record_paths_match_oracle(cuda, orc, monkeypatch, fused, n):
+def test_record_paths_match_oracle(cuda, orc, sg_env, fused, n):
     """Both level-0 record pipelines: the walk that bins its records by output
     window itself (k_rs_walk_bin, default) and the chunked walk followed by
     rs5_partition (SG_RS_FUSED=0)."""
-    monkeypatch.setenv("SG_RS_FUSED", fused)
+    sg_env(SG_RS_FUSED=fused)
     sl = g.gen_list(n, seed=n % 97)
     rank, _ = g.rs_rank(sl, 256, seed=3)
     assert np.array_equal(rank, orc.seq_rank(sl.succ))
 
 
 @pytest.mark.parametrize("fused", ["1", "0"])
-def test_record_paths_invalid_lists(cuda, monkeypatch, fused):
+def test_record_paths_invalid_lists(cuda, sg_env, fused):
     """Invalid lists overfill some output windows of the binned walk: the
     records are dropped and the reference violation is still reported."""
-    monkeypatch.setenv("SG_RS_FUSED", fused)
+    sg_env(SG_RS_FUSED=fused)
     n = 1_000_003
     base = g.gen_list(n, seed=5).succ
     order = np.argsort(-np.asarray(g.rs_rank(g.SuccessorList(base), 1)[0]))
@@ -432,14 +432,14 @@ def test_record_paths_invalid_lists(cuda, monkeypatch, fused):
 
 
 @pytest.mark.parametrize("topn,coop", [("0", "1"), ("20000", "1"), ("20000", "0"), ("524288", "1")])
-def test_top_level_ranking_paths(cuda, orc, monkeypatch, topn, coop):
+def test_top_level_ranking_paths(cuda, orc, sg_env, topn, coop):
     """The ruler list above level 0 is finished either by more walked levels
     and the one-CTA final (SG_RS_TOPN=0), or by multi-CTA in-place pointer
     jumping once it has at most SG_RS_TOPN rulers (default 2^19): one
     cooperative launch with grid barriers (default) or one launch per round
     (SG_RS_COOP=0)."""
-    monkeypatch.setenv("SG_RS_TOPN", topn)
-    monkeypatch.setenv("SG_RS_COOP", coop)
+    sg_env(SG_RS_TOPN=topn)
+    sg_env(SG_RS_COOP=coop)
     sl = g.gen_list(2_500_003, seed=11)
     rank, st = g.rs_rank(sl, 128, seed=1)
     assert np.array_equal(rank, orc.seq_rank(sl.succ))
@@ -470,3 +470,22 @@ def test_plan_boundaries(cuda, orc, n):
     d = torch.from_numpy(sl.succ.astype(np.int32)).to(cuda)
     out, _ = g.rs_rank(g.SuccessorList(d), 64, seed=2)                     # int32 ranks (device input)
     assert np.array_equal(out.cpu().numpy().astype(np.int64), want)
+
+
+@pytest.mark.parametrize("refine", ["0", "1", "2", "3"])
+def test_refine_variants(cuda, orc, sg_env, refine):
+    """rs5_refine variants (SG_RS_REFINE: 0 lean + ballots, the default; 1 the
+    block multisplit refine; 2 lean + match.any; 3 lean, alternating) on
+    windows shrunk to 8 KiB (SG_RS_WIN_KB=8) so 2^20 nodes already split
+    every coarse window into 8 fine bins and 2^25 nodes into 64 (the C3
+    fan-out): exact against the oracle, and the size-independent rank
+    properties at 2^25."""
+    sg_env(SG_RS_REFINE=refine, SG_RS_WIN_KB=8)
+    sl = g.gen_list((1 << 20) + 7, seed=13)
+    rank, st = g.rs_rank(sl, 256, seed=2)
+    assert st.meta["path"] == "ruling_set"
+    assert np.array_equal(rank, orc.seq_rank(sl.succ))
+    big = g.gen_list((1 << 25) + 3, seed=0, device=cuda, dtype=torch.int32)
+    rank, st = g.rs_rank(big, 16384)
+    assert st.meta["fallback"] is False
+    _check_rank_properties(big.succ, rank)

@@ -8,11 +8,17 @@ mkdir -p $O
 CS=/usr/local/cuda/bin/compute-sanitizer
 F="--kernel-name kns=sg:: --print-limit 50"
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
-  for part in list cc; do
+  for part in list list_top list_walk1 cc; do
     extra=""
     [ "$part" = cc ] && export SG_CC_WBITS=12 || unset SG_CC_WBITS
+    # list_top: 2^20 nodes -> 32768 level-1 rulers, ranked by the cooperative
+    # multi-CTA top (k_rs_top_coop); list_walk1: the same with the top
+    # threshold at 0, so level 1 is walked (k_rs_walk<LevelK>) instead
+    unset SG_RS_TOPN SAN_N
+    [ "$part" = list_top ] && export SAN_N=1048576
+    [ "$part" = list_walk1 ] && export SAN_N=1048576 SG_RS_TOPN=0
     [ "$tool" = racecheck ] && extra="--racecheck-report all"
-    timeout 900 $CS --tool $tool $F $extra python tools/sanitize_driver.py $part > $O/san_${tool}_${part}.txt 2>&1
+    timeout 900 $CS --tool $tool $F $extra python tools/sanitize_driver.py ${part%%_*} > $O/san_${tool}_${part}.txt 2>&1
     echo "$tool $part rc=$?" >> $O/san_summary.txt
     tail -n 3 $O/san_${tool}_${part}.txt >> $O/san_summary.txt
   done

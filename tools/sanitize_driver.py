@@ -27,7 +27,8 @@ def main():
     if which in ("all", "list"):
         sl = g.SuccessorList(torch.from_numpy(g.gen_list(n, seed=1).succ).to(dev))
         r, st = g.rs_rank(sl, 1024)
-        print("rs random", st.meta["path"], st.meta["levels"], int(r.max()))
+        print("rs random", st.meta["path"], st.meta["levels"], st.meta["level_size"], int(r.max()),
+              sorted({(x.kernel, x.blocks) for x in st.launch_log if x.kernel.startswith("rs4")}))
         # enough levels for the multi-CTA top (cooperative) at this size
         o = g.SuccessorList(torch.cat([torch.arange(1, n, device=dev), torch.tensor([n - 1], device=dev)]).to(torch.int32))
         r, st = g.rs_rank(o, 1024)
