@@ -117,6 +117,19 @@ typedef struct sg_violation {
     int64_t index;
 } sg_violation;
 
+/* ---- boundary copies (host int64 <-> device 32-bit ids) ------------------
+ * The reference's arrays are int64 (core.py:77-110); the kernels take 32-bit
+ * ids.  These copies narrow / widen on host threads, pipelined against the
+ * DMA through a pinned staging ring (sg_xfer.cu).  Both are synchronous for
+ * the host arrays (they may be reused on return) and ordered on `stream`.
+ *   sg_h2d_narrow_i64: *in_range = 0 if a value lies outside [0, bound)
+ *     (the device copy is then incomplete; copy int64 instead so the device
+ *     reports the exact error).
+ *   sg_d2h_widen_u32: waits for the stream's earlier work on `dev`. */
+int sg_h2d_narrow_i64(const int64_t* host, uint64_t count, uint32_t* dev, uint64_t bound, void* stream,
+                      int* in_range);
+int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* stream);
+
 /* ---- library ------------------------------------------------------------ */
 const char* sg_strerror(int status);
 const char* sg_kernel_name(int kernel_id);

@@ -40,17 +40,50 @@ def dtype_code(t):
     raise TypeError(f"unsupported index dtype {t.dtype}")
 
 
-def to_device(x, device):
+# host arrays at least this long cross PCIe as 32-bit ids (narrowed / widened
+# on the host, pipelined against the DMA: sg_xfer.cu); shorter ones move as
+# int64, where the pipeline's setup would cost more than the bytes it saves
+NARROW_MIN = 1 << 20
+
+
+def _narrow_h2d(addr, shape, count, bound, device):
+    d = torch.empty(shape, dtype=torch.int32, device=device)
+    ok = ctypes.c_int(1)
+    _native.check(_native.lib().sg_h2d_narrow_i64(ctypes.c_void_p(addr), count, ptr(d), bound, stream_ptr(device),
+                                                  ctypes.byref(ok)), "sg_h2d_narrow_i64")
+    return d if ok.value else None
+
+
+def to_device(x, device, bound=None):
     """numpy / host tensor / device tensor -> contiguous CUDA tensor on `device`.
-    Returns (tensor, was_host)."""
+    Returns (tensor, was_host).  With `bound` (ids lie in [0, bound) for a
+    valid input, bound <= 2^31), a long int64 host array arrives as int32:
+    narrowed on the host while earlier chunks are in flight; a value outside
+    the bound falls back to the int64 copy, so the device reports the
+    reference's exact error."""
     if isinstance(x, torch.Tensor):
         if x.is_cuda:
             if x.device != device:
                 raise ValueError(f"input lives on {x.device}, expected {device}")
             return x.contiguous(), False
-        return x.contiguous().to(device, non_blocking=x.is_pinned()), True
+        h = x.contiguous()
+        if bound is not None and bound <= 2**31 and h.dtype == torch.int64 and h.numel() >= NARROW_MIN:
+            d = _narrow_h2d(h.data_ptr(), tuple(h.shape), h.numel(), bound, device)
+            if d is not None:
+                return d, True
+        return h.to(device, non_blocking=h.is_pinned()), True
     arr = np.ascontiguousarray(x)
+    if bound is not None and bound <= 2**31 and arr.dtype == np.int64 and arr.size >= NARROW_MIN:
+        d = _narrow_h2d(arr.ctypes.data, arr.shape, arr.size, bound, device)
+        if d is not None:
+            return d, True
     return torch.from_numpy(arr).to(device), True
+
+
+def host_out_dtype(n):
+    """Device dtype of a result that goes back to a host caller: int32 when
+    it is long enough to cross PCIe narrowed (to_host_numpy widens it)."""
+    return torch.int32 if NARROW_MIN <= n < 2**31 else torch.int64
 
 
 def workspace(nbytes, device):
@@ -94,10 +127,15 @@ def exec_stats(st):
 
 
 def to_host_numpy(t):
-    """D2H through a (cached) pinned buffer -> numpy int64 array that owns
-    the pinned block.  Pageable copies run at a fraction of PCIe speed."""
-    t = t.to(torch.int64)
+    """Device ids -> numpy int64 array owning a pinned block (torch's pinned
+    caching allocator: no page faults, full PCIe speed).  A long int32 result
+    crosses PCIe as 32 bits and is widened on the host, chunk by chunk behind
+    the copy (sg_d2h_widen_u32)."""
     host = torch.empty(t.shape, dtype=torch.int64, pin_memory=True)
-    host.copy_(t, non_blocking=True)
+    if t.dtype == torch.int32 and t.numel() >= NARROW_MIN and t.is_contiguous():
+        _native.check(_native.lib().sg_d2h_widen_u32(ptr(t), t.numel(), ctypes.c_void_p(host.data_ptr()),
+                                                    stream_ptr(t.device)), "sg_d2h_widen_u32")
+        return host.numpy()
+    host.copy_(t.to(torch.int64), non_blocking=True)
     torch.cuda.current_stream(t.device).synchronize()
     return host.numpy()

@@ -68,11 +68,11 @@ def sv_components(graph, p, backend="simulated", accounting="full", block_size=2
                                and graph.edges.is_cuda else None)
     with torch.cuda.device(dev):
         if m:
-            edges, host_input = _device.to_device(graph.edges, dev)
+            edges, host_input = _device.to_device(graph.edges, dev, bound=n)
         else:
             edges, host_input = torch.empty((0, 2), dtype=torch.int64, device=dev), not graph.on_device
-        labels = torch.empty(n, dtype=torch.int64 if (host_input or edges.dtype == torch.int64) else edges.dtype,
-                             device=dev)
+        ldt = _device.host_out_dtype(n) if host_input else (torch.int64 if edges.dtype == torch.int64 else edges.dtype)
+        labels = torch.empty(n, dtype=ldt, device=dev)
         L = _native.lib()
         ws = _device.workspace(L.sg_cc_workspace_bytes(n, m), dev)
         st = _native.Stats()

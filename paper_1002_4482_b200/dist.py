@@ -259,7 +259,7 @@ def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", 
         edges = graph.edges[row0:row1]
     else:
         row0, edges = shard
-    edges, _ = _device.to_device(edges if edges.shape[0] else np.empty((0, 2), np.int64), dev)
+    edges, _ = _device.to_device(edges if edges.shape[0] else np.empty((0, 2), np.int64), dev, bound=n)
     if int(p) > n:
         raise ValueError(f"more threads ({p}) than vertices ({n})")
     ops = CudaOps(dev)

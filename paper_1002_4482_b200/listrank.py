@@ -126,12 +126,13 @@ def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=
         raise CapabilityError(f"device node ids are 32-bit: n={n} is too large")
     dev = _device.require_cuda(sl.succ.device if isinstance(sl.succ, torch.Tensor) and sl.succ.is_cuda else None)
     with torch.cuda.device(dev):
-        succ, host_input = _device.to_device(sl.succ, dev)
+        succ, host_input = _device.to_device(sl.succ, dev, bound=n)
         if reuse_succ and not scratch_out:
             rank = succ  # ranks overwrite the (device copy of the) successors, listrank.py:186-187
         else:
-            rank = torch.empty(n, dtype=torch.int64 if succ.dtype == torch.int64 or host_input else succ.dtype,
-                               device=dev)
+            odt = _device.host_out_dtype(n) if host_input else (
+                torch.int64 if succ.dtype == torch.int64 else succ.dtype)
+            rank = torch.empty(n, dtype=odt, device=dev)
         st = _native.Stats()
         viol = _native.Violation()
         L = _native.lib()
