@@ -256,7 +256,14 @@ def cpu_cc_baseline(orc, n, edges, logm):
 # our arm
 
 class Ctx:
-    pass
+    @staticmethod
+    def xfer_bytes(count, bound=None):
+        """PCIe bytes the public API moves for `count` int64 host ids: long
+        arrays cross as 32-bit ids (paper_1002_4482_b200/_device.py
+        NARROW_MIN, sg_xfer.cu), short ones as int64."""
+        from paper_1002_4482_b200._device import NARROW_MIN
+
+        return 4 * count if count >= NARROW_MIN else 8 * count
 
 
 def measure(a, ctx, name, primary):
@@ -421,7 +428,7 @@ def e2e_run(a, ctx, kind, n, m, dev_input):
 
         def step():
             return g.rs_rank(g.SuccessorList(host), a.p, seed=0)
-        h2d, d2h = 8 * n, 8 * n
+        h2d = d2h = ctx.xfer_bytes(n)
     else:
         host = dev_input.edges.to(torch.int64).cpu().pin_memory()
 
@@ -429,8 +436,8 @@ def e2e_run(a, ctx, kind, n, m, dev_input):
             if world == 1:
                 return g.sv_components(g.EdgeGraph(n, host), 1024, variant=a.variant)
             return sgdist.sv_components_dist(g.EdgeGraph(n, host), 1024, variant=a.variant)
-        h2d = 16 * m // world
-        d2h = 8 * n
+        h2d = ctx.xfer_bytes(2 * (m // world), bound=n)
+        d2h = ctx.xfer_bytes(n)
     outs = [step()[0] for _ in range(3)]  # warm: the pinned host-allocator cache fills on the first calls
     del outs
     steps = max(3, min(a.steps, 10))

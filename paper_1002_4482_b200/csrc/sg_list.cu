@@ -1058,11 +1058,15 @@ constexpr int RL_CTAS_PER_SM = 2;
 
 static size_t rl_smem_bytes() { return (size_t)RL_TILE * 8 * 2; }
 
-template <int NB, int kPeers>  // NB: bin bits (fb <= 2^NB <= 64); kPeers: 1 ballots, 0 match.any, 2 alternate
+// kTiles: the tile keeps its own slot range [tile * RL_TILE, ...) of `out`,
+// sorted by fine bin, and its fb + 1 bin offsets go to toff[tile]; the
+// scatter then collects a fine window's runs from the coarse window's tiles
+// (k_rs_rec_scatter_tiles).  No global atomics, one linear 16-B copy out.
+template <int NB, int kPeers, bool kTiles = false>  // NB: bin bits (fb <= 2^NB <= 64); kPeers: 1 ballots, 0 match.any, 2 alternate
 __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
     unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
-    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
+    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb, uint32_t* __restrict__ toff = nullptr) {
     if (layout_local(st) || st->overflow) return;
     const uint32_t fb = 1u << (cshift - fshift);  // <= 2^NB
     extern __shared__ __align__(128) unsigned char rl_raw[];
@@ -1175,8 +1179,14 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
             if (d < fb) {
 #pragma unroll
                 for (int w = 0; w < RL_WARPS; ++w) s_w[w][d] += start;
+                if (kTiles) {
+                    uint32_t* to = toff + tile * (fb + 1);
+                    to[d] = start;
+                    if (d == fb - 1) to[fb] = start + tot;
+                }
                 uint32_t base = 0;
-                if (tot) base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot);
+                if (!kTiles && tot)
+                    base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot);
                 const uint32_t cap = 1u << fshift;
                 const uint32_t room = base < cap ? cap - base : 0u;
                 s_bs[d] = start;
@@ -1196,6 +1206,15 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
             }
         }
         __syncthreads();
+        if (kTiles) {  // the sorted tile, as is, to its own slots
+            const uint32_t total = s_bs[fb];
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(out + e0);
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(s_sort);
+            for (uint32_t i = t; i < total / 2; i += RL_THREADS) __stcs(dst + i, src[i]);
+            if ((total & 1u) && t == 0) __stcs(out + e0 + total - 1, s_sort[total - 1]);
+            __syncthreads();
+            continue;
+        }
         // write out: warp w copies the runs of bins w, w + RL_WARPS, ...
         unsigned long long* wout = out + ((unsigned long long)c * fb << fshift);
         for (uint32_t d = warp; d < fb; d += RL_WARPS) {
@@ -1207,6 +1226,81 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
         __syncthreads();  // s_sort and the tables are reused by the next tile
     }
     if (over) st->bad = 1;
+}
+
+// rs5_scatter over the tile layout of k_rs_refine_lean<.., true>: one CTA
+// per fine window f (bin d of coarse window c) collects bin d's run from
+// each of the coarse window's tiles -- lane l of a warp reads the run bounds
+// of one tile, the warp then copies the runs four at a time -- scatters the
+// pairs into shared memory and stores the window coalesced.
+template <class OutT>
+__global__ void __launch_bounds__(256) k_rs_rec_scatter_tiles(const unsigned long long* __restrict__ pairs,
+                                                              const uint32_t* __restrict__ toff,
+                                                              OutT* __restrict__ rank, unsigned long long n,
+                                                              uint32_t cshift, uint32_t fshift, const ListStatus* st,
+                                                              int vec) {
+    if (layout_local(st) || ranks_invalid(st)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    OutT* win = reinterpret_cast<OutT*>(smem_raw);
+    const unsigned long long w0 = (unsigned long long)blockIdx.x << fshift;
+    if (w0 >= n) return;
+    const uint32_t size = (uint32_t)min((unsigned long long)1 << fshift, n - w0);
+    const uint32_t mask = (1u << fshift) - 1u;
+    const uint32_t fb = 1u << (cshift - fshift);
+    const uint32_t d = blockIdx.x & (fb - 1);
+    const unsigned long long c = (unsigned long long)blockIdx.x >> (cshift - fshift);
+    const unsigned long long t0 = (c << cshift) / RL_TILE;
+    const unsigned long long t1 = min(((c + 1) << cshift), n + RL_TILE - 1) / RL_TILE;  // tiles of window c holding records
+    const uint32_t ntile = (uint32_t)(t1 > t0 ? t1 - t0 : 0);
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    auto put = [&](unsigned long long pr) {
+        const uint32_t cur = (uint32_t)(pr >> 32);
+        if ((cur >> fshift) == (uint32_t)blockIdx.x) win[cur & mask] = (OutT)(uint32_t)pr;
+    };
+    for (uint32_t tb = warp * 32; tb < ntile; tb += 8 * 32) {
+        const uint32_t tl = tb + lane;
+        uint32_t lo = 0, hi = 0;
+        if (tl < ntile) {
+            const uint32_t* to = toff + (t0 + tl) * (fb + 1) + d;
+            lo = __ldg(to);
+            hi = __ldg(to + 1);
+        }
+        const uint32_t nr = min(32u, ntile - tb);
+        for (uint32_t r = 0; r < nr; r += 4) {
+            uint32_t a[4], e[4];
+            const unsigned long long* src[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t rr = min(r + q, 31u);
+                a[q] = __shfl_sync(0xffffffffu, lo, rr);
+                e[q] = (r + q < nr) ? __shfl_sync(0xffffffffu, hi, rr) : a[q];
+                src[q] = pairs + (t0 + tb + rr) * RL_TILE;
+            }
+            for (uint32_t k = lane;; k += 32) {
+                bool any = false;
+                unsigned long long v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool ok = a[q] + k < e[q];
+                    v[q] = ok ? __ldcs(src[q] + a[q] + k) : ~0ull;
+                    any |= a[q] + k - lane < e[q];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (v[q] != ~0ull) put(v[q]);
+                if (!__any_sync(0xffffffffu, any)) break;
+            }
+        }
+    }
+    __syncthreads();
+    if (vec && size == (1u << fshift)) {
+        constexpr uint32_t V = 16 / sizeof(OutT);
+        const uint4* s4 = reinterpret_cast<const uint4*>(win);
+        uint4* dst = reinterpret_cast<uint4*>(rank + w0);
+        for (uint32_t i = threadIdx.x; i < size / V; i += blockDim.x) __stcs(dst + i, s4[i]);
+        return;
+    }
+    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) rank[w0 + i] = win[i];
 }
 
 // one CTA per fine window: scatter its pairs into shared memory, then store
@@ -1961,6 +2055,7 @@ struct RsBufs {
     unsigned long long* rec_sl = nullptr;
     unsigned long long* pairs = nullptr;
     unsigned long long* cursor = nullptr;  // coarse cursors, then fine cursors
+    uint32_t* toff = nullptr;              // rs5_refine tile layout: fine-bin offsets per refine tile
     uint32_t* tiles = nullptr;
     uint32_t* tiles_end = nullptr;
     uint32_t* tiles_up = nullptr;   // levels >= 1 (level 0's offsets stay for the contraction expand)
@@ -1984,6 +2079,7 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
         b.rec_sl = c.take<unsigned long long>(nrec > npad ? nrec : npad);  // reused by rs5_refine
         b.pairs = c.take<unsigned long long>((unsigned long long)p.cbins << p.cshift);
         b.cursor = c.take<unsigned long long>(p.cbins + p.nwin);
+        b.toff = c.take<uint32_t>(p.fused ? (npad / RL_TILE + 1) * (RL_MAXB + 1) : 0);
     }
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     b.tiles = c.take<uint32_t>(ntiles + 1);
@@ -2272,14 +2368,20 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     const uint32_t fbits_r = p.cshift - p.fshift;
     const Tuning tu_r = tuning();
     // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
-    if (p.fused && fbits_r <= 6 && tu_r.rs_refine != 1 && p.rec_lb < 32 && p.walk_cap < (1u << 20)) {
-        // SG_RS_REFINE: 0 lean + ballots (default), 2 lean + match.any, 3 lean + alternate, 1 the
-        // ms_split_fn refine below
+    const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
+    bool tiled = false;
+    if (lean_ok && tu_r.rs_refine != 1) {
+        // SG_RS_REFINE: 0 lean + ballots (default), 2 lean + match.any, 3 lean + alternate,
+        // 4 lean + ballots in the tile layout (k_rs_rec_scatter_tiles); 1 the ms_split_fn refine below
+        tiled = tu_r.rs_refine == 4;
         const int pm = tu_r.rs_refine == 2 ? 0 : (tu_r.rs_refine == 3 ? 2 : 1);
         using KL = void (*)(const unsigned long long*, unsigned long long*, unsigned long long*, ListStatus*,
-                            unsigned long long, uint32_t, uint32_t, const uint32_t*, uint32_t, uint32_t);
+                            unsigned long long, uint32_t, uint32_t, const uint32_t*, uint32_t, uint32_t, uint32_t*);
         KL kl;
-        if (pm == 0)
+        if (tiled)
+            kl = fbits_r <= 2 ? k_rs_refine_lean<2, 1, true>
+                              : (fbits_r <= 4 ? k_rs_refine_lean<4, 1, true> : k_rs_refine_lean<6, 1, true>);
+        else if (pm == 0)
             kl = k_rs_refine_lean<6, 0>;
         else if (pm == 2)
             kl = fbits_r <= 4 ? k_rs_refine_lean<4, 2> : k_rs_refine_lean<6, 2>;
@@ -2291,7 +2393,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         const uint32_t g = sm_count() * RL_CTAS_PER_SM;
         rec.begin(K_RS5_REFINE, 0, g, RL_THREADS, n);
         kl<<<g, RL_THREADS, smr, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift, b.IS[1],
-                                      p.rec_sb, p.rec_lb);
+                                      p.rec_sb, p.rec_lb, b.toff);
     } else if (p.fused) {  // 8 records per thread, 3 CTAs per SM: more warps to hide the IS_1 gathers
         constexpr uint32_t t8 = MS_THREADS * 8;
         const size_t sm8 = (size_t)t8 * 8 + MsSmem::bytes(1u << (p.cshift - p.fshift), t8);
@@ -2311,10 +2413,17 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     }
     rec.end();
     SG_LAUNCH_CHECK();
-    SG_CUDA(set_smem_max(k_rs_rec_scatter<OutT>, sizeof(OutT) << p.fshift));
-    rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);
-    k_rs_rec_scatter<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(
-        b.rec_sl, rank, n, p.fshift, b.st, ((uintptr_t)rank & 15) == 0 ? 1 : 0);
+    if (tiled) {
+        SG_CUDA(set_smem_max(k_rs_rec_scatter_tiles<OutT>, sizeof(OutT) << p.fshift));
+        rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);
+        k_rs_rec_scatter_tiles<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(
+            b.rec_sl, b.toff, rank, n, p.cshift, p.fshift, b.st, ((uintptr_t)rank & 15) == 0 ? 1 : 0);
+    } else {
+        SG_CUDA(set_smem_max(k_rs_rec_scatter<OutT>, sizeof(OutT) << p.fshift));
+        rec.begin(K_RS5_SCATTER, 0, (uint32_t)p.nwin, 256, n);
+        k_rs_rec_scatter<OutT><<<(uint32_t)p.nwin, 256, sizeof(OutT) << p.fshift, s>>>(
+            b.rec_sl, rank, n, p.fshift, b.st, ((uintptr_t)rank & 15) == 0 ? 1 : 0);
+    }
     rec.end();
     SG_LAUNCH_CHECK();
     if (stats) {

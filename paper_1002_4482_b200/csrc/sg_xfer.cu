@@ -17,6 +17,7 @@
 // Data conversion only -- no ranking or labelling is computed here.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -38,6 +39,10 @@ class Pool {
     Pool() {
         unsigned hw = std::thread::hardware_concurrency();
         nthreads_ = (int)std::max(1u, std::min(hw ? hw : 1u, 32u));
+        if (const char* e = getenv("SG_XFER_THREADS")) {  // experiment switch (read once, at first use)
+            const int v = atoi(e);
+            if (v >= 1 && v <= 256) nthreads_ = v;
+        }
         for (int i = 1; i < nthreads_; ++i) workers_.emplace_back([this, i] { loop(i); });
     }
     ~Pool() {
