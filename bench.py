@@ -165,46 +165,75 @@ class ClockSampler:
         self.max_mhz = None
         self.err = None
 
+    # the sampler polls NVML in a child process (no GIL shared with the timed
+    # loop), timestamps each sample on CLOCK_MONOTONIC and the parent keeps the
+    # samples inside [start, stop]
+    CHILD = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+uuid, index, period, util_on = sys.argv[1], int(sys.argv[2]), float(sys.argv[3]), sys.argv[4] == "1"
+try:
+    h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+except Exception:
+    h = pynvml.nvmlDeviceGetHandleByIndex(index)
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+import select
+while True:
+    r, _, _ = select.select([sys.stdin], [], [], period)
+    if r:
+        break
+    try:
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu if util_on else 1
+        print(time.monotonic(), sm, rs, util, flush=True)
+    except Exception:
+        pass
+"""
+
+    # NVML queries go through the driver and stall the CUDA calls of the timed
+    # process while they run: 2 ms polling cost lr28 ~15 % (measured, r02j),
+    # so the sampler polls every PERIOD_MS (still several samples per workload)
+    PERIOD_MS = float(os.environ.get("SG_BENCH_POLL_MS", "20"))
+
     def start(self):
-        import threading
+        import subprocess
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = None
-            try:  # NVML enumerates every GPU of the host: match the CUDA device by UUID
-                import torch
-                uuid = str(torch.cuda.get_device_properties(self.index).uuid)
-                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
-            except Exception:  # noqa: BLE001
-                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            self.proc = subprocess.Popen([sys.executable, "-c", self.CHILD, uuid, str(self.index),
+                                          str(self.PERIOD_MS / 1e3), os.environ.get("SG_BENCH_POLL_UTIL", "0")],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+            first = self.proc.stdout.readline().split()
+            if not first or first[0] != "max":
+                raise RuntimeError("sampler did not start")
+            self.max_mhz = int(first[1])
         except Exception as e:  # noqa: BLE001
             self.err = f"nvml unavailable: {e}"
+            self.proc = None
             return
+        self.thread = True
 
-        def run():
-            while not self.stop_flag:
-                try:
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
-                    self.samples.append((sm, rs, util))
-                except Exception:  # noqa: BLE001
-                    pass
-                time.sleep(0.002)
-        self.thread = threading.Thread(target=run, daemon=True)
-        self.thread.start()
+    def mark(self):
+        """Open the sampled window (after warm-up, right before the timed loop)."""
+        self.t0 = time.monotonic()
 
     def stop(self):
-        if self.thread is None:
+        if self.thread is None or self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "not sampled"], "samples": 0}
-        self.stop_flag = True
-        self.thread.join()
+        t1 = time.monotonic()
+        out, _ = self.proc.communicate("stop\n", timeout=30)
+        t0 = getattr(self, "t0", 0.0)
+        for line in out.splitlines():
+            f = line.split()
+            if len(f) == 4 and t0 <= float(f[0]) <= t1:
+                self.samples.append((int(f[1]), int(f[2]), int(f[3])))
         busy = [s for s in self.samples if s[2] > 0] or self.samples
         reasons = sorted(nm for nm, bit in self.REASONS.items() if any(s[1] & bit for s in busy))
         sm = [s[0] for s in busy]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(busy), "source": "nvml, 2 ms polling during the timed region"}
+                "samples": len(busy), "source": f"nvml, {self.PERIOD_MS:g} ms polling in a child process during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -303,16 +332,17 @@ def measure(a, ctx, name, primary):
         inp = gd
     torch.cuda.synchronize(dev)
 
+    clocks = ClockSampler(ctx.local)
+    clocks.start()
     for _ in range(a.warmup):
         out = step()
     del out
-    clocks = ClockSampler(ctx.local)
-    clocks.start()
     stream = torch.cuda.current_stream(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     launches = 0
     kern_ms = {}
     ctx.barrier()
+    clocks.mark()
     wall0 = time.perf_counter()
     for k in range(a.steps):
         if need_flush:
@@ -368,7 +398,10 @@ def measure(a, ctx, name, primary):
                                       "contraction moves ~20 B/node, so frac can exceed 1") if kind == "list"
                              else ("SURVEY 8(d) E*72*m + V*40*n (per rank): every parent gather charged a 32-B "
                                    "DRAM sector although the window partition serves them from L2")}}
+    srt = sorted(step_ms)
     res = {"value": round(value, 1), "unit": unit, "ms_per_step": round(ms_per_step, 4), "steps": a.steps,
+           "step_ms_spread": {"min": round(srt[0], 4), "median": round(srt[len(srt) // 2], 4),
+                              "max": round(srt[-1], 4)},
            "warmup": a.warmup, "config": config,
            "algorithm": ("rs_rank (listrank.py:411): recursive sparse ruling set on scattered layouts, tile "
                          "contraction on local layouts" if kind == "list" else

@@ -452,182 +452,193 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
 }
 
 // ---------------------------------------------------------------------------
-// One-pass partition: a tile-local sort by window.
+// One-pass partition into per-window chunk lists.
 //
-// Tile t (TT = MS2_TILE edges) is staged into shared memory by a bulk copy,
-// validated (first bad global row, core.py:196-206), ranked by window with
-// the ballot peer ranking of sg_msplit.cuh, sorted in shared memory and
-// written back to ITS OWN slot range [t*TT, (t+1)*TT) of the copy, with the
-// P+1 window offsets of the tile in toff[t].  No count pass and no global
-// atomics: every edge is read once and written once.  The hook of window k
-// then walks the k-th slice of every tile, tiles in order, so the edge order
-// inside a window is the stable partition's.
-constexpr int TP_CTAS_PER_SM = 2;
+// Every edge is read once and written once, with no count pass and no
+// shared-memory sort.  Each CTA keeps, per window, a reservation counter in
+// shared memory over its own stream of chunks (CC_CHUNK rows, 8 KiB each).
+// Per 32 edges a warp ranks its lanes by window with NB + 1 ballots; lane w
+// reserves window w's rows with one shared atomic and claims the chunk(s)
+// its range starts (a global bump allocator hands out the chunk, whose id
+// lands in the window's directory and the CTA's chunk list); every lane then
+// stores its edge straight into the chunk -- a warp's stores are at most P
+// contiguous runs.  No barriers inside the loop: warps stream independently.
+// At the end each CTA pads its open chunks with (0, 0) rows, which the hook
+// skips (equal parents), so a window is a whole number of chunks and the
+// hook walks its directory as one virtual contiguous range (EdgesChunked).
+//
+// The edge order inside a window is the claim order of the chunks: the warps
+// walk 64-row groups grid-stride, so it is the input order up to the ~grid x
+// 64 x warps rows in flight and the D[u] side of the hook stays a streaming
+// window of D.  (A tile-local sort written back in place, r02a/b, left
+// ~65k short slices per window for the hook and lost 1.1 ms there:
+// profiles/r02_cc_partition.txt.)
+constexpr int CC_CHUNK_BITS = 10;
+constexpr uint32_t CC_CHUNK = 1u << CC_CHUNK_BITS;
+constexpr int PD_THREADS = 256;
+constexpr int PD_CTAS_PER_SM = 6;
+constexpr uint32_t PD_RING = 16;  // chunk ids of the last PD_RING chunks per window, in shared memory
 
-template <class E, int NB, bool kNarrow>
-__global__ void __launch_bounds__(MS_THREADS, TP_CTAS_PER_SM) k_cc_part_tiles(
+struct EdgesChunked {
+    static constexpr uint32_t kBytes = 8;
+    const uint2* e;       // chunk c = rows [c*CC_CHUNK, (c+1)*CC_CHUNK)
+    const uint32_t* dir;  // the window's chunk ids in claim order
+    __device__ __forceinline__ void load(unsigned long long i, unsigned long long& u, unsigned long long& v) const {
+        const uint32_t c = __ldg(dir + (i >> CC_CHUNK_BITS));
+        const uint2 x = __ldcs(e + (((unsigned long long)c << CC_CHUNK_BITS) | (i & (CC_CHUNK - 1))));
+        u = x.x;
+        v = x.y;
+    }
+};
+
+template <class E, int NB, bool kNarrow, bool kMatch>
+__global__ void __launch_bounds__(PD_THREADS, PD_CTAS_PER_SM) k_cc_part_chunks(
     E edges, unsigned long long m, unsigned long long n, unsigned long long row0, uint32_t shift, int P,
-    uint32_t* __restrict__ toff, uint2* __restrict__ out, unsigned long long* flags) {
-    extern __shared__ __align__(128) unsigned char ms_raw[];
-    unsigned char* stage = ms_raw;
-    unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(ms_raw + MS2_TILE * E::kBytes);
-    __shared__ uint32_t s_w[MS_WARPS][MAX_PARTS];   // per-warp counts, then per-warp offsets
-    __shared__ uint32_t s_start[MAX_PARTS + 1];
-    __shared__ unsigned long long bar;
-    const unsigned long long ntiles = (m + MS2_TILE - 1) / MS2_TILE;
+    uint2* __restrict__ out, uint32_t* __restrict__ dir, unsigned long long dir_stride,
+    uint32_t* __restrict__ counts /* [MAX_PARTS] chunks per window, [MAX_PARTS] chunks claimed */,
+    uint32_t* __restrict__ cta_list /* [grid][P][kmax] the CTA's chunks per window */, uint32_t kmax,
+    unsigned long long* flags) {
+    __shared__ uint32_t s_fill[MAX_PARTS];
+    __shared__ unsigned long long s_ring[MAX_PARTS][PD_RING];  // (k + 1) << 32 | chunk id
     const uint32_t lane = lane_id();
-    const int w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    uint32_t* my_list = cta_list + (size_t)blockIdx.x * P * kmax;
+    for (uint32_t i = threadIdx.x; i < MAX_PARTS * PD_RING; i += PD_THREADS) (&s_ring[0][0])[i] = 0ull;
     __syncthreads();
-    auto issue = [&](unsigned long long tile) {
-        if (threadIdx.x == 0 && tile < ntiles) {
-            const unsigned long long e0 = tile * MS2_TILE;
-            const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, m - e0);
-            const uint32_t full = cnt * E::kBytes & ~15u;
-            if (full) {
-                mbar_expect_tx(&bar, full);
-                bulk_g2s_hint(stage, reinterpret_cast<const unsigned char*>(edges.e) + e0 * E::kBytes, full, &bar,
-                              l2_evict_first());
-            } else {
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar)) : "memory");
-            }
+    // chunk k + 1 of a window is claimed when chunk k starts filling, so a
+    // writer finds its chunk id already published (no wait on the claim's
+    // atomic); chunk 0 is claimed here
+    auto preclaim = [&](uint32_t w, uint32_t k) {
+        const uint32_t c = atomicAdd(counts + MAX_PARTS, 1u);
+        my_list[w * kmax + k] = c;
+        __threadfence_block();
+        *reinterpret_cast<volatile unsigned long long*>(&s_ring[w][k % PD_RING]) =
+            ((unsigned long long)(k + 1) << 32) | c;
+    };
+    if (threadIdx.x < (uint32_t)P) {
+        s_fill[threadIdx.x] = 0;
+        preclaim(threadIdx.x, 0);
+    }
+    __syncthreads();
+    auto chunk_of = [&](uint32_t w, uint32_t k) -> uint32_t {
+        const volatile unsigned long long* slot = &s_ring[w][k % PD_RING];
+        for (;;) {  // published when chunk k - 1 started: at most a short wait
+            const unsigned long long x = *slot;
+            const uint32_t tag = (uint32_t)(x >> 32);
+            if (tag == k + 1) return (uint32_t)x;
+            if (tag > k + 1) return *reinterpret_cast<volatile uint32_t*>(my_list + w * kmax + k);  // slot reused
         }
     };
-    uint32_t phase = 0;
-    issue(blockIdx.x);
-    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const unsigned long long e0 = tile * MS2_TILE;
-        const uint32_t cnt = (uint32_t)min((unsigned long long)MS2_TILE, m - e0);
-        const uint32_t staged = (cnt * E::kBytes & ~15u) / E::kBytes;
-        mbar_wait(&bar, phase);
-        phase ^= 1u;
-        if (lane < MAX_PARTS) s_w[w][lane] = 0;
-        unsigned long long pr[MS2_ITEMS];
-        uint32_t bn[MS2_ITEMS];
-#pragma unroll
-        for (int j = 0; j < MS2_ITEMS; ++j) {
-            const uint32_t e = j * MS_THREADS + threadIdx.x;
-            unsigned long long u = n, v = n;
-            if (e < staged)
-                E::decode(stage, e, u, v);
-            else if (e < cnt)
-                edges.load(e0 + e, u, v);  // the odd tail element of the last tile
-            bool ok = false;
-            if (e < cnt) {
-                const bool oob = kNarrow ? ((uint32_t)u >= (uint32_t)n || (uint32_t)v >= (uint32_t)n)
-                                         : (u >= n || v >= n);
-                if (oob)
-                    atomicMax(flags + 1, ~(row0 + e0 + e));
-                else if ((uint32_t)u == (uint32_t)v)
-                    atomicMax(flags + 2, ~(row0 + e0 + e));
-                else
-                    ok = true;
+    // chunk k of window w takes its first row: it joins the window's directory
+    // (the hook's order) and chunk k + 1 is claimed
+    auto activate = [&](uint32_t w, uint32_t k) {
+        const uint32_t c = chunk_of(w, k);
+        const uint32_t d = atomicAdd(counts + w, 1u);
+        dir[w * dir_stride + d] = c;
+        preclaim(w, k + 1);
+    };
+    // invalid rows (range / self-loop, core.py:196-206) are flagged off the fast path
+    auto flag_bad = [&](unsigned long long e, unsigned long long u, unsigned long long v) {
+        const bool oob = kNarrow ? ((uint32_t)u >= (uint32_t)n || (uint32_t)v >= (uint32_t)n) : (u >= n || v >= n);
+        if (oob)
+            atomicMax(flags + 1, ~(row0 + e));
+        else if ((uint32_t)u == (uint32_t)v)
+            atomicMax(flags + 2, ~(row0 + e));
+    };
+    const uint32_t n32 = (uint32_t)min(n, 0xFFFFFFFFull);
+    // ok: valid row (range and self-loop checks done by the caller for four rows at once)
+    auto place = [&](bool ok, unsigned long long u, unsigned long long v) {
+        const uint32_t b = ok ? max((uint32_t)u, (uint32_t)v) >> shift : 0xFFFFFFFFu;
+        uint32_t base = 0, q = 0;
+        if (kMatch) {
+            // peers by match.any; the group leader reserves the group's rows with one shared atomic
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            const int leader = __ffs(peers) - 1;
+            if (ok && (int)lane == leader) {
+                const uint32_t cnt = __popc(peers);
+                base = atomicAdd(&s_fill[b], cnt);
+                if ((base & (CC_CHUNK - 1)) == 0)
+                    activate(b, base >> CC_CHUNK_BITS);
+                else if (((base + cnt - 1) >> CC_CHUNK_BITS) != (base >> CC_CHUNK_BITS))
+                    activate(b, (base + cnt - 1) >> CC_CHUNK_BITS);
             }
-            pr[j] = ((unsigned long long)(uint32_t)v << 32) | (uint32_t)u;
-            bn[j] = ok ? max((uint32_t)u, (uint32_t)v) >> shift : (uint32_t)MS_MAXB;
-        }
-        __syncthreads();  // staging consumed (and s_w zeroed): refill it behind the sort
-        issue(tile + gridDim.x);
-        uint32_t rk[MS2_ITEMS];
-#pragma unroll
-        for (int j = 0; j < MS2_ITEMS; ++j) {
-            const bool valid = bn[j] < (uint32_t)P;
-            const unsigned vb = __ballot_sync(0xffffffffu, valid);
-            unsigned peers = valid ? vb : ~vb;
+            q = __shfl_sync(0xffffffffu, base, leader) + __popc(peers & lt);
+        } else {
+            // peers by NB + 1 ballots; lane w reserves window w's rows
+            const unsigned vb = __ballot_sync(0xffffffffu, ok);
+            unsigned peers = vb, mine = vb;  // peers: lanes of my window; mine: lanes of window `lane`
 #pragma unroll
             for (int k = 0; k < NB; ++k) {
-                const unsigned b = __ballot_sync(0xffffffffu, (bn[j] >> k) & 1u);
-                peers &= ((bn[j] >> k) & 1u) ? b : ~b;
+                const unsigned bk = __ballot_sync(0xffffffffu, (b >> k) & 1u);
+                peers &= ((b >> k) & 1u) ? bk : ~bk;
+                mine &= ((lane >> k) & 1u) ? bk : ~bk;
             }
-            const int leader = __ffs(peers) - 1;
-            uint32_t old = 0;
-            if (valid && (int)lane == leader) {
-                old = s_w[w][bn[j]];
-                s_w[w][bn[j]] = old + __popc(peers);
+            const uint32_t cnt = lane < (uint32_t)P ? __popc(mine) : 0u;
+            if (cnt) {
+                base = atomicAdd(&s_fill[lane], cnt);
+                if ((base & (CC_CHUNK - 1)) == 0)
+                    activate(lane, base >> CC_CHUNK_BITS);
+                else if (((base + cnt - 1) >> CC_CHUNK_BITS) != (base >> CC_CHUNK_BITS))
+                    activate(lane, (base + cnt - 1) >> CC_CHUNK_BITS);
             }
-            rk[j] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
+            q = __shfl_sync(0xffffffffu, base, b & 31u) + __popc(peers & lt);
         }
-        __syncthreads();
-        if (w == 0) {  // bin totals, warp offsets and tile offsets: one warp, P <= 16 bins
-            uint32_t acc = 0;
-            if (lane < (uint32_t)P) {
-#pragma unroll
-                for (int k = 0; k < MS_WARPS; ++k) {
-                    const uint32_t c = s_w[k][lane];
-                    s_w[k][lane] = acc;
-                    acc += c;
-                }
-            }
-            uint32_t incl = acc;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((int)lane >= o) incl += v;
-            }
-            if (lane < (uint32_t)P) s_start[lane] = incl - acc;
-            if (lane == (uint32_t)P - 1) s_start[P] = incl;
+        if (ok) {
+            const uint32_t k = q >> CC_CHUNK_BITS;
+            const unsigned long long x = *reinterpret_cast<volatile unsigned long long*>(&s_ring[b][k % PD_RING]);
+            const uint32_t c = (uint32_t)(x >> 32) == k + 1 ? (uint32_t)x : chunk_of(b, k);
+            __stcs(out + (((unsigned long long)c << CC_CHUNK_BITS) | (q & (CC_CHUNK - 1))),
+                   make_uint2((uint32_t)u, (uint32_t)v));
         }
-        __syncthreads();
+    };
+    // warps take 64-row groups grid-stride, two groups (four rows per lane) in flight
+    const unsigned long long nw = (unsigned long long)gridDim.x * (PD_THREADS / 32);
+    const unsigned long long ng = (m + 63) / 64;
+    for (unsigned long long g = (unsigned long long)blockIdx.x * (PD_THREADS / 32) + (threadIdx.x >> 5); g < ng;
+         g += 2 * nw) {
+        const unsigned long long r0 = g * 64 + lane, r1 = (g + nw) * 64 + lane;
+        const unsigned long long ee[4] = {r0, r0 + 32, r1, r1 + 32};
+        unsigned long long uu[4], vv[4];
+        bool ok[4], any_bad = false;
 #pragma unroll
-        for (int j = 0; j < MS2_ITEMS; ++j)
-            if (bn[j] < (uint32_t)P) sbuf[s_start[bn[j]] + s_w[w][bn[j]] + rk[j]] = pr[j];
-        if (threadIdx.x <= (uint32_t)P) toff[tile * (MAX_PARTS + 1) + threadIdx.x] = s_start[threadIdx.x];
-        __syncthreads();
-        const uint32_t total = s_start[P];
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(out) + e0;
-        const ulonglong2* src2 = reinterpret_cast<const ulonglong2*>(sbuf);
-        for (uint32_t i = threadIdx.x; i < total / 2; i += MS_THREADS)
-            __stcs(reinterpret_cast<ulonglong2*>(dst) + i, src2[i]);
-        if ((total & 1u) && threadIdx.x == 0) __stcs(dst + total - 1, sbuf[total - 1]);
-        __syncthreads();  // sbuf and s_start are reused by the next tile
+        for (int j = 0; j < 4; ++j) {
+            uu[j] = n;
+            vv[j] = n;
+            if (ee[j] < m) edges.load(ee[j], uu[j], vv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool in = ee[j] < m;
+            ok[j] = in && (kNarrow ? ((uint32_t)uu[j] < n32 && (uint32_t)vv[j] < n32) : (uu[j] < n && vv[j] < n)) &&
+                    (uint32_t)uu[j] != (uint32_t)vv[j];
+            any_bad |= in && !ok[j];
+        }
+        if (__any_sync(0xffffffffu, any_bad)) {  // invalid rows are flagged off the fast path
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (ee[j] < m && !ok[j]) flag_bad(ee[j], uu[j], vv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) place(ok[j], uu[j], vv[j]);
+    }
+    __syncthreads();
+    // pad the open chunks with (0, 0) rows: the hook skips them (equal parents)
+    for (int w = 0; w < P; ++w) {
+        const uint32_t tot = s_fill[w], r = tot & (CC_CHUNK - 1);
+        if (r == 0) continue;  // (chunk tot >> CC_CHUNK_BITS was only pre-claimed: not in the directory)
+        const uint32_t c = *reinterpret_cast<volatile uint32_t*>(my_list + w * kmax + (tot >> CC_CHUNK_BITS));
+        for (uint32_t q = r + threadIdx.x; q < CC_CHUNK; q += PD_THREADS)
+            out[((unsigned long long)c << CC_CHUNK_BITS) | q] = make_uint2(0u, 0u);
     }
 }
 
-// hook of window k over the tile-sorted copy: one warp per tile slice (a
-// slice holds ~m/tiles * (2k+1)/P^2 edges -- 64 for the lowest window of a
-// G(n,m) graph at 8 windows -- so a CTA per slice would idle most lanes),
-// warps take tiles in order, HU edges per lane in flight
-template <bool kUF>
-__global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_tiles(const uint2* __restrict__ edges,
-                                                                const uint32_t* __restrict__ toff,
-                                                                unsigned long long ntiles, int k, uint32_t* D,
-                                                                unsigned long long* flags) {
-    bool any = false;
-    constexpr int HU = 2;
-    const uint32_t lane = lane_id();
-    const unsigned long long nw = (unsigned long long)gridDim.x * (HOOK_THREADS / 32);
-    for (unsigned long long t = (unsigned long long)blockIdx.x * (HOOK_THREADS / 32) + (threadIdx.x >> 5); t < ntiles;
-         t += nw) {
-        const uint32_t lo = __ldg(toff + t * (MAX_PARTS + 1) + k), hi = __ldg(toff + t * (MAX_PARTS + 1) + k + 1);
-        const uint2* te = edges + t * MS2_TILE;
-        for (uint32_t i = lo + lane; i < hi; i += HU * 32) {
-            uint2 uv[HU];
-            bool ok[HU];
-#pragma unroll
-            for (int q = 0; q < HU; ++q) {
-                ok[q] = i + q * 32 < hi;
-                uv[q] = ok[q] ? __ldcs(te + i + q * 32) : make_uint2(0, 0);
-            }
-            uint32_t pu[HU], pv[HU];
-#pragma unroll
-            for (int q = 0; q < HU; ++q) {
-                pu[q] = ok[q] ? ld_parent(D + uv[q].x) : 0;
-                pv[q] = ok[q] ? ld_parent(D + uv[q].y) : 0;
-            }
-#pragma unroll
-            for (int q = 0; q < HU; ++q) {
-                if (!ok[q] || pu[q] == pv[q]) continue;
-                if (kUF) {
-                    any |= unite(D, uv[q].x, pu[q], uv[q].y, pv[q]);
-                } else {
-                    const uint32_t hi2 = pu[q] > pv[q] ? pu[q] : pv[q];
-                    const uint32_t lo2 = pu[q] > pv[q] ? pv[q] : pu[q];
-                    if (atomicMin(D + hi2, lo2) > lo2) any = true;
-                }
-            }
-        }
+// hook range of window k: [0, chunks_k * CC_CHUNK)
+__global__ void k_cc_chunk_ranges(const uint32_t* __restrict__ counts, int P, unsigned long long* __restrict__ rng) {
+    const int k = threadIdx.x;
+    if (k < P) {
+        rng[2 * k] = 0;
+        rng[2 * k + 1] = (unsigned long long)counts[k] << CC_CHUNK_BITS;
     }
-    if (__any_sync(0xffffffffu, any) && lane == 0) flags[0] = 1ull;
 }
 
 // ---------------------------------------------------------------------------
@@ -732,44 +743,83 @@ struct CcPartBufs {
     unsigned long long* totals = nullptr;   // [MAX_PARTS]
     unsigned long long* cursor = nullptr;   // [MAX_PARTS]
     unsigned long long* off_part = nullptr; // [MAX_PARTS + 2]
-    uint32_t* toff = nullptr;               // [tiles][MAX_PARTS + 1] (one-pass tile sort)
+    uint32_t* counts = nullptr;             // [2 * MAX_PARTS] chunk layout: chunks per window, chunks claimed
+    uint32_t* dir = nullptr;                // [parts][dir_stride] chunk ids per window
+    unsigned long long* rng = nullptr;      // [2 * MAX_PARTS] hook range per window
+    unsigned long long dir_stride = 0;
+    uint32_t* cta_list = nullptr;           // [grid][parts][kmax] chunk ids per CTA and window
+    uint32_t kmax = 0;
     uint2* edges = nullptr;
-    bool tiled = false;                     // which layout partition_edges produced
+    bool chunked = false;                   // which layout partition_edges produced
 };
 
-static unsigned long long part_tiles(unsigned long long m) { return (m + MS2_TILE - 1) / MS2_TILE; }
+// partition mode: one pass into per-window chunk lists (default), or count +
+// scatter (SG_CC_PART=count; also taken for input rows that are not 16-B
+// aligned, which the bulk copies need).  A reused partition (sg_cc_hook_part,
+// reuse = 1) re-derives its layout from the same test.
+static bool use_chunks(const void*) { return !tuning().cc_part_count; }
+static uint32_t chunk_grid(unsigned long long m) {
+    const unsigned long long warps = (m + 127) / 128;  // two 64-row groups per warp at least
+    const unsigned long long ctas = (warps + PD_THREADS / 32 - 1) / (PD_THREADS / 32);
+    const unsigned long long g = (unsigned long long)sm_count() * PD_CTAS_PER_SM;
+    return (uint32_t)(ctas < g ? ctas : g);
+}
+// chunks the layout can claim: every full chunk, plus per (CTA, window) one
+// partial chunk and one pre-claimed chunk that may stay unused
+static unsigned long long max_chunks(unsigned long long m, int parts) {
+    return ((m + CC_CHUNK - 1) >> CC_CHUNK_BITS) + 2ull * parts * chunk_grid(m);
+}
+// chunks one CTA can fill per window: its warps' groups, whole chunks, plus the open one
+static uint32_t chunk_kmax(unsigned long long m) {
+    const unsigned long long nw = (unsigned long long)chunk_grid(m) * (PD_THREADS / 32);
+    const unsigned long long ng = (m + 63) / 64;
+    const unsigned long long rows = ((ng + nw - 1) / nw + 1) * 64 * (PD_THREADS / 32);
+    return (uint32_t)((rows >> CC_CHUNK_BITS) + 3);  // + the open chunk + the pre-claimed one
+}
 
-// partition mode: count + scatter (default), or the one-pass tile sort
-// (SG_CC_PART=tiles): the tile sort moves 0.5 ms less data at C5, but hooking
-// the per-tile slices costs 1.1 ms more (profiles/r02_cc_partition.txt)
-static bool part_one_pass() { return tuning().cc_part_tiles != 0; }
-// the one-pass layout needs 16-B aligned input rows (bulk copies); a reused
-// partition (sg_cc_hook_part, reuse = 1) re-derives its layout from this
-static bool use_tiles(const void* edges) { return part_one_pass() && ((uintptr_t)edges & 15) == 0; }
+static bool carve_part(Carver& c, unsigned long long m, const CcPlan& p, CcPartBufs& b) {
+    b.totals = c.take<unsigned long long>(MAX_PARTS);
+    b.cursor = c.take<unsigned long long>(MAX_PARTS);
+    b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
+    b.counts = c.take<uint32_t>(2 * MAX_PARTS);
+    b.rng = c.take<unsigned long long>(2 * MAX_PARTS);
+    const unsigned long long mc = max_chunks(m, p.parts);
+    b.dir_stride = mc;
+    b.dir = c.take<uint32_t>((size_t)(mc * p.parts));
+    b.kmax = chunk_kmax(m);
+    b.cta_list = c.take<uint32_t>((size_t)chunk_grid(m) * p.parts * b.kmax);
+    b.edges = c.take<uint2>((size_t)(mc << CC_CHUNK_BITS));  // >= m: also holds the count + scatter layout
+    return c.ok;
+}
 
 template <class E>
 static int partition_edges(E view, unsigned long long m, unsigned long long n, const CcPlan& p, CcPartBufs& b,
                            unsigned long long* flags, cudaStream_t s, unsigned long long row0 = 0) {
     const uint32_t nt = (uint32_t)p.ntiles;
-    b.tiled = false;
-    if (use_tiles(view.e)) {
+    b.chunked = false;
+    if (use_chunks(view.e)) {
         int nbits = 0;
         while ((1 << nbits) < p.parts) ++nbits;
         const bool narrow = E::kBytes == 8 && n <= 0x80000000ull;
-        auto kt = narrow ? (nbits <= 1 ? k_cc_part_tiles<E, 1, true>
-                            : nbits == 2 ? k_cc_part_tiles<E, 2, true>
-                            : nbits == 3 ? k_cc_part_tiles<E, 3, true> : k_cc_part_tiles<E, 4, true>)
-                         : (nbits <= 1 ? k_cc_part_tiles<E, 1, false>
-                            : nbits == 2 ? k_cc_part_tiles<E, 2, false>
-                            : nbits == 3 ? k_cc_part_tiles<E, 3, false> : k_cc_part_tiles<E, 4, false>);
-        const size_t smem = (size_t)MS2_TILE * E::kBytes + (size_t)MS2_TILE * 8;
-        SG_CUDA(set_smem_max(kt, smem));
-        const unsigned long long ntile = part_tiles(m);
-        const uint32_t ns = (uint32_t)(ntile < (unsigned long long)sm_count() * TP_CTAS_PER_SM ? ntile
-                                                                                         : sm_count() * TP_CTAS_PER_SM);
-        kt<<<ns, MS_THREADS, smem, s>>>(view, m, n, row0, p.shift, p.parts, b.toff, b.edges, flags);
+        using KT = void (*)(E, unsigned long long, unsigned long long, unsigned long long, uint32_t, int, uint2*,
+                            uint32_t*, unsigned long long, uint32_t*, uint32_t*, uint32_t, unsigned long long*);
+        KT kt;
+        if (!tuning().cc_rank_ballot)  // match.any peers (default)
+            kt = narrow ? k_cc_part_chunks<E, 4, true, true> : k_cc_part_chunks<E, 4, false, true>;
+        else
+            kt = narrow ? (nbits <= 1 ? k_cc_part_chunks<E, 1, true, false>
+                           : nbits == 2 ? k_cc_part_chunks<E, 2, true, false>
+                           : nbits == 3 ? k_cc_part_chunks<E, 3, true, false> : k_cc_part_chunks<E, 4, true, false>)
+                        : (nbits <= 1 ? k_cc_part_chunks<E, 1, false, false>
+                           : nbits == 2 ? k_cc_part_chunks<E, 2, false, false>
+                           : nbits == 3 ? k_cc_part_chunks<E, 3, false, false> : k_cc_part_chunks<E, 4, false, false>);
+        SG_CUDA(cudaMemsetAsync(b.counts, 0, sizeof(uint32_t) * 2 * MAX_PARTS, s));
+        kt<<<chunk_grid(m), PD_THREADS, 0, s>>>(view, m, n, row0, p.shift, p.parts, b.edges, b.dir, b.dir_stride,
+                                                b.counts, b.cta_list, b.kmax, flags);
         SG_LAUNCH_CHECK();
-        b.tiled = true;
+        k_cc_chunk_ranges<<<1, 32, 0, s>>>(b.counts, p.parts, b.rng);
+        SG_LAUNCH_CHECK();
+        b.chunked = true;
         return SG_OK;
     }
     SG_CUDA(cudaMemsetAsync(b.totals, 0, sizeof(unsigned long long) * MAX_PARTS, s));
@@ -825,19 +875,15 @@ static int partition_dispatch(const void* edges, int dt, unsigned long long m, u
 // one hook sweep over a partitioned edge list, window by window
 static int hook_partitions(const CcPlan& p, const CcPartBufs& b, unsigned long long m, unsigned long long n,
                            uint32_t* D, int variant, unsigned long long* flags, cudaStream_t s) {
-    if (b.tiled) {
-        const unsigned long long nt = part_tiles(m);
-        const uint32_t g = (uint32_t)(nt < (unsigned long long)sm_count() * 8 ? nt : sm_count() * 8);
+    const unsigned long long per = m / p.parts + 1;
+    if (b.chunked) {
         for (int k = 0; k < p.parts; ++k) {
-            if (variant == SG_CC_UF)
-                k_cc_hook_tiles<true><<<g, HOOK_THREADS, 0, s>>>(b.edges, b.toff, nt, k, D, flags);
-            else
-                k_cc_hook_tiles<false><<<g, HOOK_THREADS, 0, s>>>(b.edges, b.toff, nt, k, D, flags);
-            SG_LAUNCH_CHECK();
+            int rc = launch_hook(EdgesChunked{b.edges, b.dir + (size_t)k * b.dir_stride}, per, 0, n, D, variant, false,
+                                 flags, s, b.rng + 2 * k);
+            if (rc != SG_OK) return rc;
         }
         return SG_OK;
     }
-    const unsigned long long per = m / p.parts + 1;
     for (int k = 0; k < p.parts; ++k) {
         int rc = launch_hook(EdgesU32{b.edges}, per, 0, n, D, variant, false, flags, s, b.off_part + k);
         if (rc != SG_OK) return rc;
@@ -909,13 +955,7 @@ static bool carve_cc(Carver& c, uint64_t n, uint64_t m, const CcPlan& p, unsigne
                      CcPartBufs& b) {
     flags = c.take<unsigned long long>(8);  // [0..3] flags, [4] roots
     Dws = c.take<uint32_t>(n);
-    if (p.parts > 1) {
-        b.totals = c.take<unsigned long long>(MAX_PARTS);
-        b.cursor = c.take<unsigned long long>(MAX_PARTS);
-        b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
-        b.toff = c.take<uint32_t>((size_t)part_tiles(m) * (MAX_PARTS + 1));
-        b.edges = c.take<uint2>(m);
-    }
+    if (p.parts > 1) carve_part(c, m, p, b);
     return c.ok;
 }
 
@@ -1065,11 +1105,7 @@ size_t sg_cc_hook_workspace_bytes(uint64_t n, uint64_t m) {
     if (p.parts <= 1) return 256;
     Carver c(nullptr, 0);
     CcPartBufs b;
-    b.totals = c.take<unsigned long long>(MAX_PARTS);
-    b.cursor = c.take<unsigned long long>(MAX_PARTS);
-    b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
-    b.toff = c.take<uint32_t>((size_t)part_tiles(m) * (MAX_PARTS + 1));
-    b.edges = c.take<uint2>(m);
+    carve_part(c, m, p, b);
     return c.off + 256;
 }
 
@@ -1083,13 +1119,8 @@ int sg_cc_hook_part(const void* edges, int edge_dtype, uint64_t m, uint64_t row0
     ms_configure();
     Carver c(ws, ws_bytes);
     CcPartBufs b;
-    b.totals = c.take<unsigned long long>(MAX_PARTS);
-    b.cursor = c.take<unsigned long long>(MAX_PARTS);
-    b.off_part = c.take<unsigned long long>((size_t)MAX_PARTS + 2);
-    b.toff = c.take<uint32_t>((size_t)part_tiles(m) * (MAX_PARTS + 1));
-    b.edges = c.take<uint2>(m);
-    if (!c.ok) return SG_ERR_WORKSPACE;
-    b.tiled = use_tiles(edges);
+    if (!carve_part(c, m, p, b)) return SG_ERR_WORKSPACE;
+    b.chunked = use_chunks(edges);
     if (!reuse) {  // rows are validated while they are partitioned (flags hold ~global row)
         int rc = partition_dispatch(edges, edge_dtype, m, n, p, b, (unsigned long long*)flags, s, row0);
         if (rc != SG_OK) return rc;

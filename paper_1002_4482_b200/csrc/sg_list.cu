@@ -1062,7 +1062,7 @@ static size_t rl_smem_bytes() { return (size_t)RL_TILE * 8 * 2; }
 // sorted by fine bin, and its fb + 1 bin offsets go to toff[tile]; the
 // scatter then collects a fine window's runs from the coarse window's tiles
 // (k_rs_rec_scatter_tiles).  No global atomics, one linear 16-B copy out.
-template <int NB, int kPeers, bool kTiles = false>  // NB: bin bits (fb <= 2^NB <= 64); kPeers: 1 ballots, 0 match.any, 2 alternate
+template <int NB, int kPeers, bool kTiles = false>  // NB: bin bits (fb <= 2^NB <= 64); kPeers: 1 ballots, 0 match.any, 2 alternate, 3 shared atomics
 __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
     unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
@@ -1132,6 +1132,10 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
         // rank among the warp's records of the same bin: rk = warp counter before + peers below
 #pragma unroll
         for (int j = 0; j < RL_IT; ++j) {
+            if (kPeers == 3) {  // shared atomics on the warp's counters: one ATOMS per record, any order in a bin
+                if (bn[j] != 0xFFu) loc[j] |= atomicAdd(&s_w[warp][bn[j]], 1u) << 20;
+                continue;
+            }
             unsigned peers;
             if (kPeers == 0 || (kPeers == 2 && (j & 1))) {
                 peers = __match_any_sync(0xffffffffu, bn[j]);
@@ -1224,6 +1228,170 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
             if (se < s1) over = true;
         }
         __syncthreads();  // s_sort and the tables are reused by the next tile
+    }
+    if (over) st->bad = 1;
+}
+
+// rs5_refine with shared-atomic ranking (default).  Same job and output as
+// k_rs_refine_lean: a coarse window's records -> {cur, rank} pairs split by
+// fine window (rank = IS_1[sid] - local - 1, listrank.py:375-379).
+//  * A record's slot among its warp's records of the same fine bin comes from
+//    one shared atomicAdd on the warp's bin counter (order inside a bin is
+//    free: rs5_scatter places every pair by its node id), instead of NB + 1
+//    ballots and a leader update per record.
+//  * The tile's runs are claimed in their fine windows with one global atomic
+//    per bin, and the tile is written out one iteration later (double-
+//    buffered sorted tile): the atomics' latency hides behind the next tile's
+//    ranking instead of stalling every warp at a barrier.
+//  * Tiles of 2048 records, 4 CTAs of 256 threads per SM, two barriers per
+//    tile.
+constexpr int RA_THREADS = 256;
+constexpr int RA_WARPS = RA_THREADS / 32;
+constexpr int RA_IT = 8;
+constexpr int RA_TILE = RA_THREADS * RA_IT;  // 2048 records (2^cshift is a multiple)
+constexpr int RA_MAXB = 64;
+constexpr int RA_CTAS_PER_SM = 4;
+
+static size_t ra_smem_bytes() { return (size_t)RA_TILE * 8 * 3; }  // staging + two sorted tiles
+
+__global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
+    const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
+    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
+    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
+    if (layout_local(st) || st->overflow) return;
+    const uint32_t fb = 1u << (cshift - fshift);  // <= RA_MAXB
+    extern __shared__ __align__(128) unsigned char ra_raw[];
+    unsigned long long* s_in = reinterpret_cast<unsigned long long*>(ra_raw);
+    unsigned long long* s_sort0 = s_in + RA_TILE;  // sorted tiles: buffer k at s_sort0 + k * RA_TILE
+    __shared__ unsigned long long bar;
+    __shared__ uint32_t s_w[RA_WARPS][RA_MAXB];  // per-warp bin counts -> absolute tile slots
+    __shared__ uint32_t s_bs[2][RA_MAXB + 1];     // bin starts in the sorted tile
+    __shared__ uint32_t s_gb[2][RA_MAXB];         // window slot of the bin's first tile record
+    __shared__ uint32_t s_ge[2][RA_MAXB];         // tile end of the bin's writable run
+    __shared__ uint32_t s_half;
+    const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
+    const unsigned long long ntiles = (n + RA_TILE - 1) / RA_TILE;
+    const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
+    const unsigned long long pol_last = l2_evict_last();
+    const uint32_t fmask = fb - 1;
+    const uint32_t lmask = (1u << lb) - 1u;  // lb < 32 (host-checked)
+    const uint32_t smask = (uint32_t)((1ull << (sb - lb)) - 1);
+    const uint32_t cap = 1u << fshift;
+    if (t == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    auto issue = [&](unsigned long long tile) {
+        if (t == 0 && tile < ntiles) {
+            const unsigned long long e0 = tile * RA_TILE;
+            const uint32_t cnt = (uint32_t)min((unsigned long long)RA_TILE, n - e0);
+            const uint32_t bytes = (cnt * 8u + 15u) & ~15u;  // the buffer is padded to whole windows
+            mbar_expect_tx(&bar, bytes);
+            bulk_g2s_hint(s_in, in + e0, bytes, &bar, l2_evict_first());
+        }
+    };
+    // the previous tile's claim, held by prefix thread d (bin d) until its write-out
+    uint32_t p_base = 0, p_tot = 0, p_start = 0;
+    // write out the sorted tile in buffer k of coarse window cw: warp w copies bins w, w + RA_WARPS, ...
+    bool over = false;
+    auto write_out = [&](int k, uint32_t cw) {
+        const unsigned long long* srt = s_sort0 + k * RA_TILE;
+        unsigned long long* wout = out + ((unsigned long long)cw * fb << fshift);
+        for (uint32_t d = warp; d < fb; d += RA_WARPS) {
+            const uint32_t s0 = s_bs[k][d], s1 = s_bs[k][d + 1], se = s_ge[k][d];
+            unsigned long long* dst = wout + ((unsigned long long)d << fshift) + s_gb[k][d];
+            for (uint32_t i = s0 + lane; i < se; i += 32) __stcs(dst + (i - s0), srt[i]);
+            if (se < s1) over = true;
+        }
+    };
+    auto publish_prev = [&](int k) {  // prefix threads: the previous tile's global slots
+        if (t < fb) {
+            const uint32_t room = p_base < cap ? cap - p_base : 0u;
+            s_gb[k][t] = p_base;
+            s_ge[k][t] = p_start + (p_tot < room ? p_tot : room);
+        }
+    };
+    uint32_t phase = 0, it = 0, c_prev = 0;
+    issue(blockIdx.x);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int k = (int)(it & 1u);
+        const unsigned long long e0 = tile * RA_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)RA_TILE, n - e0);
+        const uint32_t c = (uint32_t)(e0 >> cshift);  // tiles never straddle a coarse window
+        s_w[warp][lane] = 0u;
+        s_w[warp][lane + 32] = 0u;
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        uint32_t cur[RA_IT], gv[RA_IT], loc[RA_IT], bn[RA_IT];
+#pragma unroll
+        for (int j = 0; j < RA_IT; ++j) {
+            const uint32_t e = j * RA_THREADS + t;
+            const unsigned long long r = e < cnt ? s_in[e] : 0ull;
+            cur[j] = (uint32_t)(r >> sb);
+            const uint32_t sid = (uint32_t)(r >> lb) & smask;
+            loc[j] = (uint32_t)r & lmask;
+            // issued now, first used at the placement: the gathers fly while the tile is ranked
+            gv[j] = ld_hint(IS1 + (sid < R1 ? sid : 0u), pol_last);
+            bn[j] = (e < cnt && (cur[j] >> cshift) == c) ? (cur[j] >> fshift) & fmask : 0xFFu;
+        }
+        __syncwarp();  // this warp's counters are zeroed
+#pragma unroll
+        for (int j = 0; j < RA_IT; ++j)
+            if (bn[j] != 0xFFu) loc[j] |= atomicAdd(&s_w[warp][bn[j]], 1u) << 20;  // local < 2^20 (host-checked)
+        __syncthreads();  // (1) staging consumed, every warp's counts in, the tile before last written out
+        issue(tile + gridDim.x);
+        // (warp, bin) counts -> absolute slots of the bin-sorted tile; one global
+        // atomic per non-empty bin claims the bin's run in its fine window (used next iteration)
+        if (t < 64) {
+            const uint32_t d = t;
+            uint32_t tot = 0;
+            if (d < fb) {
+#pragma unroll
+                for (int w = 0; w < RA_WARPS; ++w) {
+                    const uint32_t x = s_w[w][d];
+                    s_w[w][d] = tot;
+                    tot += x;
+                }
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += y;
+            }
+            if (t == 31) s_half = incl;
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            const uint32_t start = incl - tot + (t >= 32 ? s_half : 0u);
+            if (it > 0) publish_prev(k ^ 1);
+            if (d < fb) {
+#pragma unroll
+                for (int w = 0; w < RA_WARPS; ++w) s_w[w][d] += start;
+                s_bs[k][d] = start;
+                if (d == fb - 1) s_bs[k][fb] = start + tot;
+                p_base = tot ? (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot) : 0u;
+                p_tot = tot;
+                p_start = start;
+            }
+        }
+        __syncthreads();  // (2) this tile's slots and the previous tile's claims known
+        unsigned long long* srt = s_sort0 + k * RA_TILE;
+#pragma unroll
+        for (int j = 0; j < RA_IT; ++j) {
+            if (bn[j] != 0xFFu) {
+                const uint32_t pos = s_w[warp][bn[j]] + (loc[j] >> 20);
+                const uint32_t rank = gv[j] - (loc[j] & 0xFFFFFu) - 1u;
+                srt[pos] = ((unsigned long long)cur[j] << 32) | rank;
+            }
+        }
+        if (it > 0) write_out(k ^ 1, c_prev);
+        c_prev = c;
+        // no closing barrier: the next tile rewrites s_w / s_bs[k ^ 1] / the other sorted
+        // buffer only after its barrier (1)
+    }
+    if (it > 0) {  // the last tile
+        const int k = (int)((it - 1) & 1u);
+        __syncthreads();  // its placement is complete
+        publish_prev(k);
+        __syncthreads();
+        write_out(k, c_prev);
     }
     if (over) st->bad = 1;
 }
@@ -2370,11 +2538,19 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
     const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
     bool tiled = false;
-    if (lean_ok && tu_r.rs_refine != 1) {
-        // SG_RS_REFINE: 0 lean + ballots (default), 2 lean + match.any, 3 lean + alternate,
-        // 4 lean + ballots in the tile layout (k_rs_rec_scatter_tiles); 1 the ms_split_fn refine below
+    if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
+        const size_t sma = ra_smem_bytes();
+        SG_CUDA(set_smem_max(k_rs_refine_atom, sma));
+        const uint32_t g = sm_count() * RA_CTAS_PER_SM;
+        rec.begin(K_RS5_REFINE, 0, g, RA_THREADS, n);
+        k_rs_refine_atom<<<g, RA_THREADS, sma, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
+                                                   b.IS[1], p.rec_sb, p.rec_lb);
+    } else if (lean_ok && tu_r.rs_refine != 1) {
+        // SG_RS_REFINE: 0 k_rs_refine_atom above (default), 6 lean + ballots, 2 lean + match.any, 3 lean + alternate,
+        // 4 lean + ballots in the tile layout (k_rs_rec_scatter_tiles); 5 lean + shared atomics;
+        // 1 the ms_split_fn refine below
         tiled = tu_r.rs_refine == 4;
-        const int pm = tu_r.rs_refine == 2 ? 0 : (tu_r.rs_refine == 3 ? 2 : 1);
+        const int pm = tu_r.rs_refine == 2 ? 0 : (tu_r.rs_refine == 3 ? 2 : (tu_r.rs_refine == 5 ? 3 : 1));  // 6: ballots
         using KL = void (*)(const unsigned long long*, unsigned long long*, unsigned long long*, ListStatus*,
                             unsigned long long, uint32_t, uint32_t, const uint32_t*, uint32_t, uint32_t, uint32_t*);
         KL kl;
@@ -2383,6 +2559,8 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
                               : (fbits_r <= 4 ? k_rs_refine_lean<4, 1, true> : k_rs_refine_lean<6, 1, true>);
         else if (pm == 0)
             kl = k_rs_refine_lean<6, 0>;
+        else if (pm == 3)
+            kl = k_rs_refine_lean<6, 3>;
         else if (pm == 2)
             kl = fbits_r <= 4 ? k_rs_refine_lean<4, 2> : k_rs_refine_lean<6, 2>;
         else

@@ -188,10 +188,12 @@ static Tuning read_tuning(uint32_t generation) {
     v.rs_topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
     v.rs_packed = env_u32("SG_RS_PACKED", 1, 0, 1);
     v.rs_fused = env_u32("SG_RS_FUSED", 1, 0, 1);
-    v.rs_refine = env_u32("SG_RS_REFINE", 0, 0, 4);  // rs5_refine variant (sg_list.cu)
+    v.rs_refine = env_u32("SG_RS_REFINE", 0, 0, 6);  // rs5_refine variant (sg_list.cu)
     v.cc_wbits = env_u32("SG_CC_WBITS", 0, 0, 31);
     const char* part = getenv("SG_CC_PART");
-    v.cc_part_tiles = part && strcmp(part, "tiles") == 0;
+    v.cc_part_count = part && strcmp(part, "count") == 0;  // count + scatter instead of chunk lists
+    const char* rk = getenv("SG_CC_RANK");
+    v.cc_rank_ballot = rk && strcmp(rk, "ballot") == 0;  // chunk partition: ballot peers instead of match.any
     v.ms_peers = env_u32("SG_MS_PEERS", 1, 0, 2);
     v.generation = generation;
     return v;

@@ -20,6 +20,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <emmintrin.h>  // SSE2 (x86-64 baseline): 16-B non-temporal stores
+
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -138,6 +140,53 @@ inline void split(size_t n, int p, int parts, size_t& lo, size_t& hi) {
     hi = std::min(n, lo + per);
 }
 
+
+// int64 -> u32 over [0, len): returns nonzero if any value lies outside
+// [0, bound) (bound <= 2^31).  dst (pinned staging) gets 16-B non-temporal
+// stores: it is DMA'd next, so there is no point in reading it for
+// ownership or keeping it in the host caches.
+inline uint64_t narrow_range(const int64_t* src, uint32_t* dst, size_t len, uint64_t bound) {
+    uint64_t acc = 0;
+    size_t i = 0;
+    for (; i < len && ((uintptr_t)(dst + i) & 15); ++i) {
+        const uint64_t v = (uint64_t)src[i];
+        acc |= (uint64_t)(v >= bound);
+        dst[i] = (uint32_t)v;
+    }
+    const __m128i bm1 = _mm_set1_epi32((int)(bound - 1));  // bound - 1 < 2^31: a signed compare works
+    __m128i hi_any = _mm_setzero_si128();  // any nonzero high word: out of range
+    __m128i sgn = _mm_setzero_si128();     // sign bits: low word >= 2^31, or low word > bound - 1
+    for (; i + 4 <= len; i += 4) {
+        const __m128 a = _mm_castsi128_ps(_mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i)));
+        const __m128 b = _mm_castsi128_ps(_mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 2)));
+        const __m128i lo = _mm_castps_si128(_mm_shuffle_ps(a, b, _MM_SHUFFLE(2, 0, 2, 0)));
+        const __m128i hi = _mm_castps_si128(_mm_shuffle_ps(a, b, _MM_SHUFFLE(3, 1, 3, 1)));
+        hi_any = _mm_or_si128(hi_any, hi);
+        sgn = _mm_or_si128(sgn, _mm_or_si128(lo, _mm_cmpgt_epi32(lo, bm1)));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), lo);
+    }
+    acc |= (uint64_t)(_mm_movemask_epi8(_mm_cmpeq_epi32(hi_any, _mm_setzero_si128())) != 0xFFFF);
+    acc |= (uint64_t)(_mm_movemask_ps(_mm_castsi128_ps(sgn)) != 0);
+    for (; i < len; ++i) {
+        const uint64_t v = (uint64_t)src[i];
+        acc |= (uint64_t)(v >= bound);
+        dst[i] = (uint32_t)v;
+    }
+    return acc;
+}
+
+// u32 -> int64 over [0, len), 16-B non-temporal stores into the caller's array
+inline void widen(const uint32_t* src, int64_t* dst, size_t len) {
+    size_t i = 0;
+    for (; i < len && ((uintptr_t)(dst + i) & 15); ++i) dst[i] = (int64_t)src[i];
+    const __m128i z = _mm_setzero_si128();
+    for (; i + 4 <= len; i += 4) {
+        const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_unpacklo_epi32(x, z));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 2), _mm_unpackhi_epi32(x, z));
+    }
+    for (; i < len; ++i) dst[i] = (int64_t)src[i];
+}
 }  // namespace
 }  // namespace sg
 
@@ -168,13 +217,8 @@ int sg_h2d_narrow_i64(const int64_t* host, uint64_t count, uint32_t* dev, uint64
         pool().run([&](int p, int parts) {
             size_t lo, hi;
             split(len, p, parts, lo, hi);
-            uint64_t acc = 0;  // any value outside [0, bound) sets a bit we can test once
-            for (size_t i = lo; i < hi; ++i) {
-                const uint64_t v = (uint64_t)src[i];
-                acc |= (uint64_t)(v >= bound);
-                dst[i] = (uint32_t)v;
-            }
-            if (acc) bad.store(1, std::memory_order_relaxed);
+            if (narrow_range(src + lo, dst + lo, hi - lo, bound)) bad.store(1, std::memory_order_relaxed);
+            _mm_sfence();  // the non-temporal stores are visible before the DMA reads the slot
         });
         if (bad.load(std::memory_order_relaxed)) {
             *in_range = 0;  // the caller copies int64 instead; the device reports the exact error
@@ -198,7 +242,7 @@ int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* s
     }
     cudaStream_t s = (cudaStream_t)stream;
     const uint64_t nchunks = (count + kChunk - 1) / kChunk;
-    auto widen = [&](uint64_t k) -> int {
+    auto widen_chunk = [&](uint64_t k) -> int {
         const int sl = (int)(k % kSlots);
         const size_t off = k * kChunk;
         const size_t len = std::min<uint64_t>(kChunk, count - off);
@@ -208,7 +252,8 @@ int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* s
         pool().run([&](int p, int parts) {
             size_t lo, hi;
             split(len, p, parts, lo, hi);
-            for (size_t i = lo; i < hi; ++i) dst[i] = (int64_t)src[i];
+            widen(src + lo, dst + lo, hi - lo);
+            _mm_sfence();
         });
         return SG_OK;
     };
@@ -216,7 +261,7 @@ int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* s
     for (uint64_t k = 0; k < nchunks; ++k) {
         const int sl = (int)(k % kSlots);
         if (k >= (uint64_t)kSlots) {
-            const int rc = widen(k - kSlots);  // frees slot sl
+            const int rc = widen_chunk(k - kSlots);  // frees slot sl
             if (rc != SG_OK) return rc;
         }
         const size_t off = k * kChunk;
@@ -225,7 +270,7 @@ int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* s
         SG_CUDA(cudaEventRecord(r->ev[sl], s));
     }
     for (uint64_t k = nchunks > (uint64_t)kSlots ? nchunks - kSlots : 0; k < nchunks; ++k) {
-        const int rc = widen(k);
+        const int rc = widen_chunk(k);
         if (rc != SG_OK) return rc;
     }
     return SG_OK;

@@ -63,3 +63,35 @@ def test_api_errors_through_narrow_path(cuda):
     e[123_456] = [5, (1 << 20) + 1]
     with pytest.raises(g.InvalidGraphError, match="out of range at row 123456"):
         g.sv_components(g.EdgeGraph(1 << 20, e), 64)
+
+
+@pytest.mark.parametrize("bad", [2**31, 2**31 + 5, 2**32 + 1, 2**40, -1, -(2**31)])
+def test_narrow_detects_every_out_of_range_value(cuda, bad):
+    """Values outside [0, bound) anywhere (vector body, unaligned head,
+    scalar tail) fall back to the exact int64 copy; values just below the
+    bound narrow."""
+    count = (1 << 22) + 7
+    bound = count
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, bound, count + 1, dtype=np.int64)
+    base[5] = bound - 1
+    for view in (base[:count], base[1:]):  # 16-B aligned and unaligned starts
+        d, _ = _device.to_device(view, cuda, bound=bound)
+        assert d.dtype == torch.int32 and np.array_equal(d.cpu().numpy().astype(np.int64), view)
+        for pos in (0, 1, 2, 3, 4, 1000, count // 2 + 1, count - 2, count - 1):
+            v = view.copy()
+            v[pos] = bad
+            d, _ = _device.to_device(v, cuda, bound=bound)
+            assert d.dtype == torch.int64, (bad, pos)
+            assert np.array_equal(d.cpu().numpy(), v)
+    v = base[:count].copy()
+    v[77] = bound  # exactly the bound
+    d, _ = _device.to_device(v, cuda, bound=bound)
+    assert d.dtype == torch.int64
+
+
+def test_widen_into_unaligned_and_odd_arrays(cuda):
+    for count in ((1 << 22) + 3, (1 << 21) + 1):
+        x = torch.randint(0, 2**31 - 1, (count,), dtype=torch.int32, device=cuda)
+        back = _device.to_host_numpy(x)
+        assert back.dtype == np.int64 and np.array_equal(back, x.cpu().numpy().astype(np.int64))

@@ -205,13 +205,24 @@ def test_building_blocks_c_abi(cuda, orc):
     assert int(flags[0].item()) == 1 and int(flags[1].item()) == 0 and int(flags[2].item()) == 0
 
 
+@pytest.mark.parametrize("part", ["chunks", "count"])
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_partitioned_path_small_windows(cuda, orc, sg_env, variant):
+def test_partitioned_path_small_windows(cuda, orc, sg_env, variant, part):
     """Force the windowed (partitioned-edge) hook on small graphs: windows of
-    2^12 vertices -> up to 16 partitions."""
-    sg_env(SG_CC_WBITS="12")
+    2^12 vertices -> up to 16 partitions; both partition layouts (one-pass
+    chunk lists, the default, and count + scatter).  The star and the
+    one-window graph put every edge of a tile into one window (chunk claims
+    several chunks per tile); the last case has fewer edges than one tile
+    per CTA, so most chunks are padding."""
+    sg_env(SG_CC_WBITS="12", **({"SG_CC_PART": "count"} if part == "count" else {}))
+    n = 70_000  # > 2^16 edges in the star: partitioned
+    star = np.stack([np.arange(n - 1, dtype=np.int64), np.full(n - 1, n - 1, dtype=np.int64)], axis=1)
+    rng = np.random.default_rng(5)
+    hi = rng.integers(65_600, n, size=(200_000, 2), dtype=np.int64)  # every edge in the top window
+    hi = hi[hi[:, 0] != hi[:, 1]]
     cases = [g.gen_random_graph(60_000, 5e-5, seed=4), g.gen_tree_graph(70_000, 3, seed=2),
-             g.list_to_graph(g.gen_list(66_000, seed=1)), g.gen_random_graph(30_000, 2e-4, seed=9)]
+             g.list_to_graph(g.gen_list(66_000, seed=1)), g.gen_random_graph(30_000, 2e-4, seed=9),
+             g.EdgeGraph(n, star), g.EdgeGraph(n, hi), g.gen_random_graph(300_000, 2e-6, seed=3)]
     for gr in cases:
         labels, stats = g.sv_components(gr, p=64, variant=variant)
         assert np.array_equal(labels, orc.seq_components(gr.n, gr.edges)), (gr.n, gr.m)
