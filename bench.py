@@ -30,6 +30,7 @@ all-reduce of the parent array per round (strong scaling).
 """
 
 import argparse
+import gc
 import hashlib
 import json
 import os
@@ -198,6 +199,9 @@ while True:
 
     def start(self):
         import subprocess
+        if self.PERIOD_MS <= 0:  # diagnostics only: no sampling
+            self.err = "sampling disabled (SG_BENCH_POLL_MS=0)"
+            return
         try:
             import torch
             uuid = str(torch.cuda.get_device_properties(self.index).uuid)
@@ -341,6 +345,12 @@ def measure(a, ctx, name, primary):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     launches = 0
     kern_ms = {}
+    # the cyclic GC is paused over the timed steps (as timeit does): a
+    # collection landing between an event record and the call's first launch
+    # idles the GPU for milliseconds (measured: single-step outliers of +5-13 ms)
+    gc.collect()
+    if os.environ.get("SG_BENCH_GC", "0") != "1":
+        gc.disable()
     ctx.barrier()
     clocks.mark()
     wall0 = time.perf_counter()
@@ -357,6 +367,7 @@ def measure(a, ctx, name, primary):
             kern_ms.setdefault(rec.kernel, []).append(rec.ms)
     ctx.barrier()
     wall = time.perf_counter() - wall0
+    gc.enable()
     clk = clocks.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     ms_per_step = ctx.max_over_ranks(sum(step_ms)) / a.steps
@@ -400,8 +411,10 @@ def measure(a, ctx, name, primary):
                                    "DRAM sector although the window partition serves them from L2")}}
     srt = sorted(step_ms)
     res = {"value": round(value, 1), "unit": unit, "ms_per_step": round(ms_per_step, 4), "steps": a.steps,
+           "timing": "CUDA events on the launching stream around each API call; python cyclic GC paused over "
+                     "the timed steps",
            "step_ms_spread": {"min": round(srt[0], 4), "median": round(srt[len(srt) // 2], 4),
-                              "max": round(srt[-1], 4)},
+                              "max": round(srt[-1], 4), "argmax": int(max(range(len(step_ms)), key=step_ms.__getitem__))},
            "warmup": a.warmup, "config": config,
            "algorithm": ("rs_rank (listrank.py:411): recursive sparse ruling set on scattered layouts, tile "
                          "contraction on local layouts" if kind == "list" else
@@ -538,7 +551,7 @@ def ours(a):
                 "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
                 "kernels_ms_per_step": head["kernels_ms_per_step"],
                 "wall_s_timed_region": head["wall_s_timed_region"]}
-        for k in ("algorithm", "inputs", "ruling_set", "cc", "wyllie_rank"):
+        for k in ("timing", "step_ms_spread", "algorithm", "inputs", "ruling_set", "cc", "wyllie_rank"):
             if k in head:
                 line[k] = head[k]
         for b, r in blocks.items():

@@ -1238,13 +1238,14 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
 //  * A record's slot among its warp's records of the same fine bin comes from
 //    one shared atomicAdd on the warp's bin counter (order inside a bin is
 //    free: rs5_scatter places every pair by its node id), instead of NB + 1
-//    ballots and a leader update per record.
-//  * The tile's runs are claimed in their fine windows with one global atomic
-//    per bin, and the tile is written out one iteration later (double-
-//    buffered sorted tile): the atomics' latency hides behind the next tile's
-//    ranking instead of stalling every warp at a barrier.
-//  * Tiles of 2048 records, 4 CTAs of 256 threads per SM, two barriers per
-//    tile.
+//    ballots and a leader update per record (1.25 G -> 0.8 G warp
+//    instructions at 2^28, rs5_refine 2.36 -> 1.85 ms).
+//  * The global atomic that claims a bin's run in its fine window is issued
+//    before the placement barrier and only consumed after the placement, so
+//    its latency overlaps the tile's shared-memory sort.
+//  * Tiles of 2048 records, 4 CTAs of 256 threads per SM.  (A variant that
+//    deferred each tile's write-out by one iteration behind a double-buffered
+//    sorted tile measured slower: 2.74 ms.)
 constexpr int RA_THREADS = 256;
 constexpr int RA_WARPS = RA_THREADS / 32;
 constexpr int RA_IT = 8;
@@ -1252,7 +1253,7 @@ constexpr int RA_TILE = RA_THREADS * RA_IT;  // 2048 records (2^cshift is a mult
 constexpr int RA_MAXB = 64;
 constexpr int RA_CTAS_PER_SM = 4;
 
-static size_t ra_smem_bytes() { return (size_t)RA_TILE * 8 * 3; }  // staging + two sorted tiles
+static size_t ra_smem_bytes() { return (size_t)RA_TILE * 8 * 2; }
 
 __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
     const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
@@ -1262,12 +1263,12 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
     const uint32_t fb = 1u << (cshift - fshift);  // <= RA_MAXB
     extern __shared__ __align__(128) unsigned char ra_raw[];
     unsigned long long* s_in = reinterpret_cast<unsigned long long*>(ra_raw);
-    unsigned long long* s_sort0 = s_in + RA_TILE;  // sorted tiles: buffer k at s_sort0 + k * RA_TILE
+    unsigned long long* s_sort = s_in + RA_TILE;
     __shared__ unsigned long long bar;
     __shared__ uint32_t s_w[RA_WARPS][RA_MAXB];  // per-warp bin counts -> absolute tile slots
-    __shared__ uint32_t s_bs[2][RA_MAXB + 1];     // bin starts in the sorted tile
-    __shared__ uint32_t s_gb[2][RA_MAXB];         // window slot of the bin's first tile record
-    __shared__ uint32_t s_ge[2][RA_MAXB];         // tile end of the bin's writable run
+    __shared__ uint32_t s_bs[RA_MAXB + 1];        // bin starts in the sorted tile
+    __shared__ uint32_t s_gb[RA_MAXB];            // window slot of the bin's first tile record
+    __shared__ uint32_t s_ge[RA_MAXB];            // tile end of the bin's writable run
     __shared__ uint32_t s_half;
     const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
     const unsigned long long ntiles = (n + RA_TILE - 1) / RA_TILE;
@@ -1288,31 +1289,10 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
             bulk_g2s_hint(s_in, in + e0, bytes, &bar, l2_evict_first());
         }
     };
-    // the previous tile's claim, held by prefix thread d (bin d) until its write-out
-    uint32_t p_base = 0, p_tot = 0, p_start = 0;
-    // write out the sorted tile in buffer k of coarse window cw: warp w copies bins w, w + RA_WARPS, ...
     bool over = false;
-    auto write_out = [&](int k, uint32_t cw) {
-        const unsigned long long* srt = s_sort0 + k * RA_TILE;
-        unsigned long long* wout = out + ((unsigned long long)cw * fb << fshift);
-        for (uint32_t d = warp; d < fb; d += RA_WARPS) {
-            const uint32_t s0 = s_bs[k][d], s1 = s_bs[k][d + 1], se = s_ge[k][d];
-            unsigned long long* dst = wout + ((unsigned long long)d << fshift) + s_gb[k][d];
-            for (uint32_t i = s0 + lane; i < se; i += 32) __stcs(dst + (i - s0), srt[i]);
-            if (se < s1) over = true;
-        }
-    };
-    auto publish_prev = [&](int k) {  // prefix threads: the previous tile's global slots
-        if (t < fb) {
-            const uint32_t room = p_base < cap ? cap - p_base : 0u;
-            s_gb[k][t] = p_base;
-            s_ge[k][t] = p_start + (p_tot < room ? p_tot : room);
-        }
-    };
-    uint32_t phase = 0, it = 0, c_prev = 0;
+    uint32_t phase = 0;
     issue(blockIdx.x);
-    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int k = (int)(it & 1u);
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const unsigned long long e0 = tile * RA_TILE;
         const uint32_t cnt = (uint32_t)min((unsigned long long)RA_TILE, n - e0);
         const uint32_t c = (uint32_t)(e0 >> cshift);  // tiles never straddle a coarse window
@@ -1320,7 +1300,10 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
         s_w[warp][lane + 32] = 0u;
         mbar_wait(&bar, phase);
         phase ^= 1u;
-        uint32_t cur[RA_IT], gv[RA_IT], loc[RA_IT], bn[RA_IT];
+        // loc: local (bits 0-19) | rank among the warp's records of the bin (bits 20-27) | valid (bit 31);
+        // the fine bin is recomputed from cur (fewer live registers)
+        constexpr uint32_t kValid = 0x80000000u;
+        uint32_t cur[RA_IT], gv[RA_IT], loc[RA_IT];
 #pragma unroll
         for (int j = 0; j < RA_IT; ++j) {
             const uint32_t e = j * RA_THREADS + t;
@@ -1330,16 +1313,18 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
             loc[j] = (uint32_t)r & lmask;
             // issued now, first used at the placement: the gathers fly while the tile is ranked
             gv[j] = ld_hint(IS1 + (sid < R1 ? sid : 0u), pol_last);
-            bn[j] = (e < cnt && (cur[j] >> cshift) == c) ? (cur[j] >> fshift) & fmask : 0xFFu;
+            if (e < cnt && (cur[j] >> cshift) == c) loc[j] |= kValid;
         }
         __syncwarp();  // this warp's counters are zeroed
 #pragma unroll
         for (int j = 0; j < RA_IT; ++j)
-            if (bn[j] != 0xFFu) loc[j] |= atomicAdd(&s_w[warp][bn[j]], 1u) << 20;  // local < 2^20 (host-checked)
-        __syncthreads();  // (1) staging consumed, every warp's counts in, the tile before last written out
+            if (loc[j] & kValid)  // local < 2^20 (host-checked)
+                loc[j] |= atomicAdd(&s_w[warp][(cur[j] >> fshift) & fmask], 1u) << 20;
+        __syncthreads();  // (1) staging consumed, every warp's counts in
         issue(tile + gridDim.x);
         // (warp, bin) counts -> absolute slots of the bin-sorted tile; one global
-        // atomic per non-empty bin claims the bin's run in its fine window (used next iteration)
+        // atomic per non-empty bin claims the bin's run in its fine window
+        uint32_t base = 0;
         if (t < 64) {
             const uint32_t d = t;
             uint32_t tot = 0;
@@ -1350,6 +1335,8 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
                     s_w[w][d] = tot;
                     tot += x;
                 }
+                // issued here, consumed after the placement
+                if (tot) base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot);
             }
             uint32_t incl = tot;
 #pragma unroll
@@ -1360,38 +1347,45 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
             if (t == 31) s_half = incl;
             asm volatile("bar.sync 1, 64;" ::: "memory");
             const uint32_t start = incl - tot + (t >= 32 ? s_half : 0u);
-            if (it > 0) publish_prev(k ^ 1);
             if (d < fb) {
 #pragma unroll
                 for (int w = 0; w < RA_WARPS; ++w) s_w[w][d] += start;
-                s_bs[k][d] = start;
-                if (d == fb - 1) s_bs[k][fb] = start + tot;
-                p_base = tot ? (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot) : 0u;
-                p_tot = tot;
-                p_start = start;
+                s_bs[d] = start;
+                if (d == fb - 1) s_bs[fb] = start + tot;
             }
         }
-        __syncthreads();  // (2) this tile's slots and the previous tile's claims known
-        unsigned long long* srt = s_sort0 + k * RA_TILE;
+        __syncthreads();  // (2) tile slots known
 #pragma unroll
         for (int j = 0; j < RA_IT; ++j) {
-            if (bn[j] != 0xFFu) {
-                const uint32_t pos = s_w[warp][bn[j]] + (loc[j] >> 20);
+            if (loc[j] & kValid) {
+                const uint32_t pos = s_w[warp][(cur[j] >> fshift) & fmask] + ((loc[j] >> 20) & 0xFFu);
                 const uint32_t rank = gv[j] - (loc[j] & 0xFFFFFu) - 1u;
-                srt[pos] = ((unsigned long long)cur[j] << 32) | rank;
+                s_sort[pos] = ((unsigned long long)cur[j] << 32) | rank;
             }
         }
-        if (it > 0) write_out(k ^ 1, c_prev);
-        c_prev = c;
-        // no closing barrier: the next tile rewrites s_w / s_bs[k ^ 1] / the other sorted
-        // buffer only after its barrier (1)
-    }
-    if (it > 0) {  // the last tile
-        const int k = (int)((it - 1) & 1u);
-        __syncthreads();  // its placement is complete
-        publish_prev(k);
-        __syncthreads();
-        write_out(k, c_prev);
+        if (t < fb) {  // the claims, now back
+            const uint32_t s0 = s_bs[t], cnt_b = s_bs[t + 1] - s0;
+            const uint32_t room = base < cap ? cap - base : 0u;
+            s_gb[t] = base;
+            s_ge[t] = s0 + (cnt_b < room ? cnt_b : room);
+        }
+        __syncthreads();  // (3) tile sorted, runs claimed
+        // write out: warp w copies the runs of bins w, w + RA_WARPS, ...
+        unsigned long long* wout = out + ((unsigned long long)c * fb << fshift);
+        for (uint32_t d = warp; d < fb; d += RA_WARPS) {
+            const uint32_t s0 = s_bs[d], s1 = s_bs[d + 1], se = s_ge[d];
+            unsigned long long* dst = wout + ((unsigned long long)d << fshift) + s_gb[d] - s0;
+            uint32_t i = s0 + lane;
+            for (; i + 32 < se; i += 64) {  // two loads in flight per lane
+                const unsigned long long x0 = s_sort[i], x1 = s_sort[i + 32];
+                __stcs(dst + i, x0);
+                __stcs(dst + i + 32, x1);
+            }
+            if (i < se) __stcs(dst + i, s_sort[i]);
+            if (se < s1) over = true;
+        }
+        // no closing barrier: the next tile rewrites s_w only after its own
+        // warps' write-out, and s_bs / s_gb / s_ge / s_sort after barrier (1)
     }
     if (over) st->bad = 1;
 }
@@ -2539,7 +2533,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
     bool tiled = false;
     if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
-        const size_t sma = ra_smem_bytes();
+        const size_t sma = ra_smem_bytes();  // (k_rs_refine_atom: staging + one sorted tile)
         SG_CUDA(set_smem_max(k_rs_refine_atom, sma));
         const uint32_t g = sm_count() * RA_CTAS_PER_SM;
         rec.begin(K_RS5_REFINE, 0, g, RA_THREADS, n);

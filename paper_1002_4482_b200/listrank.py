@@ -24,6 +24,7 @@ validated exactly like ``vkm.Machine`` (vkm.py:434-454) and recorded in
 import ctypes
 import functools
 import math
+import threading
 from collections import namedtuple
 from dataclasses import dataclass
 
@@ -116,6 +117,21 @@ def _raise_invalid(sl, code, viol):
     raise InvalidListError(str(ListViolation(VIOLATION_KINDS.get(kind, "unreachable"), int(index))))
 
 
+_META_STAGING = {}
+_META_LOCK = threading.Lock()
+
+
+def _meta_staging(dev, count):
+    """Pinned int64 staging block of at least `count` elements for device
+    `dev` (kept for the process; grows by doubling)."""
+    key = str(dev)
+    t = _META_STAGING.get(key)
+    if t is None or t.numel() < count:
+        t = torch.empty(max(count, 2 * (t.numel() if t is not None else 0)), dtype=torch.int64, pin_memory=True)
+        _META_STAGING[key] = t
+    return t
+
+
 def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=None):
     """Rank `sl` on the GPU.  Returns (rank tensor, native stats, status,
     violation, host_input).  `meta` = (spl_nodes, cache key) asks the ruling
@@ -153,15 +169,18 @@ def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=
                 r = len(spl_nodes)
                 idx = _device_index(spl_nodes, dev, key)
                 res = torch.empty((3, r), dtype=torch.int64, device=dev)
-                # a fresh block from torch's caching pinned allocator: the result
-                # array is a view of it (no 3r-element copy on the call's tail)
-                host = torch.empty(3 * r, dtype=torch.int64, pin_memory=True)
+                # a persistent pinned staging block per device: a fresh block from
+                # torch's caching pinned allocator costs a cudaHostAlloc (~1.5 ms)
+                # whenever its cache runs dry (measured: every few calls); the
+                # result is copied out after the call (3r int64, ~20 us)
                 mws = _device.workspace(L.sg_splitter_meta_workspace_bytes(r), dev)
-                rc = L.sg_rs_rank_meta(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
-                                       _device.ptr(ws), ws.numel(), _device.ptr(idx), r, _device.ptr(res),
-                                       ctypes.c_void_p(host.data_ptr()), _device.ptr(mws), mws.numel(), stream,
-                                       ctypes.byref(st), ctypes.byref(viol))
-                meta_out.append(host.numpy().reshape(3, r))
+                with _META_LOCK:  # the staging block is shared by the device's calls
+                    host = _meta_staging(dev, 3 * r)
+                    rc = L.sg_rs_rank_meta(_device.ptr(succ), sdt, _device.ptr(rank), odt, n,
+                                           int(seed) & (2**64 - 1), _device.ptr(ws), ws.numel(), _device.ptr(idx), r,
+                                           _device.ptr(res), ctypes.c_void_p(host.data_ptr()), _device.ptr(mws),
+                                           mws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
+                    meta_out.append(host.numpy()[: 3 * r].reshape(3, r).copy())
         del ws
     if rc not in (_native.SG_OK, _native.SG_ERR_INVALID_LIST):
         _native.check(rc, f"sg_{kind}_rank")

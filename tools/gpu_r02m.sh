@@ -1,0 +1,18 @@
+#!/bin/bash
+# refine atom (claim overlapped, no spills); partition 8 rows/lane; sanitizer pass
+TAG=${TAG:-r02m}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
+timeout 900 python -m pytest tests/test_concomp_gpu.py tests/test_listrank_gpu.py -q -x > $O/pytest.log 2>&1
+timeout 300 python bench.py --workload cc26 --steps 10 --warmup 3 --no-e2e --no-cpu --blocks none > $O/cc26.json 2>$O/cc26.err
+timeout 300 python bench.py --workload lr28 --steps 10 --warmup 3 --no-e2e --no-cpu --blocks none > $O/lr28.json 2>$O/lr28.err
+timeout 300 python bench.py --workload lr26 --steps 10 --warmup 3 --no-e2e --no-cpu --blocks none > $O/lr26.json 2>$O/lr26.err
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:refine -s 2 -c 1 \
+    -o $O/ncu_refine_atom python bench.py --workload lr28 --steps 1 --warmup 3 --no-e2e --no-cpu --blocks none > $O/ncu_refine.log 2>&1
+tail -n 3 $O/pytest.log
+for f in $O/*.json; do python -c "
+import json,sys
+d=json.loads(open('$f').read().strip().splitlines()[-1]); k=d['kernels_ms_per_step']; print('$f', d['ms_per_step'], round(sum(k.values()),4), {a:b for a,b in k.items() if b>0.1}, d['clocks']['samples'], d.get('step_ms_spread'))"; done
+TAG=$TAG timeout 2400 bash tools/sanitize.sh > $O/sanitize.log 2>&1
+tail -40 $O/san_summary.txt
