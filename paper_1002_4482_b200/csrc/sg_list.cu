@@ -1265,11 +1265,14 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
     unsigned long long* s_in = reinterpret_cast<unsigned long long*>(ra_raw);
     unsigned long long* s_sort = s_in + RA_TILE;
     __shared__ unsigned long long bar;
-    __shared__ uint32_t s_w[RA_WARPS][RA_MAXB];  // per-warp bin counts -> absolute tile slots
+    // per-(bin, warp) counts -> absolute tile slots, bin-major with a stride of
+    // RA_WARPS + 1 words so a warp's counter updates spread over the banks
+    constexpr uint32_t kStride = RA_WARPS + 1;
+    __shared__ uint32_t s_c[RA_MAXB * kStride];
+    __shared__ uint32_t s_tot[RA_WARPS];
     __shared__ uint32_t s_bs[RA_MAXB + 1];        // bin starts in the sorted tile
     __shared__ uint32_t s_gb[RA_MAXB];            // window slot of the bin's first tile record
     __shared__ uint32_t s_ge[RA_MAXB];            // tile end of the bin's writable run
-    __shared__ uint32_t s_half;
     const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
     const unsigned long long ntiles = (n + RA_TILE - 1) / RA_TILE;
     const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
@@ -1296,8 +1299,8 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
         const unsigned long long e0 = tile * RA_TILE;
         const uint32_t cnt = (uint32_t)min((unsigned long long)RA_TILE, n - e0);
         const uint32_t c = (uint32_t)(e0 >> cshift);  // tiles never straddle a coarse window
-        s_w[warp][lane] = 0u;
-        s_w[warp][lane + 32] = 0u;
+        s_c[lane * kStride + warp] = 0u;  // this warp's counters
+        s_c[(lane + 32) * kStride + warp] = 0u;
         mbar_wait(&bar, phase);
         phase ^= 1u;
         // loc: local (bits 0-19) | rank among the warp's records of the bin (bits 20-27) | valid (bit 31);
@@ -1316,78 +1319,182 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
             if (e < cnt && (cur[j] >> cshift) == c) loc[j] |= kValid;
         }
         __syncwarp();  // this warp's counters are zeroed
+        // branch-free: an invalid record adds 0 to bin 0, so the eight atomics issue back to back
+        uint32_t slot[RA_IT];
 #pragma unroll
-        for (int j = 0; j < RA_IT; ++j)
-            if (loc[j] & kValid)  // local < 2^20 (host-checked)
-                loc[j] |= atomicAdd(&s_w[warp][(cur[j] >> fshift) & fmask], 1u) << 20;
+        for (int j = 0; j < RA_IT; ++j) {
+            const bool v = (loc[j] & kValid) != 0;
+            slot[j] = atomicAdd(&s_c[(v ? (cur[j] >> fshift) & fmask : 0u) * kStride + warp], v ? 1u : 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < RA_IT; ++j) loc[j] |= slot[j] << 20;  // local < 2^20 (host-checked)
         __syncthreads();  // (1) staging consumed, every warp's counts in
         issue(tile + gridDim.x);
-        // (warp, bin) counts -> absolute slots of the bin-sorted tile; one global
-        // atomic per non-empty bin claims the bin's run in its fine window
-        uint32_t base = 0;
-        if (t < 64) {
-            const uint32_t d = t;
-            uint32_t tot = 0;
-            if (d < fb) {
+        // (bin, warp) counts -> absolute slots of the bin-sorted tile: a block
+        // scan in bin-major order, thread t owning bin t / 4, warps 2 (t % 4) and
+        // 2 (t % 4) + 1; one global atomic per non-empty bin claims the bin's
+        // run in its fine window (issued here, consumed after the placement)
+        const uint32_t bq = t >> 2, i0 = bq * kStride + 2 * (t & 3u);
+        const uint32_t a0 = s_c[i0], a1 = s_c[i0 + 1], pair = a0 + a1;
+        uint32_t incl = pair;
 #pragma unroll
-                for (int w = 0; w < RA_WARPS; ++w) {
-                    const uint32_t x = s_w[w][d];
-                    s_w[w][d] = tot;
-                    tot += x;
-                }
-                // issued here, consumed after the placement
-                if (tot) base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + d, (unsigned long long)tot);
-            }
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((int)lane >= o) incl += y;
-            }
-            if (t == 31) s_half = incl;
-            asm volatile("bar.sync 1, 64;" ::: "memory");
-            const uint32_t start = incl - tot + (t >= 32 ? s_half : 0u);
-            if (d < fb) {
-#pragma unroll
-                for (int w = 0; w < RA_WARPS; ++w) s_w[w][d] += start;
-                s_bs[d] = start;
-                if (d == fb - 1) s_bs[fb] = start + tot;
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += y;
         }
+        if (lane == 31) s_tot[warp] = incl;
+        // the bin's total: the four threads of a bin are adjacent lanes
+        uint32_t btot = pair;
+        btot += __shfl_xor_sync(0xffffffffu, btot, 1);
+        btot += __shfl_xor_sync(0xffffffffu, btot, 2);
+        uint32_t base = 0;
+        const bool head = (t & 3u) == 0 && bq < fb;
+        if (head && btot) base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + bq, (unsigned long long)btot);
+        __syncthreads();  // (1b) warp totals
+        uint32_t woff = lane < (uint32_t)warp ? s_tot[lane] : 0u;  // lanes < 8 hold the earlier warps' totals
+#pragma unroll
+        for (int o = 1; o < RA_WARPS; o <<= 1) woff += __shfl_xor_sync(0xffffffffu, woff, o);
+        woff = __shfl_sync(0xffffffffu, woff, 0);  // (the reduction ran in groups of RA_WARPS lanes)
+        const uint32_t excl = incl - pair + woff;
+        s_c[i0] = excl;
+        s_c[i0 + 1] = excl + a0;
+        if (head) s_bs[bq] = excl;
+        if (t == RA_THREADS - 1) s_bs[fb] = incl + woff;  // every record of the tile (bins >= fb are empty)
         __syncthreads();  // (2) tile slots known
 #pragma unroll
         for (int j = 0; j < RA_IT; ++j) {
             if (loc[j] & kValid) {
-                const uint32_t pos = s_w[warp][(cur[j] >> fshift) & fmask] + ((loc[j] >> 20) & 0xFFu);
+                const uint32_t pos = s_c[((cur[j] >> fshift) & fmask) * kStride + warp] + ((loc[j] >> 20) & 0xFFu);
                 const uint32_t rank = gv[j] - (loc[j] & 0xFFFFFu) - 1u;
                 s_sort[pos] = ((unsigned long long)cur[j] << 32) | rank;
             }
         }
-        if (t < fb) {  // the claims, now back
-            const uint32_t s0 = s_bs[t], cnt_b = s_bs[t + 1] - s0;
+        if (head) {  // the claims, now back
             const uint32_t room = base < cap ? cap - base : 0u;
-            s_gb[t] = base;
-            s_ge[t] = s0 + (cnt_b < room ? cnt_b : room);
+            s_gb[bq] = base;
+            s_ge[bq] = excl + (btot < room ? btot : room);
         }
         __syncthreads();  // (3) tile sorted, runs claimed
-        // write out: warp w copies the runs of bins w, w + RA_WARPS, ...
+        // write out, flat: slot i -> its bin's run in the fine window (consecutive
+        // slots of a bin are consecutive in the window, so a warp's stores coalesce)
         unsigned long long* wout = out + ((unsigned long long)c * fb << fshift);
-        for (uint32_t d = warp; d < fb; d += RA_WARPS) {
-            const uint32_t s0 = s_bs[d], s1 = s_bs[d + 1], se = s_ge[d];
-            unsigned long long* dst = wout + ((unsigned long long)d << fshift) + s_gb[d] - s0;
-            uint32_t i = s0 + lane;
-            for (; i + 32 < se; i += 64) {  // two loads in flight per lane
-                const unsigned long long x0 = s_sort[i], x1 = s_sort[i + 32];
-                __stcs(dst + i, x0);
-                __stcs(dst + i + 32, x1);
-            }
-            if (i < se) __stcs(dst + i, s_sort[i]);
-            if (se < s1) over = true;
+        const uint32_t total = s_bs[fb];
+#pragma unroll 4
+        for (uint32_t i = t; i < total; i += RA_THREADS) {
+            const unsigned long long x = s_sort[i];
+            const uint32_t d = ((uint32_t)(x >> 32) >> fshift) & fmask;
+            if (i < s_ge[d])
+                __stcs(wout + ((unsigned long long)d << fshift) + s_gb[d] + (i - s_bs[d]), x);
+            else
+                over = true;
         }
-        // no closing barrier: the next tile rewrites s_w only after its own
-        // warps' write-out, and s_bs / s_gb / s_ge / s_sort after barrier (1)
+        // no closing barrier: the next tile zeroes a warp's counters from that
+        // warp, and rewrites s_bs / s_gb / s_ge / s_sort after barrier (1)
     }
     if (over) st->bad = 1;
+}
+
+// rs5_refine, warp-autonomous variant (SG_RS_REFINE=7): every warp ranks,
+// claims and writes its own 256-record tile (8 per lane) -- warp-private bin
+// counters, one warp scan, one global claim per non-empty bin, a warp-private
+// sorted tile in shared memory -- so no block barrier is ever taken; the
+// price is 8x more claim atomics (one per bin per 256 records).
+constexpr int RW_THREADS = 256;
+constexpr int RW_WARPS = RW_THREADS / 32;
+constexpr int RW_IT = 8;
+constexpr int RW_TILE = 32 * RW_IT;  // 256 records per warp tile
+constexpr int RW_CTAS_PER_SM = 4;
+
+__global__ void __launch_bounds__(RW_THREADS, RW_CTAS_PER_SM) k_rs_refine_warp(
+    const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
+    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
+    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
+    if (layout_local(st) || st->overflow) return;
+    const uint32_t fb = 1u << (cshift - fshift);  // <= 64
+    __shared__ unsigned long long s_sort[RW_WARPS][RW_TILE];
+    __shared__ uint32_t s_cnt[RW_WARPS][64];  // counts -> run starts in the sorted tile
+    __shared__ uint32_t s_gb[RW_WARPS][64];   // window slot of the run's first record
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
+    const unsigned long long pol_last = l2_evict_last();
+    const uint32_t fmask = fb - 1;
+    const uint32_t lmask = (1u << lb) - 1u;
+    const uint32_t smask = (uint32_t)((1ull << (sb - lb)) - 1);
+    const uint32_t cap = 1u << fshift;
+    constexpr uint32_t kValid = 0x80000000u;
+    const unsigned long long ntiles = (n + RW_TILE - 1) / RW_TILE;
+    const unsigned long long nw = (unsigned long long)gridDim.x * RW_WARPS;
+    bool over = false;
+    for (unsigned long long tile = (unsigned long long)blockIdx.x * RW_WARPS + warp; tile < ntiles; tile += nw) {
+        const unsigned long long e0 = tile * RW_TILE;
+        const uint32_t cnt = (uint32_t)min((unsigned long long)RW_TILE, n - e0);
+        const uint32_t c = (uint32_t)(e0 >> cshift);
+        s_cnt[warp][lane] = 0u;
+        s_cnt[warp][lane + 32] = 0u;
+        uint32_t cur[RW_IT], gv[RW_IT], loc[RW_IT];
+        unsigned long long r[RW_IT];
+#pragma unroll
+        for (int j = 0; j < RW_IT; ++j) {
+            const uint32_t e = j * 32 + lane;
+            r[j] = e < cnt ? __ldcs(in + e0 + e) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < RW_IT; ++j) {
+            const uint32_t e = j * 32 + lane;
+            cur[j] = (uint32_t)(r[j] >> sb);
+            const uint32_t sid = (uint32_t)(r[j] >> lb) & smask;
+            loc[j] = (uint32_t)r[j] & lmask;
+            gv[j] = ld_hint(IS1 + (sid < R1 ? sid : 0u), pol_last);
+            if (e < cnt && (cur[j] >> cshift) == c) loc[j] |= kValid;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < RW_IT; ++j)
+            if (loc[j] & kValid) loc[j] |= atomicAdd(&s_cnt[warp][(cur[j] >> fshift) & fmask], 1u) << 20;
+        __syncwarp();
+        // lane l owns bins 2l, 2l + 1: run starts (warp scan) and the global claims
+        const uint32_t c0 = s_cnt[warp][2 * lane], c1 = s_cnt[warp][2 * lane + 1];
+        uint32_t incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += y;
+        }
+        const uint32_t st0 = incl - c0 - c1;
+        uint32_t g0 = 0, g1 = 0;
+        const unsigned long long* cb = cursor + (unsigned long long)c * fb;
+        if (c0) g0 = (uint32_t)atomicAdd((unsigned long long*)cb + 2 * lane, (unsigned long long)c0);
+        if (c1) g1 = (uint32_t)atomicAdd((unsigned long long*)cb + 2 * lane + 1, (unsigned long long)c1);
+        __syncwarp();
+        s_cnt[warp][2 * lane] = st0;
+        s_cnt[warp][2 * lane + 1] = st0 + c0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < RW_IT; ++j) {
+            if (loc[j] & kValid) {
+                const uint32_t pos = s_cnt[warp][(cur[j] >> fshift) & fmask] + ((loc[j] >> 20) & 0xFFu);
+                s_sort[warp][pos] = ((unsigned long long)cur[j] << 32) | (gv[j] - (loc[j] & 0xFFFFFu) - 1u);
+            }
+        }
+        s_gb[warp][2 * lane] = g0;
+        s_gb[warp][2 * lane + 1] = g1;
+        __syncwarp();
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long* wout = out + ((unsigned long long)c * fb << fshift);
+        for (uint32_t i = lane; i < total; i += 32) {
+            const unsigned long long x = s_sort[warp][i];
+            const uint32_t d = ((uint32_t)(x >> 32) >> fshift) & fmask;
+            const uint32_t slot = s_gb[warp][d] + (i - s_cnt[warp][d]);
+            if (slot < cap)
+                __stcs(wout + ((unsigned long long)d << fshift) + slot, x);
+            else
+                over = true;
+        }
+        __syncwarp();
+    }
+    if (over) st->bad = 1;
+    (void)lt;
 }
 
 // rs5_scatter over the tile layout of k_rs_refine_lean<.., true>: one CTA
@@ -2532,7 +2639,12 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
     const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
     bool tiled = false;
-    if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
+    if (lean_ok && tu_r.rs_refine == 7 && p.cshift >= 8) {
+        const uint32_t g = sm_count() * RW_CTAS_PER_SM;
+        rec.begin(K_RS5_REFINE, 0, g, RW_THREADS, n);
+        k_rs_refine_warp<<<g, RW_THREADS, 0, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
+                                                 b.IS[1], p.rec_sb, p.rec_lb);
+    } else if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
         const size_t sma = ra_smem_bytes();  // (k_rs_refine_atom: staging + one sorted tile)
         SG_CUDA(set_smem_max(k_rs_refine_atom, sma));
         const uint32_t g = sm_count() * RA_CTAS_PER_SM;
