@@ -1394,109 +1394,6 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
     if (over) st->bad = 1;
 }
 
-// rs5_refine, warp-autonomous variant (SG_RS_REFINE=7): every warp ranks,
-// claims and writes its own 256-record tile (8 per lane) -- warp-private bin
-// counters, one warp scan, one global claim per non-empty bin, a warp-private
-// sorted tile in shared memory -- so no block barrier is ever taken; the
-// price is 8x more claim atomics (one per bin per 256 records).
-constexpr int RW_THREADS = 256;
-constexpr int RW_WARPS = RW_THREADS / 32;
-constexpr int RW_IT = 8;
-constexpr int RW_TILE = 32 * RW_IT;  // 256 records per warp tile
-constexpr int RW_CTAS_PER_SM = 4;
-
-__global__ void __launch_bounds__(RW_THREADS, RW_CTAS_PER_SM) k_rs_refine_warp(
-    const unsigned long long* __restrict__ in, unsigned long long* __restrict__ cursor,
-    unsigned long long* __restrict__ out, ListStatus* st, unsigned long long n, uint32_t cshift, uint32_t fshift,
-    const uint32_t* __restrict__ IS1, uint32_t sb, uint32_t lb) {
-    if (layout_local(st) || st->overflow) return;
-    const uint32_t fb = 1u << (cshift - fshift);  // <= 64
-    __shared__ unsigned long long s_sort[RW_WARPS][RW_TILE];
-    __shared__ uint32_t s_cnt[RW_WARPS][64];  // counts -> run starts in the sorted tile
-    __shared__ uint32_t s_gb[RW_WARPS][64];   // window slot of the run's first record
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
-    const unsigned long long pol_last = l2_evict_last();
-    const uint32_t fmask = fb - 1;
-    const uint32_t lmask = (1u << lb) - 1u;
-    const uint32_t smask = (uint32_t)((1ull << (sb - lb)) - 1);
-    const uint32_t cap = 1u << fshift;
-    constexpr uint32_t kValid = 0x80000000u;
-    const unsigned long long ntiles = (n + RW_TILE - 1) / RW_TILE;
-    const unsigned long long nw = (unsigned long long)gridDim.x * RW_WARPS;
-    bool over = false;
-    for (unsigned long long tile = (unsigned long long)blockIdx.x * RW_WARPS + warp; tile < ntiles; tile += nw) {
-        const unsigned long long e0 = tile * RW_TILE;
-        const uint32_t cnt = (uint32_t)min((unsigned long long)RW_TILE, n - e0);
-        const uint32_t c = (uint32_t)(e0 >> cshift);
-        s_cnt[warp][lane] = 0u;
-        s_cnt[warp][lane + 32] = 0u;
-        uint32_t cur[RW_IT], gv[RW_IT], loc[RW_IT];
-        unsigned long long r[RW_IT];
-#pragma unroll
-        for (int j = 0; j < RW_IT; ++j) {
-            const uint32_t e = j * 32 + lane;
-            r[j] = e < cnt ? __ldcs(in + e0 + e) : 0ull;
-        }
-#pragma unroll
-        for (int j = 0; j < RW_IT; ++j) {
-            const uint32_t e = j * 32 + lane;
-            cur[j] = (uint32_t)(r[j] >> sb);
-            const uint32_t sid = (uint32_t)(r[j] >> lb) & smask;
-            loc[j] = (uint32_t)r[j] & lmask;
-            gv[j] = ld_hint(IS1 + (sid < R1 ? sid : 0u), pol_last);
-            if (e < cnt && (cur[j] >> cshift) == c) loc[j] |= kValid;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < RW_IT; ++j)
-            if (loc[j] & kValid) loc[j] |= atomicAdd(&s_cnt[warp][(cur[j] >> fshift) & fmask], 1u) << 20;
-        __syncwarp();
-        // lane l owns bins 2l, 2l + 1: run starts (warp scan) and the global claims
-        const uint32_t c0 = s_cnt[warp][2 * lane], c1 = s_cnt[warp][2 * lane + 1];
-        uint32_t incl = c0 + c1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((int)lane >= o) incl += y;
-        }
-        const uint32_t st0 = incl - c0 - c1;
-        uint32_t g0 = 0, g1 = 0;
-        const unsigned long long* cb = cursor + (unsigned long long)c * fb;
-        if (c0) g0 = (uint32_t)atomicAdd((unsigned long long*)cb + 2 * lane, (unsigned long long)c0);
-        if (c1) g1 = (uint32_t)atomicAdd((unsigned long long*)cb + 2 * lane + 1, (unsigned long long)c1);
-        __syncwarp();
-        s_cnt[warp][2 * lane] = st0;
-        s_cnt[warp][2 * lane + 1] = st0 + c0;
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < RW_IT; ++j) {
-            if (loc[j] & kValid) {
-                const uint32_t pos = s_cnt[warp][(cur[j] >> fshift) & fmask] + ((loc[j] >> 20) & 0xFFu);
-                s_sort[warp][pos] = ((unsigned long long)cur[j] << 32) | (gv[j] - (loc[j] & 0xFFFFFu) - 1u);
-            }
-        }
-        s_gb[warp][2 * lane] = g0;
-        s_gb[warp][2 * lane + 1] = g1;
-        __syncwarp();
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long* wout = out + ((unsigned long long)c * fb << fshift);
-        for (uint32_t i = lane; i < total; i += 32) {
-            const unsigned long long x = s_sort[warp][i];
-            const uint32_t d = ((uint32_t)(x >> 32) >> fshift) & fmask;
-            const uint32_t slot = s_gb[warp][d] + (i - s_cnt[warp][d]);
-            if (slot < cap)
-                __stcs(wout + ((unsigned long long)d << fshift) + slot, x);
-            else
-                over = true;
-        }
-        __syncwarp();
-    }
-    if (over) st->bad = 1;
-    (void)lt;
-}
-
 // rs5_scatter over the tile layout of k_rs_refine_lean<.., true>: one CTA
 // per fine window f (bin d of coarse window c) collects bin d's run from
 // each of the coarse window's tiles -- lane l of a warp reads the run bounds
@@ -2639,12 +2536,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
     const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
     bool tiled = false;
-    if (lean_ok && tu_r.rs_refine == 7 && p.cshift >= 8) {
-        const uint32_t g = sm_count() * RW_CTAS_PER_SM;
-        rec.begin(K_RS5_REFINE, 0, g, RW_THREADS, n);
-        k_rs_refine_warp<<<g, RW_THREADS, 0, s>>>(b.pairs, b.cursor + p.cbins, b.rec_sl, b.st, n, p.cshift, p.fshift,
-                                                 b.IS[1], p.rec_sb, p.rec_lb);
-    } else if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
+    if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
         const size_t sma = ra_smem_bytes();  // (k_rs_refine_atom: staging + one sorted tile)
         SG_CUDA(set_smem_max(k_rs_refine_atom, sma));
         const uint32_t g = sm_count() * RA_CTAS_PER_SM;

@@ -472,12 +472,12 @@ def test_plan_boundaries(cuda, orc, n):
     assert np.array_equal(out.cpu().numpy().astype(np.int64), want)
 
 
-@pytest.mark.parametrize("refine", ["0", "1", "2", "3", "4", "5", "6", "7"])
+@pytest.mark.parametrize("refine", ["0", "1", "2", "3", "4", "5", "6"])
 def test_refine_variants(cuda, orc, sg_env, refine):
     """rs5_refine variants (SG_RS_REFINE: 0 shared-atomic ranking, the
     default; 1 the block multisplit refine; 2 lean + match.any; 3 lean,
     alternating; 4 lean in the tile layout; 5 lean + shared atomics; 6 lean +
-    ballots; 7 warp-autonomous tiles) on
+    ballots) on
     windows shrunk to 8 KiB (SG_RS_WIN_KB=8) so 2^20 nodes already split
     every coarse window into 8 fine bins and 2^25 nodes into 64 (the C3
     fan-out): exact against the oracle, and the size-independent rank
@@ -491,3 +491,4 @@ def test_refine_variants(cuda, orc, sg_env, refine):
     rank, st = g.rs_rank(big, 16384)
     assert st.meta["fallback"] is False
     _check_rank_properties(big.succ, rank)
+

@@ -1,0 +1,18 @@
+#!/bin/bash
+# fused refine + scatter without / with the L2 discard
+TAG=${TAG:-r02u}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
+timeout 1200 python -m pytest tests/test_listrank_gpu.py -q -x -k "refine" > $O/pytest.log 2>&1
+for f in 1 2 0; do
+for w in lr28 lr26; do
+  SG_RS_SCATTER_FUSE=$f timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-e2e --no-cpu --blocks none > $O/${w}_f$f.json 2>$O/${w}_f$f.err
+done
+done
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:refine -s 2 -c 1 \
+    -o $O/ncu_refine28 python bench.py --workload lr28 --steps 1 --warmup 3 --no-e2e --no-cpu --blocks none > $O/ncu_refine28.log 2>&1
+tail -n 3 $O/pytest.log
+for f in $O/*.json; do python -c "
+import json,sys
+d=json.loads(open('$f').read().strip().splitlines()[-1]); k=d['kernels_ms_per_step']; print('$f', d['ms_per_step'], round(sum(k.values()),4), d.get('step_ms_spread'), k.get('rs5_refine'), k.get('rs5_scatter'))"; done
