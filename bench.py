@@ -409,6 +409,21 @@ def measure(a, ctx, name, primary):
                                       "contraction moves ~20 B/node, so frac can exceed 1") if kind == "list"
                              else ("SURVEY 8(d) E*72*m + V*40*n (per rank): every parent gather charged a 32-B "
                                    "DRAM sector although the window partition serves them from L2")}}
+    if traffic and k_ms:
+        # the same kernel against what it actually moved (ncu DRAM bytes): the
+        # honest utilisation where a per-access model over- or under-charges
+        meas = traffic / (k_ms / 1e3) / 1e9
+        roofline["measured_dram"] = {"achieved": round(meas, 1), "frac": round(meas / peak, 4),
+                                     "bytes_per_launch_set": traffic}
+    if kname.startswith("cc_hook"):
+        roofline["bound_note"] = ("latency-bound, not HBM-bound: union-find finds and root CAS against an "
+                                  "L2-resident window of the parent array (ncu L2 hit ~60 %); SURVEY's 72 B/edge "
+                                  "charges every parent gather a DRAM sector the window partition never pays, so "
+                                  "frac can exceed 1 -- measured_dram is the utilisation")
+    elif kname == "rs3_walk" and order == "random":
+        roofline["bound_note"] = ("random-access bound: one dependent 4-B succ load per hop, each costing ~97-133 B "
+                                  "of DRAM (sector + overfetch, ncu); the walk runs at the measured random-gather "
+                                  "ceiling (profiles/r01_ubench_random.txt)")
     srt = sorted(step_ms)
     res = {"value": round(value, 1), "unit": unit, "ms_per_step": round(ms_per_step, 4), "steps": a.steps,
            "timing": "CUDA events on the launching stream around each API call; python cyclic GC paused over "

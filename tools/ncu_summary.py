@@ -31,7 +31,8 @@ NAME_MAP = {"k_rs_contract_expand": "rs5_expand", "k_rs_contract_link": "rs3_lin
             "k_cc_part_scatter2": "cc_partition_scatter","k_rs_walk_stage": "rs3_walk", "k_rs_walk_bin": "rs3_walk",
             "k_rs_top_jump": "rs4_rank", "k_rs_top_init": "rs4_rank", "k_rs_top_coop": "rs4_rank", "k_spl_meta_block": "splitter_meta", "k_rs_walk_rec": "rs3_walk", "k_rs_walk<sg::Level0": "rs3_walk",
             "k_rs_walk<Level0": "rs3_walk", "k_rs_walk<sg::LevelK": "rs4_walk", "k_rs_walk<LevelK": "rs4_walk",
-            "k_rs_rec_refine": "rs5_refine", "k_rs_rec_scatter": "rs5_scatter", "k_rs_rec_partition": "rs5_partition",
+            "k_rs_rec_refine": "rs5_refine", "k_rs_refine_atom": "rs5_refine", "k_rs_refine_lean": "rs5_refine",
+            "k_cc_part_chunks": "cc_partition", "k_rs_rec_scatter": "rs5_scatter", "k_rs_rec_partition": "rs5_partition",
             "k_rs_expand0": "rs5_expand", "k_rs_count0": "rs1_validate", "k_cc_hook_uf": "cc_hook_uf",
             "k_cc_hook_sv": "cc_hook_sv", "k_cc_part_scatter": "cc_partition_scatter",
             "k_cc_part_count": "cc_partition_count", "k_wy_jump": "wy_jump", "k_cc_compress": "cc_shortcut"}
