@@ -1271,8 +1271,8 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
     __shared__ uint32_t s_c[RA_MAXB * kStride];
     __shared__ uint32_t s_tot[RA_WARPS];
     __shared__ uint32_t s_bs[RA_MAXB + 1];        // bin starts in the sorted tile
-    __shared__ uint32_t s_gb[RA_MAXB];            // window slot of the bin's first tile record
-    __shared__ uint32_t s_ge[RA_MAXB];            // tile end of the bin's writable run
+    // per bin: {window slot of the bin's first tile record minus its tile slot, tile end of the writable run}
+    __shared__ uint2 s_de[RA_MAXB];
     const uint32_t t = threadIdx.x, lane = lane_id(), warp = t >> 5;
     const unsigned long long ntiles = (n + RA_TILE - 1) / RA_TILE;
     const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
@@ -1371,8 +1371,7 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
         }
         if (head) {  // the claims, now back
             const uint32_t room = base < cap ? cap - base : 0u;
-            s_gb[bq] = base;
-            s_ge[bq] = excl + (btot < room ? btot : room);
+            s_de[bq] = make_uint2(base - excl, excl + (btot < room ? btot : room));
         }
         __syncthreads();  // (3) tile sorted, runs claimed
         // write out, flat: slot i -> its bin's run in the fine window (consecutive
@@ -1383,13 +1382,14 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
         for (uint32_t i = t; i < total; i += RA_THREADS) {
             const unsigned long long x = s_sort[i];
             const uint32_t d = ((uint32_t)(x >> 32) >> fshift) & fmask;
-            if (i < s_ge[d])
-                __stcs(wout + ((unsigned long long)d << fshift) + s_gb[d] + (i - s_bs[d]), x);
+            const uint2 de = s_de[d];
+            if (i < de.y)
+                __stcs(wout + ((unsigned long long)d << fshift) + (uint32_t)(i + de.x), x);
             else
                 over = true;
         }
         // no closing barrier: the next tile zeroes a warp's counters from that
-        // warp, and rewrites s_bs / s_gb / s_ge / s_sort after barrier (1)
+        // warp, and rewrites s_bs / s_de / s_sort after barrier (1)
     }
     if (over) st->bad = 1;
 }
