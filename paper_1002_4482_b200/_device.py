@@ -96,14 +96,16 @@ def exec_stats(st):
     es = ExecStats(backend="sm_100a")
     nl = min(st.n_launches, _native.SG_MAX_LAUNCHES)
     resolved = []
+    warnings = es.warnings  # (the closures hold the list, not `es`: no reference cycle, so a
+    #                          dropped ExecStats -- and the meta arrays it holds -- is freed at once)
 
     def resolve():  # event times are read on first use (sg_stats_resolve)
         if not resolved:
             rc = _native.lib().sg_stats_resolve(ctypes.byref(st))
             resolved.append(rc == _native.SG_OK)
             if rc != _native.SG_OK:
-                es.warnings.append("launch timings unavailable: this call's CUDA events were recycled "
-                                   "(read ExecStats timings within 64 calls on the device)")
+                warnings.append("launch timings unavailable: this call's CUDA events were recycled "
+                                "(read ExecStats timings within 64 calls on the device)")
         return resolved[0]
 
     def build():  # `st` is this call's own sg_stats, kept alive by the closure

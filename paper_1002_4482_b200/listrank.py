@@ -23,8 +23,9 @@ validated exactly like ``vkm.Machine`` (vkm.py:434-454) and recorded in
 
 import ctypes
 import functools
+import collections
 import math
-import threading
+import weakref
 from collections import namedtuple
 from dataclasses import dataclass
 
@@ -117,19 +118,40 @@ def _raise_invalid(sl, code, viol):
     raise InvalidListError(str(ListViolation(VIOLATION_KINDS.get(kind, "unreachable"), int(index))))
 
 
-_META_STAGING = {}
-_META_LOCK = threading.Lock()
+class _PinnedPool:
+    """Pinned int64 host blocks for meta["splitter_set"], recycled: a block is
+    lent to one call, its result arrays are views of it, and it returns to the
+    pool when the last of those views is gone (weakref.finalize on the numpy
+    array every view hangs off).  A fresh block from torch's caching pinned
+    allocator costs a cudaHostAlloc (~1.5 ms) whenever that cache runs dry
+    (measured: every few calls), and copying the result out of one shared
+    block costs ~100 us per call."""
+
+    def __init__(self):
+        # no lock: the finalizer can run inside any allocation of any thread
+        # (a lock taken here could be re-entered by it); deque append / pop
+        # and dict.setdefault are atomic under the GIL
+        self.free = {}
+
+    def take(self, count):
+        try:
+            return self.free[count].pop()
+        except (KeyError, IndexError):
+            return torch.empty(count, dtype=torch.int64, pin_memory=True)
+
+    def lend(self, block, count, shape):
+        """numpy view of `block` whose death returns `block` to the pool."""
+        own = block.numpy()
+        weakref.finalize(own, self._give_back, count, block)
+        return own[:count].reshape(shape)
+
+    def _give_back(self, count, block):
+        q = self.free.setdefault(count, collections.deque())
+        if len(q) < 8:
+            q.append(block)
 
 
-def _meta_staging(dev, count):
-    """Pinned int64 staging block of at least `count` elements for device
-    `dev` (kept for the process; grows by doubling)."""
-    key = str(dev)
-    t = _META_STAGING.get(key)
-    if t is None or t.numel() < count:
-        t = torch.empty(max(count, 2 * (t.numel() if t is not None else 0)), dtype=torch.int64, pin_memory=True)
-        _META_STAGING[key] = t
-    return t
+_META_POOL = _PinnedPool()
 
 
 def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=None):
@@ -174,13 +196,12 @@ def _run_list(kind, sl, variant_code, seed, reuse_succ, scratch_out=False, meta=
                 # whenever its cache runs dry (measured: every few calls); the
                 # result is copied out after the call (3r int64, ~20 us)
                 mws = _device.workspace(L.sg_splitter_meta_workspace_bytes(r), dev)
-                with _META_LOCK:  # the staging block is shared by the device's calls
-                    host = _meta_staging(dev, 3 * r)
-                    rc = L.sg_rs_rank_meta(_device.ptr(succ), sdt, _device.ptr(rank), odt, n,
-                                           int(seed) & (2**64 - 1), _device.ptr(ws), ws.numel(), _device.ptr(idx), r,
-                                           _device.ptr(res), ctypes.c_void_p(host.data_ptr()), _device.ptr(mws),
-                                           mws.numel(), stream, ctypes.byref(st), ctypes.byref(viol))
-                    meta_out.append(host.numpy()[: 3 * r].reshape(3, r).copy())
+                host = _META_POOL.take(3 * r)  # this call's own block (recycled, see _PinnedPool)
+                rc = L.sg_rs_rank_meta(_device.ptr(succ), sdt, _device.ptr(rank), odt, n, int(seed) & (2**64 - 1),
+                                       _device.ptr(ws), ws.numel(), _device.ptr(idx), r, _device.ptr(res),
+                                       ctypes.c_void_p(host.data_ptr()), _device.ptr(mws), mws.numel(), stream,
+                                       ctypes.byref(st), ctypes.byref(viol))
+                meta_out.append(_META_POOL.lend(host, 3 * r, (3, r)))
         del ws
     if rc not in (_native.SG_OK, _native.SG_ERR_INVALID_LIST):
         _native.check(rc, f"sg_{kind}_rank")
@@ -240,12 +261,16 @@ def _draw_splitters(n, r, seed):
     arguments; cached for r <= _CACHE_MAX_R)."""
     if int(r) > _CACHE_MAX_R:
         return _draw_splitters_uncached(int(n), int(r), int(seed))
-    return _draw_splitters_cached(int(n), int(r), int(seed)).copy()
+    return _draw_splitters_cached(int(n), int(r), int(seed))  # read-only, shared by the calls that drew it
 
 
 @functools.lru_cache(maxsize=64)
 def _draw_splitters_cached(n, r, seed):
-    return _draw_splitters_uncached(n, r, seed)
+    a = _draw_splitters_uncached(n, r, seed)
+    a.setflags(write=False)
+    return a
+
+
 
 
 def _draw_splitters_uncached(n, r, seed):
@@ -279,13 +304,13 @@ def _device_index(spl_nodes, dev, key):
     """Device copy of a splitter-node array; cached when `key` names a
     deterministic draw (n, p, seed)."""
     if key is None or len(spl_nodes) > _CACHE_MAX_R:
-        return torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
+        return torch.from_numpy(np.array(spl_nodes, dtype=np.int64)).to(dev)  # (a copy: the cached draw is read-only)
     key = (str(dev),) + tuple(key)
     t = _IDX_CACHE.get(key)
     if t is None:
         if len(_IDX_CACHE) > 32:
             _IDX_CACHE.clear()
-        t = torch.from_numpy(np.ascontiguousarray(spl_nodes, dtype=np.int64)).to(dev)
+        t = torch.from_numpy(np.array(spl_nodes, dtype=np.int64)).to(dev)  # (a copy: the cached draw is read-only)
         _IDX_CACHE[key] = t
     return t
 

@@ -210,3 +210,28 @@ def test_canonical_and_compare():
 def test_list_to_graph():
     gr = g.list_to_graph(g.SuccessorList([1, 2, 2]))
     assert gr.n == 3 and gr.edges.tolist() == [[0, 1], [1, 2]]
+
+
+def test_exec_stats_has_no_reference_cycle():
+    """A dropped ExecStats (and the meta arrays it holds) is freed by
+    reference counting alone -- the bench times with the cyclic GC paused,
+    and the splitter-meta pinned blocks return to their pool only when their
+    arrays die (listrank._PinnedPool)."""
+    import gc
+    import weakref
+
+    from paper_1002_4482_b200 import _device, _native
+
+    st = _native.Stats()
+    st.n_launches = 2
+    es = _device.exec_stats(st)
+    es.meta["x"] = object()
+    ref = weakref.ref(es)
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        del es
+        assert ref() is None
+    finally:
+        if was:
+            gc.enable()

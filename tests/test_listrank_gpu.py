@@ -492,3 +492,26 @@ def test_refine_variants(cuda, orc, sg_env, refine):
     assert st.meta["fallback"] is False
     _check_rank_properties(big.succ, rank)
 
+
+
+def test_splitter_meta_blocks_are_not_shared(cuda, orc):
+    """meta["splitter_set"] arrays live in pinned blocks lent per call
+    (listrank._PinnedPool): results kept from earlier calls stay intact while
+    later calls run, and a block returns to the pool once its arrays are gone."""
+    import gc
+
+    from paper_1002_4482_b200 import listrank
+
+    sls = [g.gen_list((1 << 18) + k, seed=30 + k) for k in range(3)]
+    kept = []
+    for sl in sls:
+        _, st = g.rs_rank(sl, 512, seed=4)
+        kept.append(st.meta["splitter_set"])
+    for _ in range(3):  # more calls of the same shape reuse whatever blocks are free
+        g.rs_rank(sls[0], 512, seed=4)
+    for sl, ss in zip(sls, kept):
+        assert np.array_equal(orc.seq_rank(sl.succ)[ss.splitter_node], ss.splitter_rank)
+        assert not ss.splitter_node.flags.writeable  # the cached draw is shared read-only
+    del kept, ss, st
+    gc.collect()
+    assert sum(len(v) for v in listrank._META_POOL.free.values()) >= 1
