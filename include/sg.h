@@ -191,6 +191,12 @@ int sg_rs_rank_meta(const void* succ, int succ_dtype, void* rank, int rank_dtype
                     void* meta_ws, size_t meta_ws_bytes,
                     void* stream, sg_stats* st, sg_violation* viol);
 
+/* rs_rank_even's perfect splitters (listrank.py:431-436): out[k] (int64,
+ * device) = the node at chain position k * (n / p), i.e. whose rank is
+ * n - 1 - k * (n / p), for k < p; p must divide n.  One streaming pass over
+ * the ranks (replaces the reference's position array). */
+int sg_even_splitters(const void* rank, int rank_dtype, uint64_t n, uint64_t p, int64_t* out, void* stream);
+
 /* out[i] = src[idx[i]] for i < k (int64 ranks at the official splitters;
  * listrank.py:355-356 splitter_rank is the global rank of the splitter). */
 int sg_gather_i64(const int64_t* src, const int64_t* idx, uint64_t k,

@@ -226,6 +226,19 @@ __global__ void k_gather_i64(const long long* __restrict__ src, const long long*
 
 using namespace sg;
 
+// rs_rank_even's splitters (listrank.py:431-436): the node at chain position
+// k * step for k < p, i.e. the node whose rank is n - 1 - k * step.  One
+// streaming pass over the ranks, p scattered 8-B writes.
+template <class R>
+__global__ void k_even_nodes(const R* __restrict__ rank, unsigned long long n, unsigned long long step,
+                             unsigned long long p, long long* __restrict__ out) {
+    const unsigned long long st = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+        const unsigned long long pos = (n - 1) - (unsigned long long)(long long)rank[i];
+        if (pos % step == 0 && pos / step < p) out[pos / step] = (long long)i;
+    }
+}
+
 extern "C" {
 
 int sg_kiss_device(const uint64_t* states, uint64_t chunks, uint64_t chunk_len, uint64_t n, uint64_t* out,
@@ -307,6 +320,22 @@ int sg_splitter_meta(const void* rank, int rank_dtype, uint64_t n, const int64_t
     if (block) return launch_spl_block(k0, r, n, bits, out, s);
     SG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, k0, k1, v0, v1, (int)r, 0, bits, s));
     k_spl_meta<<<g, 256, 0, s>>>(k1, v1, r, n, (long long*)out);
+    SG_LAUNCH_CHECK();
+    return SG_OK;
+}
+
+int sg_even_splitters(const void* rank, int rank_dtype, uint64_t n, uint64_t p, int64_t* out, void* stream) {
+    if (p == 0) return SG_OK;
+    if (n == 0 || n % p != 0) return SG_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t g = grid_for(n, 256, 4, sm_count() * 8);
+    const unsigned long long step = n / p;
+    switch (rank_dtype) {
+        case SG_U32: k_even_nodes<uint32_t><<<g, 256, 0, s>>>((const uint32_t*)rank, n, step, p, (long long*)out); break;
+        case SG_I32: k_even_nodes<int32_t><<<g, 256, 0, s>>>((const int32_t*)rank, n, step, p, (long long*)out); break;
+        case SG_I64: k_even_nodes<int64_t><<<g, 256, 0, s>>>((const int64_t*)rank, n, step, p, (long long*)out); break;
+        default: return SG_ERR_VALUE;
+    }
     SG_LAUNCH_CHECK();
     return SG_OK;
 }

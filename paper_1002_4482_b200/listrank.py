@@ -362,9 +362,12 @@ def _rs(sl, p, packing, seed, backend, accounting, block_size, workers, reuse_su
     if even:
         # perfect splitters every n/p chain positions (listrank.py:431-436):
         # node at chain position k has rank n-1-k
-        node_at = torch.empty(n, dtype=torch.int64, device=rank.device)
-        node_at[(n - 1) - rank.to(torch.int64)] = torch.arange(n, dtype=torch.int64, device=rank.device)
-        spl_nodes = node_at[:: n // p].cpu().numpy()
+        # (one streaming pass on the device, sg_even_splitters: p writes instead of an n-long position array)
+        dnodes = torch.empty(p, dtype=torch.int64, device=rank.device)
+        _native.check(_native.lib().sg_even_splitters(_device.ptr(rank), _device.dtype_code(rank), n, p,
+                                                      _device.ptr(dnodes), _device.stream_ptr(rank.device)),
+                      "sg_even_splitters")
+        spl_nodes = dnodes.cpu().numpy()
         splitters = _splitter_set(rank, spl_nodes, n)
     elif meta is not None and meta[2]:
         host = meta[2][0]

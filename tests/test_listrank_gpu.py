@@ -515,3 +515,21 @@ def test_splitter_meta_blocks_are_not_shared(cuda, orc):
     del kept, ss, st
     gc.collect()
     assert sum(len(v) for v in listrank._META_POOL.free.values()) >= 1
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64])
+def test_rs_rank_even_splitters_device(cuda, orc, dtype):
+    """rs_rank_even's perfect splitters (listrank.py:431-436) come from one
+    device pass over the ranks (sg_even_splitters): the node at chain
+    position k * n/p, for p = 1, a middle p and p = n."""
+    n = 3 * (1 << 16)
+    sl = g.gen_list(n, seed=8)
+    want_rank = orc.seq_rank(sl.succ)
+    node_at = np.empty(n, dtype=np.int64)
+    node_at[(n - 1) - want_rank] = np.arange(n)
+    d = g.SuccessorList(torch.from_numpy(sl.succ).to(cuda).to(dtype))
+    for p in (1, 3 * 256, n):
+        rank, st = g.rs_rank_even(d, p)
+        ss = st.meta["splitter_set"]
+        assert np.array_equal(ss.splitter_node, node_at[:: n // p]), p
+        assert np.array_equal(ss.splitter_rank, want_rank[ss.splitter_node])
