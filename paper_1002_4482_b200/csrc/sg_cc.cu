@@ -457,12 +457,16 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
 // Every edge is read once and written once, with no count pass and no
 // shared-memory sort.  Each CTA keeps, per window, a reservation counter in
 // shared memory over its own stream of chunks (CC_CHUNK rows, 8 KiB each).
-// Per 32 edges a warp ranks its lanes by window with NB + 1 ballots; lane w
-// reserves window w's rows with one shared atomic and claims the chunk(s)
-// its range starts (a global bump allocator hands out the chunk, whose id
-// lands in the window's directory and the CTA's chunk list); every lane then
-// stores its edge straight into the chunk -- a warp's stores are at most P
-// contiguous runs.  No barriers inside the loop: warps stream independently.
+// Per 32 edges a warp groups its lanes by window (one match.any, kMatch, the
+// default; or NB + 1 ballots) and each group's leader reserves the group's
+// rows with one shared atomic.  Chunk k + 1 of a window is claimed from a
+// global bump allocator when chunk k starts filling (its id published in a
+// shared-memory ring and in the CTA's chunk list), so a writer never waits on
+// a claim's atomic; chunk k joins the window's directory when its first row
+// is reserved.  Every lane then stores its edge straight into its chunk -- a
+// warp's stores are at most P contiguous runs.  No barriers inside the loop:
+// warps stream independently.  The identity forest D[i] = i (cc_init) is
+// written by the same launch.
 // At the end each CTA pads its open chunks with (0, 0) rows, which the hook
 // skips (equal parents), so a window is a whole number of chunks and the
 // hook walks its directory as one virtual contiguous range (EdgesChunked).
