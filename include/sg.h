@@ -259,6 +259,26 @@ int sg_cc_compress(uint32_t* D, uint64_t lo, uint64_t hi, uint64_t* roots,
 int sg_cc_labels(const uint32_t* D, uint64_t n, void* out, int out_dtype,
                  void* stream);
 
+/* ---- connected components over G GPUs, one host thread ------------------
+ * Replaces the reference's sv_components over the edge-sharded layout
+ * (SURVEY §8(b) sg_cc_multi; rounds as concomp.py:225-240): device g hooks
+ * its shard edges[g] (m_shard[g] rows; global row = the shards before it +
+ * the local row, for InvalidGraphError) into its replica of D, the replicas
+ * merge with an NCCL min all-reduce per round until no device changed
+ * anything, then a sharded shortcut + all-gather; labels[g] (n entries,
+ * label_dtype) receive the component-minimum labels on every device.
+ * comms[g]: one NCCL clique (e.g. sg_nccl_comms_init), streams[g] on
+ * devs[g], ws[g]: sg_cc_multi_workspace_bytes(n, m_shard[g], G) bytes on
+ * devs[g].  NCCL is the process's own libnccl.so.2, resolved at run time. */
+size_t sg_cc_multi_workspace_bytes(uint64_t n, uint64_t m_shard, int G);
+int sg_cc_multi(int G, const int* devs, const void* const* edges, int edge_dtype, const uint64_t* m_shard,
+                uint64_t n, void* const* labels, int label_dtype, int variant, int round_bound,
+                void* const* ws, const size_t* ws_bytes, void* const* comms, void* const* streams,
+                sg_stats* st, sg_violation* viol);
+/* ncclCommInitAll / ncclCommDestroy of the process's NCCL (comms: G opaque handles) */
+int sg_nccl_comms_init(int G, const int* devs, void** comms);
+int sg_nccl_comms_destroy(int G, void** comms);
+
 /* ---- input generation (gen.py) ----------------------------------------- */
 
 /* KISS64 draws on the host (gen.py:30-64); state[4] = {x,y,z,c} in/out. */

@@ -35,7 +35,8 @@ SG_MAX_LEVELS = 8
 EXPORTS = (
     "sg_strerror", "sg_kernel_name", "sg_version", "sg_tuning_reload", "sg_source_hash", "sg_last_cuda_error", "sg_stats_resolve",
     "sg_wyllie_workspace_bytes", "sg_rs_workspace_bytes", "sg_wyllie_rank", "sg_rs_rank",
-    "sg_gather_i64", "sg_even_splitters", "sg_cc_workspace_bytes", "sg_cc", "sg_cc_init", "sg_cc_hook",
+    "sg_gather_i64", "sg_even_splitters", "sg_cc_multi_workspace_bytes", "sg_cc_multi", "sg_nccl_comms_init",
+    "sg_nccl_comms_destroy", "sg_cc_workspace_bytes", "sg_cc", "sg_cc_init", "sg_cc_hook",
     "sg_cc_hook_workspace_bytes", "sg_cc_hook_part", "sg_splitter_meta_workspace_bytes", "sg_splitter_meta",
     "sg_rs_rank_meta", "sg_cc_changes", "sg_cc_apply_min",
     "sg_cc_compress", "sg_cc_labels", "sg_kiss_batch_host", "sg_kiss_device",
@@ -89,6 +90,10 @@ _SIGS = {
                         ctypes.POINTER(Violation)]),
     "sg_gather_i64": (_I, [_P, _P, _U64, _P, _P]),
     "sg_even_splitters": (_I, [_P, _I, _U64, _U64, _P, _P]),
+    "sg_cc_multi_workspace_bytes": (_SZ, [_U64, _U64, _I]),
+    "sg_cc_multi": (_I, [_I, _P, _P, _I, _P, _U64, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "sg_nccl_comms_init": (_I, [_I, _P, _P]),
+    "sg_nccl_comms_destroy": (_I, [_I, _P]),
     "sg_splitter_meta_workspace_bytes": (_SZ, [ctypes.c_uint32]),
     "sg_splitter_meta": (_I, [_P, _I, _U64, _P, ctypes.c_uint32, _P, _P, _SZ, _P]),
     "sg_rs_rank_meta": (_I, [_P, _I, _P, _I, _U64, _U64, _P, _SZ, _P, ctypes.c_uint32, _P, _P, _P, _SZ, _P,

@@ -18,7 +18,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsg.so")
 
-SOURCES = ["sg_runtime.cu", "sg_list.cu", "sg_cc.cu", "sg_gen.cu", "sg_host.cpp", "sg_xfer.cu"]
+SOURCES = ["sg_runtime.cu", "sg_list.cu", "sg_cc.cu", "sg_gen.cu", "sg_host.cpp", "sg_xfer.cu", "sg_multi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -286,3 +286,86 @@ def sv_components_dist(graph, p, group=None, variant="uf", backend="simulated", 
     if isinstance(graph.edges, torch.Tensor) and graph.edges.is_cuda:
         return labels, stats
     return labels.cpu().numpy(), stats
+
+
+# ---------------------------------------------------------------------------
+# one process, G GPUs: the C ABI's sg_cc_multi
+
+_COMMS = {}
+
+
+def _nccl_comms(devs):
+    """One NCCL clique per device tuple (ncclCommInitAll through libsg),
+    created on first use and kept for the process."""
+    key = tuple(devs)
+    c = _COMMS.get(key)
+    if c is None:
+        G = len(devs)
+        c = (ctypes.c_void_p * G)()
+        d = (ctypes.c_int * G)(*devs)
+        _native.check(_native.lib().sg_nccl_comms_init(G, d, c), "sg_nccl_comms_init")
+        _COMMS[key] = c
+    return c
+
+
+def sv_components_multi(graph, p, devices=None, variant="uf", backend="simulated", accounting="full",
+                        block_size=256, seed=0, workers=None):
+    """Edge-sharded ``sv_components`` over several GPUs driven by this one
+    process (``sg_cc_multi``: per-device hook sweeps, NCCL min all-reduce per
+    round, sharded shortcut + all-gather; concomp.py:225-240).  `devices`:
+    CUDA device indices (default: all).  Returns the labels like
+    ``sv_components`` (numpy int64 for a host graph, a tensor on the first
+    device for a device graph) and ExecStats."""
+    if graph.n <= 0:
+        raise InvalidGraphError("graph needs at least one vertex")
+    n, m = graph.n, graph.m
+    if int(p) > n:
+        raise ValueError(f"more threads ({p}) than vertices ({n})")
+    if variant not in ("uf", "sv"):
+        raise ValueError(f"unknown variant {variant!r}")
+    devs = list(range(torch.cuda.device_count())) if devices is None else [int(d) for d in devices]
+    if not devs:
+        raise RuntimeError("sv_components_multi needs at least one CUDA device")
+    G = len(devs)
+    L = _native.lib()
+    per = -(-m // G)
+    shards, ws, labels, streams = [], [], [], []
+    for g, d in enumerate(devs):
+        dev = torch.device("cuda", d)
+        r0, r1 = min(g * per, m), min((g + 1) * per, m)
+        blk = graph.edges[r0:r1]
+        if isinstance(blk, torch.Tensor) and blk.is_cuda and blk.device != dev:
+            blk = blk.to(dev)
+        e, _ = _device.to_device(blk if blk.shape[0] else np.empty((0, 2), np.int64), dev, bound=n)
+        shards.append(e)
+        ws.append(_device.workspace(L.sg_cc_multi_workspace_bytes(n, r1 - r0, G), dev))
+        labels.append(torch.empty(n, dtype=torch.int64, device=dev))
+        streams.append(_device.stream_ptr(dev))
+    dt = _device.dtype_code(shards[0])
+    if any(_device.dtype_code(e) != dt for e in shards):  # one shard fell back to int64: use int64 everywhere
+        shards = [e.to(torch.int64) for e in shards]
+        dt = _device.dtype_code(shards[0])
+    arr = lambda ty, xs: (ty * G)(*xs)  # noqa: E731
+    st = _native.Stats()
+    viol = _native.Violation()
+    rc = L.sg_cc_multi(G, arr(ctypes.c_int, devs), arr(ctypes.c_void_p, [_device.ptr(e) for e in shards]), dt,
+                       arr(ctypes.c_uint64, [e.shape[0] for e in shards]), n,
+                       arr(ctypes.c_void_p, [_device.ptr(t) for t in labels]), _native.SG_I64,
+                       _native.SG_CC_UF if variant == "uf" else _native.SG_CC_SV, sv_round_bound(n),
+                       arr(ctypes.c_void_p, [_device.ptr(w) for w in ws]), arr(ctypes.c_size_t, [w.numel() for w in ws]),
+                       _nccl_comms(devs), arr(ctypes.c_void_p, streams), ctypes.byref(st), ctypes.byref(viol))
+    if rc == _native.SG_ERR_INVALID_GRAPH:
+        raise InvalidGraphError(_graph_error_message(viol.kind, int(viol.index)))
+    if rc == _native.SG_ERR_RUNTIME:
+        raise RuntimeError(f"no convergence within {sv_round_bound(n)} rounds")
+    _native.check(rc, "sg_cc_multi")
+    stats = ExecStats(backend="sm_100a")
+    stats.rounds = int(st.rounds)
+    roots = [int(st.roots_per_round[k]) for k in range(st.n_roots)]
+    stats.meta.update(n=n, p=int(p), m_stored=m, oriented_m=2 * m, rounds=int(st.rounds), round_bound=sv_round_bound(n),
+                      roots_per_round=roots, variant=variant, edge_sweeps=int(st.edge_sweeps),
+                      vertex_sweeps=int(st.vertex_sweeps), world=G, devices=devs, backend=backend,
+                      accounting=accounting, block_size=block_size, seed=seed, workers=workers)
+    if isinstance(graph.edges, torch.Tensor) and graph.edges.is_cuda:
+        return labels[0], stats
+    return labels[0].cpu().numpy(), stats
