@@ -2,7 +2,7 @@
 # compute-sanitizer over libsg's kernels (memcheck, racecheck, synccheck,
 # initcheck) at small sizes; summaries land in gpurun_out/$TAG/san_*.txt.
 # Only kernels in namespace sg are checked (torch's own launches excluded).
-TAG=${TAG:-r02san}
+TAG=${TAG:-r02san2}
 O=gpurun_out/$TAG
 mkdir -p $O
 CS=/usr/local/cuda/bin/compute-sanitizer

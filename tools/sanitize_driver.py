@@ -3,9 +3,11 @@ kernel family once, at sizes the sanitizers finish in minutes.
 
     list ranking: rs_rank on random (ruling-set walk + binned records,
       refine, scatter, levels >= 1, cooperative top) and ordered lists
-      (tile contraction), wyllie_rank both variants;
+      (tile contraction), rs_rank_even (even splitters), wyllie_rank both
+      variants;
     components: uf and sv, with and without the window partition
-      (SG_CC_WBITS=12 forces several windows at small n).
+      (SG_CC_WBITS=12 forces several windows at small n), and the
+      one-process multi-GPU entry (sg_cc_multi) on a one-device clique.
 """
 import os
 import sys
@@ -33,6 +35,8 @@ def main():
         o = g.SuccessorList(torch.cat([torch.arange(1, n, device=dev), torch.tensor([n - 1], device=dev)]).to(torch.int32))
         r, st = g.rs_rank(o, 1024)
         print("rs ordered", st.meta["path"], int(r[0]))
+        r, st = g.rs_rank_even(sl, 1024)  # sg_even_splitters
+        print("rs even", st.meta["path"], len(st.meta["splitter_set"].splitter_node))
         r, _ = g.wyllie_rank(g.SuccessorList(torch.from_numpy(g.gen_list(1 << 14, seed=2).succ).to(dev)), 64)
         r, _ = g.wyllie_rank(g.SuccessorList(torch.from_numpy(g.gen_list(200, seed=3).succ).to(dev)), 128,
                              variant="single_block")
@@ -43,6 +47,9 @@ def main():
         for variant in ("uf", "sv"):
             lab, st = g.sv_components(gr, 64, variant=variant)
             print("cc", variant, st.meta["rounds"], int(lab.max()))
+        from paper_1002_4482_b200 import dist as sgdist
+        lab, st = sgdist.sv_components_multi(gr, 64, devices=[0])  # sg_cc_multi (NCCL clique of one)
+        print("cc multi", st.meta["rounds"], int(lab.max()))
     torch.cuda.synchronize()
 
 
