@@ -220,9 +220,13 @@ def test_partitioned_path_small_windows(cuda, orc, sg_env, variant, part):
     rng = np.random.default_rng(5)
     hi = rng.integers(65_600, n, size=(200_000, 2), dtype=np.int64)  # every edge in the top window
     hi = hi[hi[:, 0] != hi[:, 1]]
+    lowonly = rng.integers(0, 10_000, size=(70_000, 2), dtype=np.int64)  # windows >= 3 of 16 stay empty
+    lowonly = lowonly[lowonly[:, 0] != lowonly[:, 1]]
+    exact = g.list_to_graph(g.gen_list((1 << 16) + 1, seed=6))  # exactly 2^16 rows: the split threshold
     cases = [g.gen_random_graph(60_000, 5e-5, seed=4), g.gen_tree_graph(70_000, 3, seed=2),
              g.list_to_graph(g.gen_list(66_000, seed=1)), g.gen_random_graph(30_000, 2e-4, seed=9),
-             g.EdgeGraph(n, star), g.EdgeGraph(n, hi), g.gen_random_graph(300_000, 2e-6, seed=3)]
+             g.EdgeGraph(n, star), g.EdgeGraph(n, hi), g.gen_random_graph(300_000, 2e-6, seed=3),
+             g.EdgeGraph(60_000, lowonly), exact]
     for gr in cases:
         labels, stats = g.sv_components(gr, p=64, variant=variant)
         assert np.array_equal(labels, orc.seq_components(gr.n, gr.edges)), (gr.n, gr.m)
