@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
     const unsigned long long N = st->R[0];
     const unsigned long long ntiles = (N + TILE - 1) / TILE;
     const uint32_t lane = lane_id();
+    const uint32_t rT = 1u << (32u - kbits);  // ruler iff (i * PHI + salt) < rT, or i == 0 (is_ruler)
     const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     for (unsigned long long tile = gw; tile < ntiles; tile += nw) {
@@ -330,9 +331,12 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
                     }
             }
 #pragma unroll
-            for (int j = 0; j < SUB; ++j)
+            for (int j = 0; j < SUB; ++j) {
+                // ruler hash along the lane's VEC consecutive ids: h advances by PHI per id
+                // (is_ruler's (h >> (32 - kbits)) == 0 is h < 2^(32 - kbits); node 0 is added below)
+                uint32_t h = ((uint32_t)base + s0 + (uint32_t)(j * 32 + lane) * VEC) * PHI + salt;
 #pragma unroll
-                for (int c = 0; c < VEC; ++c) {
+                for (int c = 0; c < VEC; ++c, h += PHI) {
                     const uint32_t l = s0 + (j * 32 + lane) * VEC + c;
                     if (full || base + l < N) {
                         const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
@@ -340,11 +344,12 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
                         const bool oor = kNarrow ? x >= (uint32_t)N : x64 >= N;
                         const bool self = !oor && x == i;
                         if (oor | self) note_succ(st, i, x64, N);
-                        packed += (is_ruler(i, kbits, salt) ? 0x10000u : 0u) +
-                                  ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
+                        packed += (h < rT ? 0x10000u : 0u) + ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
                     }
                 }
+            }
         }
+        if (tile == 0 && lane == 0 && !(salt < rT)) packed += 0x10000u;  // node 0 is always a ruler
         const uint32_t tot = __reduce_add_sync(0xffffffffu, packed);
         if (lane == 0) {
             tile_cnt[tile] = tot >> 16;
@@ -495,12 +500,18 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
     for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const unsigned long long base = tile * TILE;
         const unsigned long long i0 = base + (unsigned long long)threadIdx.x * TILE_ITEMS;
+        // ruler test along the run: h = i * PHI + salt advances by PHI per id,
+        // and (h >> (32 - kbits)) == 0 is h < 2^(32 - kbits) (is_ruler)
         uint32_t flags = 0;
+        const uint32_t T = 1u << (32u - kbits);
+        uint32_t h = (uint32_t)i0 * PHI + salt;
 #pragma unroll
         for (int j = 0; j < TILE_ITEMS; ++j) {
-            const unsigned long long i = i0 + j;
-            if (i < N && is_ruler((uint32_t)i, kbits, salt)) flags |= 1u << j;
+            flags |= (h < T ? 1u : 0u) << j;
+            h += PHI;
         }
+        if (i0 == 0) flags |= 1u;  // node 0 is always a ruler
+        if (i0 + TILE_ITEMS > N) flags &= i0 >= N ? 0u : (1u << (uint32_t)(N - i0)) - 1u;
         uint32_t pre;
         BS(tmp).ExclusiveSum((uint32_t)__popc(flags), pre);
         unsigned long long id = (unsigned long long)tile_off[tile] + pre;

@@ -1,5 +1,5 @@
 #!/bin/bash
-TAG=${TAG:-r02al}
+TAG=${TAG:-r02an}
 O=gpurun_out/$TAG
 mkdir -p $O
 python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
