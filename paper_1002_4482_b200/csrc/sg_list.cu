@@ -531,6 +531,54 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_select(const uint32_t* __re
     }
 }
 
+// Level-0 ruler ids, one warp per 4096-node tile (no block barrier): lane l
+// owns ids [l*128, (l+1)*128) of the tile as four 32-id groups, hashes them
+// along the run, and a warp scan of the lanes' ruler counts gives every
+// group its first id -> rgrp {mask, first id} (a warp writes 1 KiB
+// contiguously) and spl[id] = node for the rulers.
+__global__ void __launch_bounds__(256) k_rs_select0(const uint32_t* __restrict__ tile_off, uint32_t* __restrict__ spl,
+                                                    const ListStatus* st, uint32_t kbits, uint32_t salt,
+                                                    unsigned long long cap, uint2* __restrict__ rgrp) {
+    if (layout_local(st)) return;  // k_rs_contract takes this list
+    static_assert(TILE == 32 * 128, "a lane owns 128 ids of a tile");
+    const unsigned long long N = st->R[0];
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
+    const uint32_t lane = lane_id();
+    const uint32_t T = 1u << (32u - kbits);
+    const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    for (unsigned long long tile = gw; tile < ntiles; tile += nw) {
+        const unsigned long long i0 = tile * TILE + (unsigned long long)lane * 128;
+        uint32_t m[4], cnt = 0;
+        uint32_t h = (uint32_t)i0 * PHI + salt;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            uint32_t f = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j, h += PHI) f |= (h < T ? 1u : 0u) << j;
+            const unsigned long long gb = i0 + (unsigned long long)g * 32;
+            if (gb == 0) f |= 1u;  // node 0 is always a ruler
+            if (gb + 32 > N) f &= gb >= N ? 0u : (1u << (uint32_t)(N - gb)) - 1u;
+            m[g] = f;
+            cnt += __popc(f);
+        }
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += y;
+        }
+        unsigned long long id = (unsigned long long)tile_off[tile] + (incl - cnt);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const unsigned long long gb = i0 + (unsigned long long)g * 32;
+            if (gb < N) rgrp[gb >> 5] = make_uint2(m[g], (uint32_t)id);
+            for (uint32_t rem = m[g]; rem != 0; rem &= rem - 1, ++id)
+                if (id < cap) spl[id] = (uint32_t)(gb + (__ffs(rem) - 1));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // sublist walk (RS3 at level 0, weighted RS4 walk above)
 //
@@ -2394,8 +2442,14 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.end();
         SG_LAUNCH_CHECK();
         rec.begin(k == 0 ? K_RS_SELECT : K_RS4_SELECT, k, nt, TILE_THREADS, capN);
-        k_rs_select<false><<<nt < sm_count() * 8 ? nt : sm_count() * 8, TILE_THREADS, 0, s>>>(tk, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR,
-                                                        k == 0 ? b.rgrp : nullptr);
+        if (k == 0) {  // warp per tile, no block barrier
+            const unsigned long long ctas = (nt + 7) / 8;
+            const uint32_t g0 = (uint32_t)(ctas < (unsigned long long)sm_count() * 8 ? ctas : sm_count() * 8);
+            k_rs_select0<<<g0 ? g0 : 1, 256, 0, s>>>(tk, b.spl[0], b.st, p.kbits[0], p.salt[0], capR, b.rgrp);
+        } else {
+            k_rs_select<false><<<nt < sm_count() * 8 ? nt : sm_count() * 8, TILE_THREADS, 0, s>>>(
+                tk, b.spl[k], wk, b.st, k, p.kbits[k], p.salt[k], capR, nullptr);
+        }
         rec.end();
         SG_LAUNCH_CHECK();
         if (k == 0) {

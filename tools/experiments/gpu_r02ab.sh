@@ -1,5 +1,5 @@
 #!/bin/bash
-TAG=${TAG:-r02an}
+TAG=${TAG:-r02ao}
 O=gpurun_out/$TAG
 mkdir -p $O
 python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
