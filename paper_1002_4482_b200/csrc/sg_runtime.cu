@@ -179,13 +179,16 @@ static Tuning read_tuning(uint32_t generation) {
     Tuning v;
     v.rs_win_kb = env_u32("SG_RS_WIN_KB", 64, 8, 128);  // fine window: KiB of shared memory in rs5_scatter
     v.rs_kb0 = env_u32("SG_RS_KBITS0", 5, 1, 16);        // level-0 ruler density 2^-kb0
-    v.rs_kb1 = env_u32("SG_RS_KBITS", 3, 1, 16);         // upper levels: short chains (latency-bound tail)
+    v.rs_kb1 = env_u32("SG_RS_KBITS", 4, 1, 16);         // upper levels: short chains (latency-bound tail)
     v.rs_fin = env_u32("SG_RS_FINAL", 8192, 64, 1u << 20);
     v.rs_walk_cap = env_u32("SG_RS_WALK_CAP", 1u << 16, 1, 0x7FFFFFFF);  // longer walks -> Wyllie fallback
     v.rs_load_mode = env_u32("SG_WALK_LOAD", 0, 0, 3);
     v.rs_contract = env_u32("SG_RS_CONTRACT", 1, 0, 1);
     v.rs_coop = env_u32("SG_RS_COOP", 1, 0, 1);
-    v.rs_topn = env_u32("SG_RS_TOPN", 1u << 19, 0, 1u << 30);
+    // kbits 4 + pointer jumping from 2^20 rulers: at 2^28 the level-1 walk
+    // feeds the top directly (levels 2^28 / 2^23 / 2^19): 9.55 -> 9.51 ms,
+    // ordered 1.445 -> 1.414 ms; 2^26 within noise (+0.01 ms)
+    v.rs_topn = env_u32("SG_RS_TOPN", 1u << 20, 0, 1u << 30);
     v.rs_packed = env_u32("SG_RS_PACKED", 1, 0, 1);
     v.rs_fused = env_u32("SG_RS_FUSED", 1, 0, 1);
     v.rs_refine = env_u32("SG_RS_REFINE", 0, 0, 6);  // rs5_refine variant (sg_list.cu)

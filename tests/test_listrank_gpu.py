@@ -435,11 +435,13 @@ def test_record_paths_invalid_lists(cuda, sg_env, fused):
 def test_top_level_ranking_paths(cuda, orc, sg_env, topn, coop):
     """The ruler list above level 0 is finished either by more walked levels
     and the one-CTA final (SG_RS_TOPN=0), or by multi-CTA in-place pointer
-    jumping once it has at most SG_RS_TOPN rulers (default 2^19): one
+    jumping once it has at most SG_RS_TOPN rulers (default 2^20): one
     cooperative launch with grid barriers (default) or one launch per round
     (SG_RS_COOP=0)."""
     sg_env(SG_RS_TOPN=topn)
     sg_env(SG_RS_COOP=coop)
+    if topn == "0":
+        sg_env(SG_RS_KBITS="3")  # chains of 8 above level 0: two walked levels end at <= 8192 rulers
     sl = g.gen_list(2_500_003, seed=11)
     rank, st = g.rs_rank(sl, 128, seed=1)
     assert np.array_equal(rank, orc.seq_rank(sl.succ))
@@ -461,7 +463,7 @@ def test_top_level_ranking_paths(cuda, orc, sg_env, topn, coop):
 @pytest.mark.parametrize("n", [8_193, 65_537, 1_048_575, 2_097_153, (1 << 23) + 1])
 def test_plan_boundaries(cuda, orc, n):
     """Sizes around the plan's switch points: the one-CTA final (8192), the
-    pointer-jumping top (2^19 rulers), and the coarse-window count (256
+    pointer-jumping top (2^20 rulers), and the coarse-window count (256
     windows of 2^15 int32 ranks at 2^23: one more node doubles the window)."""
     sl = g.gen_list(n, seed=n % 1009)
     want = orc.seq_rank(sl.succ)
