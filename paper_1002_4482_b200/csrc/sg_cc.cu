@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
 constexpr int CC_CHUNK_BITS = 10;
 constexpr uint32_t CC_CHUNK = 1u << CC_CHUNK_BITS;
 constexpr int PD_THREADS = 256;
-constexpr int PD_CTAS_PER_SM = 6;
+constexpr int PD_CTAS_PER_SM = 5;
 constexpr uint32_t PD_RING = 16;  // chunk ids of the last PD_RING chunks per window, in shared memory
 // 64-row groups per warp iteration: 4 rows per lane in flight (8 rows with 4
 // CTAs per SM measured slower: 1.60 vs 1.09 ms at C5)
@@ -498,7 +498,7 @@ struct EdgesChunked {
     }
 };
 
-template <class E, int NB, bool kNarrow, bool kMatch>
+template <class E, int NB, bool kNarrow, bool kMatch, bool kV16 = false>
 __global__ void __launch_bounds__(PD_THREADS, PD_CTAS_PER_SM) k_cc_part_chunks(
     E edges, unsigned long long m, unsigned long long n, unsigned long long row0, uint32_t shift, int P,
     uint2* __restrict__ out, uint32_t* __restrict__ dir, unsigned long long dir_stride,
@@ -608,20 +608,43 @@ __global__ void __launch_bounds__(PD_THREADS, PD_CTAS_PER_SM) k_cc_part_chunks(
                    make_uint2((uint32_t)u, (uint32_t)v));
         }
     };
-    // warps take 64-row groups grid-stride, PD_GROUPS groups (2 * PD_GROUPS rows per lane) in flight
-    constexpr int RL = 2 * PD_GROUPS;
+    // warps take 64-row groups grid-stride, G groups (2 G rows per lane) in flight.
+    // kV16 (8-B rows, 16-B aligned): a lane loads rows 2l, 2l + 1 of a group
+    // with one 16-B load, so four groups (eight rows, 64 B per lane) are in
+    // flight for the registers the 8-B path spends on two
+    constexpr int G = kV16 ? 4 : PD_GROUPS;
+    constexpr int RL = 2 * G;
     const unsigned long long nw = (unsigned long long)gridDim.x * (PD_THREADS / 32);
     const unsigned long long ng = (m + 63) / 64;
     for (unsigned long long g = (unsigned long long)blockIdx.x * (PD_THREADS / 32) + (threadIdx.x >> 5); g < ng;
-         g += PD_GROUPS * nw) {
+         g += G * nw) {
         unsigned long long ee[RL], uu[RL], vv[RL];
         bool ok[RL], any_bad = false;
+        if (kV16) {
 #pragma unroll
-        for (int j = 0; j < RL; ++j) {
-            ee[j] = (g + (j >> 1) * nw) * 64 + (j & 1) * 32 + lane;
-            uu[j] = n;
-            vv[j] = n;
-            if (ee[j] < m) edges.load(ee[j], uu[j], vv[j]);
+            for (int k = 0; k < G; ++k) {
+                const unsigned long long r = (g + k * nw) * 64 + 2 * lane;
+                ee[2 * k] = r;
+                ee[2 * k + 1] = r + 1;
+                uu[2 * k] = vv[2 * k] = uu[2 * k + 1] = vv[2 * k + 1] = n;
+                if (r + 1 < m) {
+                    const uint4 x = __ldcs(reinterpret_cast<const uint4*>(edges.e) + (r >> 1));
+                    uu[2 * k] = x.x;
+                    vv[2 * k] = x.y;
+                    uu[2 * k + 1] = x.z;
+                    vv[2 * k + 1] = x.w;
+                } else if (r < m) {
+                    edges.load(r, uu[2 * k], vv[2 * k]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < RL; ++j) {
+                ee[j] = (g + (j >> 1) * nw) * 64 + (j & 1) * 32 + lane;
+                uu[j] = n;
+                vv[j] = n;
+                if (ee[j] < m) edges.load(ee[j], uu[j], vv[j]);
+            }
         }
 #pragma unroll
         for (int j = 0; j < RL; ++j) {
@@ -826,8 +849,10 @@ static int partition_edges(E view, unsigned long long m, unsigned long long n, c
                             uint32_t*, unsigned long long, uint32_t*, uint32_t*, uint32_t, unsigned long long*,
                             uint32_t*, unsigned long long);
         KT kt;
+        const bool v16 = E::kBytes == 8 && narrow && ((uintptr_t)view.e & 15) == 0;
         if (!tuning().cc_rank_ballot)  // match.any peers (default)
-            kt = narrow ? k_cc_part_chunks<E, 4, true, true> : k_cc_part_chunks<E, 4, false, true>;
+            kt = v16 ? k_cc_part_chunks<E, 4, true, true, (E::kBytes == 8)>
+                     : (narrow ? k_cc_part_chunks<E, 4, true, true> : k_cc_part_chunks<E, 4, false, true>);
         else
             kt = narrow ? (nbits <= 1 ? k_cc_part_chunks<E, 1, true, false>
                            : nbits == 2 ? k_cc_part_chunks<E, 2, true, false>
