@@ -35,7 +35,11 @@
 namespace sg {
 namespace {
 
-// fixed pool of host threads running one parallel-for at a time
+// fixed pool of host threads running one parallel-for at a time.  A pipelined
+// copy calls run() once per chunk (every ~0.3-0.5 ms), so workers spin on the
+// generation counter for a while before sleeping on the condition variable:
+// a condition-variable wake-up per chunk and per worker cost ~1-3 ms per
+// 2^28-id transfer.
 class Pool {
   public:
     Pool() {
@@ -45,13 +49,14 @@ class Pool {
             const int v = atoi(e);
             if (v >= 1 && v <= 256) nthreads_ = v;
         }
+        if (const char* e = getenv("SG_XFER_SPIN")) kSpin = std::max(0, atoi(e));
         for (int i = 1; i < nthreads_; ++i) workers_.emplace_back([this, i] { loop(i); });
     }
     ~Pool() {
         {
             std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            ++gen_;
+            stop_.store(true);
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
         for (auto& w : workers_) w.join();
@@ -63,31 +68,45 @@ class Pool {
         {
             std::lock_guard<std::mutex> lk(mu_);
             fn_ = &fn;
-            pending_ = nthreads_ - 1;
-            ++gen_;
+            pending_.store(nthreads_ - 1, std::memory_order_relaxed);
+            gen_.fetch_add(1, std::memory_order_release);  // spinning workers see fn_ with it
         }
         cv_.notify_all();
         fn(0, nthreads_);
-        std::unique_lock<std::mutex> lk(mu_);
-        done_cv_.wait(lk, [this] { return pending_ == 0; });
+        for (int i = 0; pending_.load(std::memory_order_acquire) != 0; ++i) {
+            if (i < kSpin) {
+                _mm_pause();
+                continue;
+            }
+            std::unique_lock<std::mutex> lk(mu_);
+            done_cv_.wait(lk, [this] { return pending_.load(std::memory_order_acquire) == 0; });
+            break;
+        }
         fn_ = nullptr;
     }
 
   private:
+    int kSpin = 1 << 16;  // pause loops before sleeping (~ms); SG_XFER_SPIN=0: sleep at once
     void loop(int id) {
         uint64_t seen = 0;
         for (;;) {
-            const std::function<void(int, int)>* fn;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (stop_) return;
-                fn = fn_;
+            uint64_t g = gen_.load(std::memory_order_acquire);
+            for (int i = 0; g == seen && i < kSpin; ++i) {
+                _mm_pause();
+                g = gen_.load(std::memory_order_acquire);
             }
-            (*fn)(id, nthreads_);
-            std::lock_guard<std::mutex> lk(mu_);
-            if (--pending_ == 0) done_cv_.notify_one();
+            if (g == seen) {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                g = gen_.load(std::memory_order_acquire);
+            }
+            seen = g;
+            if (stop_.load()) return;
+            (*fn_)(id, nthreads_);
+            if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+                std::lock_guard<std::mutex> lk(mu_);  // a waiter may be asleep on done_cv_
+                done_cv_.notify_one();
+            }
         }
     }
     int nthreads_ = 1;
@@ -95,9 +114,9 @@ class Pool {
     std::mutex mu_, call_mu_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(int, int)>* fn_ = nullptr;
-    uint64_t gen_ = 0;
-    int pending_ = 0;
-    bool stop_ = false;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> pending_{0};
+    std::atomic<bool> stop_{false};
 };
 
 Pool& pool() {
