@@ -125,7 +125,20 @@ Pool& pool() {
 }
 
 constexpr int kSlots = 4;
-constexpr size_t kChunk = size_t(4) << 20;  // elements per chunk (16 MiB of u32, 32 MiB of int64)
+// ids per pipelined chunk: the first chunk's conversion and the last chunk's
+// copy are not overlapped, so smaller chunks shorten the ends of the pipe
+// (SG_XFER_CHUNK_MI: Mi ids per chunk, 1..16, read once at first use)
+size_t chunk_ids() {
+    static const size_t v = [] {
+        size_t x = size_t(4) << 20;
+        if (const char* e = getenv("SG_XFER_CHUNK_MI")) {
+            const int m = atoi(e);
+            if (m >= 1 && m <= 16) x = size_t(m) << 20;
+        }
+        return x;
+    }();
+    return v;
+}
 
 // pinned staging ring of one device (u32 slots big enough for either direction)
 struct Ring {
@@ -143,7 +156,7 @@ Ring* ring_for_current_device() {
     Ring& r = g_rings[dev];
     if (r.ok) return &r;
     for (int k = 0; k < kSlots; ++k) {
-        if (cudaHostAlloc(reinterpret_cast<void**>(&r.slot[k]), kChunk * sizeof(uint32_t), cudaHostAllocPortable) !=
+        if (cudaHostAlloc(reinterpret_cast<void**>(&r.slot[k]), chunk_ids() * sizeof(uint32_t), cudaHostAllocPortable) !=
                 cudaSuccess ||
             cudaEventCreateWithFlags(&r.ev[k], cudaEventDisableTiming) != cudaSuccess)
             return nullptr;
@@ -224,12 +237,13 @@ int sg_h2d_narrow_i64(const int64_t* host, uint64_t count, uint32_t* dev, uint64
         return SG_ERR_CUDA;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    const size_t kChunkV = chunk_ids();
     std::atomic<int> bad{0};
-    const uint64_t nchunks = (count + kChunk - 1) / kChunk;
+    const uint64_t nchunks = (count + kChunkV - 1) / kChunkV;
     for (uint64_t k = 0; k < nchunks; ++k) {
         const int sl = (int)(k % kSlots);
-        const size_t off = k * kChunk;
-        const size_t len = std::min<uint64_t>(kChunk, count - off);
+        const size_t off = k * kChunkV;
+        const size_t len = std::min<uint64_t>(kChunkV, count - off);
         SG_CUDA(cudaEventSynchronize(r->ev[sl]));  // the slot's previous DMA has finished
         uint32_t* dst = r->slot[sl];
         const int64_t* src = host + off;
@@ -260,11 +274,12 @@ int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* s
         return SG_ERR_CUDA;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    const uint64_t nchunks = (count + kChunk - 1) / kChunk;
+    const size_t kChunkV = chunk_ids();
+    const uint64_t nchunks = (count + kChunkV - 1) / kChunkV;
     auto widen_chunk = [&](uint64_t k) -> int {
         const int sl = (int)(k % kSlots);
-        const size_t off = k * kChunk;
-        const size_t len = std::min<uint64_t>(kChunk, count - off);
+        const size_t off = k * kChunkV;
+        const size_t len = std::min<uint64_t>(kChunkV, count - off);
         SG_CUDA(cudaEventSynchronize(r->ev[sl]));
         const uint32_t* src = r->slot[sl];
         int64_t* dst = host + off;
@@ -283,8 +298,8 @@ int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* s
             const int rc = widen_chunk(k - kSlots);  // frees slot sl
             if (rc != SG_OK) return rc;
         }
-        const size_t off = k * kChunk;
-        const size_t len = std::min<uint64_t>(kChunk, count - off);
+        const size_t off = k * kChunkV;
+        const size_t len = std::min<uint64_t>(kChunkV, count - off);
         SG_CUDA(cudaMemcpyAsync(r->slot[sl], dev + off, len * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         SG_CUDA(cudaEventRecord(r->ev[sl], s));
     }
