@@ -1,6 +1,6 @@
 #!/bin/bash
 # UF hook: hook a root larger endpoint straight under the other endpoint's parent
-TAG=${TAG:-r02at}
+TAG=${TAG:-r02au}
 O=gpurun_out/$TAG
 mkdir -p $O
 python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
