@@ -30,6 +30,8 @@ def _nvcc():
 
 
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3"]
+# experiments only: extra -D flags for A/B builds (part of the source hash)
+FLAGS += [f for f in os.environ.get("SG_NVCC_DEFS", "").split() if f.startswith("-D")]
 LINK = ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
 MARKER = b"SG_SOURCE_HASH="
 

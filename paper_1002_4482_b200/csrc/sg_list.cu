@@ -1291,6 +1291,9 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
     if (over) st->bad = 1;
 }
 
+#ifndef RA_THREADS_CFG
+#define RA_THREADS_CFG 256
+#endif
 // rs5_refine with shared-atomic ranking (default).  Same job and output as
 // k_rs_refine_lean: a coarse window's records -> {cur, rank} pairs split by
 // fine window (rank = IS_1[sid] - local - 1, listrank.py:375-379).
@@ -1305,12 +1308,12 @@ __global__ void __launch_bounds__(RL_THREADS, RL_CTAS_PER_SM) k_rs_refine_lean(
 //  * Tiles of 2048 records, 4 CTAs of 256 threads per SM.  (A variant that
 //    deferred each tile's write-out by one iteration behind a double-buffered
 //    sorted tile measured slower: 2.74 ms.)
-constexpr int RA_THREADS = 256;
+constexpr int RA_THREADS = RA_THREADS_CFG;
 constexpr int RA_WARPS = RA_THREADS / 32;
 constexpr int RA_IT = 8;
 constexpr int RA_TILE = RA_THREADS * RA_IT;  // 2048 records (2^cshift is a multiple)
 constexpr int RA_MAXB = 64;
-constexpr int RA_CTAS_PER_SM = 4;
+constexpr int RA_CTAS_PER_SM = 1024 / RA_THREADS;
 
 static size_t ra_smem_bytes() { return (size_t)RA_TILE * 8 * 2; }
 
@@ -1390,10 +1393,12 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
         __syncthreads();  // (1) staging consumed, every warp's counts in
         issue(tile + gridDim.x);
         // (bin, warp) counts -> absolute slots of the bin-sorted tile: a block
-        // scan in bin-major order, thread t owning bin t / 4, warps 2 (t % 4) and
-        // 2 (t % 4) + 1; one global atomic per non-empty bin claims the bin's
-        // run in its fine window (issued here, consumed after the placement)
-        const uint32_t bq = t >> 2, i0 = bq * kStride + 2 * (t & 3u);
+        // scan in bin-major order, thread t owning bin t / TPB, warps 2 (t % TPB)
+        // and 2 (t % TPB) + 1; one global atomic per non-empty bin claims the
+        // bin's run in its fine window (issued here, consumed after the placement)
+        constexpr uint32_t TPB = RA_WARPS / 2;  // threads per bin (2 counters each)
+        static_assert(RA_MAXB * TPB == RA_THREADS, "two counters per thread");
+        const uint32_t bq = t / TPB, i0 = bq * kStride + 2 * (t % TPB);
         const uint32_t a0 = s_c[i0], a1 = s_c[i0 + 1], pair = a0 + a1;
         uint32_t incl = pair;
 #pragma unroll
@@ -1402,12 +1407,12 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
             if ((int)lane >= o) incl += y;
         }
         if (lane == 31) s_tot[warp] = incl;
-        // the bin's total: the four threads of a bin are adjacent lanes
+        // the bin's total: the TPB threads of a bin are adjacent lanes
         uint32_t btot = pair;
-        btot += __shfl_xor_sync(0xffffffffu, btot, 1);
-        btot += __shfl_xor_sync(0xffffffffu, btot, 2);
+#pragma unroll
+        for (uint32_t o = 1; o < TPB; o <<= 1) btot += __shfl_xor_sync(0xffffffffu, btot, o);
         uint32_t base = 0;
-        const bool head = (t & 3u) == 0 && bq < fb;
+        const bool head = (t % TPB) == 0 && bq < fb;
         if (head && btot) base = (uint32_t)atomicAdd(cursor + (unsigned long long)c * fb + bq, (unsigned long long)btot);
         __syncthreads();  // (1b) warp totals
         uint32_t woff = lane < (uint32_t)warp ? s_tot[lane] : 0u;  // lanes < 8 hold the earlier warps' totals
@@ -2601,7 +2606,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
     const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
     bool tiled = false;
-    if (lean_ok && tu_r.rs_refine == 0 && p.cshift >= 11) {
+    if (lean_ok && tu_r.rs_refine == 0 && ((1ull << p.cshift) % RA_TILE) == 0) {
         const size_t sma = ra_smem_bytes();  // (k_rs_refine_atom: staging + one sorted tile)
         SG_CUDA(set_smem_max(k_rs_refine_atom, sma));
         const uint32_t g = sm_count() * RA_CTAS_PER_SM;
