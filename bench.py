@@ -514,7 +514,14 @@ def e2e_run(a, ctx, kind, n, m, dev_input):
             "ms_per_step": round(dt * 1e3, 3), "steps": steps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": "rs_rank(SuccessorList(pinned int64)) -> numpy int64" if kind == "list"
             else "sv_components(EdgeGraph(pinned int64)) -> numpy int64",
+            "host_threads": _xfer_threads(),
             "timing": "host perf_counter around the API calls, max over ranks"}
+
+
+def _xfer_threads():
+    """Host threads of the boundary conversions (sg_xfer_threads)."""
+    from paper_1002_4482_b200 import _native
+    return int(_native.lib().sg_xfer_threads())
 
 
 def ours(a):

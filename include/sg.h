@@ -129,6 +129,10 @@ typedef struct sg_violation {
 int sg_h2d_narrow_i64(const int64_t* host, uint64_t count, uint32_t* dev, uint64_t bound, void* stream,
                       int* in_range);
 int sg_d2h_widen_u32(const uint32_t* dev, uint64_t count, int64_t* host, void* stream);
+/* Host threads the two copies convert with (the process's usable CPUs: the
+ * affinity mask capped by a cgroup CPU quota, at most 32; SG_XFER_THREADS
+ * overrides).  Starts the pool on first use. */
+int sg_xfer_threads(void);
 
 /* ---- library ------------------------------------------------------------ */
 const char* sg_strerror(int status);

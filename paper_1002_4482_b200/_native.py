@@ -41,7 +41,7 @@ EXPORTS = (
     "sg_rs_rank_meta", "sg_cc_changes", "sg_cc_apply_min",
     "sg_cc_compress", "sg_cc_labels", "sg_kiss_batch_host", "sg_kiss_device",
     "sg_list_from_order", "sg_edge_keys", "sg_edges_from_keys", "sg_list_violation_host",
-    "sg_h2d_narrow_i64", "sg_d2h_widen_u32",
+    "sg_h2d_narrow_i64", "sg_d2h_widen_u32", "sg_xfer_threads",
 )
 
 
@@ -79,6 +79,7 @@ _SIGS = {
     "sg_h2d_narrow_i64": (_I, [ctypes.c_void_p, _U64, ctypes.c_void_p, _U64, ctypes.c_void_p,
                                ctypes.POINTER(ctypes.c_int)]),
     "sg_d2h_widen_u32": (_I, [ctypes.c_void_p, _U64, ctypes.c_void_p, ctypes.c_void_p]),
+    "sg_xfer_threads": (_I, []),
     "sg_source_hash": (ctypes.c_char_p, []),
     "sg_last_cuda_error": (ctypes.c_char_p, []),
     "sg_stats_resolve": (_I, [ctypes.POINTER(Stats)]),

@@ -21,6 +21,8 @@
 #include <string.h>
 
 #include <emmintrin.h>  // SSE2 (x86-64 baseline): 16-B non-temporal stores
+#include <sched.h>
+#include <stdio.h>
 
 #include <algorithm>
 #include <atomic>
@@ -35,6 +37,32 @@
 namespace sg {
 namespace {
 
+// host CPUs this process may actually run on: the affinity mask (what
+// hardware_concurrency ignores: it counts the machine's online CPUs), capped
+// by a cgroup CPU quota (v2 cpu.max, v1 cfs_quota_us / cfs_period_us).  More
+// spinning workers than usable CPUs would time-slice against each other.
+int usable_cpus() {
+    int n = 0;
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) n = CPU_COUNT(&set);
+    if (n <= 0) n = (int)std::max(1u, std::thread::hardware_concurrency());
+    long long quota = -1, period = 0;
+    if (FILE* f = fopen("/sys/fs/cgroup/cpu.max", "r")) {
+        char q[32] = {0};
+        if (fscanf(f, "%31s %lld", q, &period) == 2 && strcmp(q, "max") != 0) quota = atoll(q);
+        fclose(f);
+    } else if (FILE* fq = fopen("/sys/fs/cgroup/cpu/cpu.cfs_quota_us", "r")) {
+        if (fscanf(fq, "%lld", &quota) != 1) quota = -1;
+        fclose(fq);
+        if (FILE* fp = fopen("/sys/fs/cgroup/cpu/cpu.cfs_period_us", "r")) {
+            if (fscanf(fp, "%lld", &period) != 1) period = 0;
+            fclose(fp);
+        }
+    }
+    if (quota > 0 && period > 0) n = std::min<long long>(n, std::max(1LL, quota / period));
+    return n;
+}
+
 // fixed pool of host threads running one parallel-for at a time.  A pipelined
 // copy calls run() once per chunk (every ~0.3-0.5 ms), so workers spin on the
 // generation counter for a while before sleeping on the condition variable:
@@ -43,8 +71,7 @@ namespace {
 class Pool {
   public:
     Pool() {
-        unsigned hw = std::thread::hardware_concurrency();
-        nthreads_ = (int)std::max(1u, std::min(hw ? hw : 1u, 32u));
+        nthreads_ = std::max(1, std::min(usable_cpus(), 32));
         if (const char* e = getenv("SG_XFER_THREADS")) {  // experiment switch (read once, at first use)
             const int v = atoi(e);
             if (v >= 1 && v <= 256) nthreads_ = v;
@@ -223,6 +250,8 @@ inline void widen(const uint32_t* src, int64_t* dst, size_t len) {
 }  // namespace sg
 
 extern "C" {
+
+int sg_xfer_threads(void) { return sg::pool().size(); }
 
 int sg_h2d_narrow_i64(const int64_t* host, uint64_t count, uint32_t* dev, uint64_t bound, void* stream,
                       int* in_range) {
