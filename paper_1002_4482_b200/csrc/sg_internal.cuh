@@ -24,6 +24,14 @@ constexpr unsigned long long NONE64 = ~0ull;
 // SMs of the current device (148 on a B200), queried once per device; every
 // persistent grid is sized from it
 int sm_count();
+// CTAs of `kernel` resident per SM at `threads` threads (no dynamic shared
+// memory), queried once per (kernel, threads, device): grids of persistent
+// loops are sized sm_count() x this, so no CTA waits for a slot
+int resident_ctas(const void* kernel, int threads);
+template <class K>
+int resident_ctas(K* kernel, int threads) {
+    return resident_ctas(reinterpret_cast<const void*>(kernel), threads);
+}
 
 // Experiment switches (SG_* environment variables).  The defaults are the
 // measured configuration; the switches exist to re-run the comparisons

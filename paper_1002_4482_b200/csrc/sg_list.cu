@@ -310,41 +310,81 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
         const unsigned long long base = tile * TILE;
         const bool full = kVec && base + TILE <= N;
         uint32_t packed = 0;  // rulers << 16 | ends
+        // full tiles of 32-bit ids: branch-free counts, the range and
+        // self-loop checks folded into one flag per lane (half the
+        // instructions of the exact path: the census was issue-bound at 4.5
+        // TB/s); a tile that raises the flag is re-scanned below with the
+        // exact per-node report (note_succ)
+#ifdef SG_COUNT0_EXACT_ONLY
+        constexpr bool kFast = false;
+#else
+        constexpr bool kFast = kNarrow;
+#endif
+        bool exact = !(kFast && full);
+        if (kFast && full) {
+            const uint32_t Nn = (uint32_t)N, b32 = (uint32_t)base;
+            uint32_t rul = 0, ends = 0;
+            bool err = false;
 #pragma unroll 1
-        for (uint32_t s0 = 0; s0 < (uint32_t)TILE; s0 += PER) {
-            SuccT e[SUB * VEC];
-            if (full) {
+            for (uint32_t s0 = 0; s0 < (uint32_t)TILE; s0 += PER) {
+                V v[SUB];
                 const V* src = reinterpret_cast<const V*>(succ + base + s0);
 #pragma unroll
+                for (int j = 0; j < SUB; ++j) v[j] = __ldcs(src + j * 32 + lane);
+#pragma unroll
                 for (int j = 0; j < SUB; ++j) {
-                    const V v = __ldcs(src + j * 32 + lane);
+                    const uint32_t i0 = b32 + s0 + (uint32_t)(j * 32 + lane) * VEC;
+                    uint32_t h = i0 * PHI + salt;
 #pragma unroll
-                    for (int c = 0; c < VEC; ++c) e[j * VEC + c] = reinterpret_cast<const SuccT*>(&v)[c];
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < SUB; ++j)
-#pragma unroll
-                    for (int c = 0; c < VEC; ++c) {
-                        const unsigned long long i = base + s0 + (unsigned long long)(j * 32 + lane) * VEC + c;
-                        e[j * VEC + c] = i < N ? __ldcs(succ + i) : SuccT(0);
+                    for (int c = 0; c < VEC; ++c, h += PHI) {
+                        const uint32_t x = (uint32_t)reinterpret_cast<const SuccT*>(&v[j])[c];
+                        err |= (x >= Nn) | (x == i0 + c);
+                        rul += h < rT ? 1u : 0u;
+                        ends += (x - b32) >= (uint32_t)TILE ? 1u : 0u;
                     }
+                }
             }
+            exact = __any_sync(0xffffffffu, err);
+            packed = (rul << 16) + ends;
+        }
+        if (exact) {
+            packed = 0;
+#pragma unroll 1
+            for (uint32_t s0 = 0; s0 < (uint32_t)TILE; s0 += PER) {
+                SuccT e[SUB * VEC];
+                if (full) {
+                    const V* src = reinterpret_cast<const V*>(succ + base + s0);
 #pragma unroll
-            for (int j = 0; j < SUB; ++j) {
-                // ruler hash along the lane's VEC consecutive ids: h advances by PHI per id
-                // (is_ruler's (h >> (32 - kbits)) == 0 is h < 2^(32 - kbits); node 0 is added below)
-                uint32_t h = ((uint32_t)base + s0 + (uint32_t)(j * 32 + lane) * VEC) * PHI + salt;
+                    for (int j = 0; j < SUB; ++j) {
+                        const V v = __ldcs(src + j * 32 + lane);
 #pragma unroll
-                for (int c = 0; c < VEC; ++c, h += PHI) {
-                    const uint32_t l = s0 + (j * 32 + lane) * VEC + c;
-                    if (full || base + l < N) {
-                        const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
-                        const uint32_t i = (uint32_t)base + l, x = (uint32_t)x64;
-                        const bool oor = kNarrow ? x >= (uint32_t)N : x64 >= N;
-                        const bool self = !oor && x == i;
-                        if (oor | self) note_succ(st, i, x64, N);
-                        packed += (h < rT ? 0x10000u : 0u) + ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
+                        for (int c = 0; c < VEC; ++c) e[j * VEC + c] = reinterpret_cast<const SuccT*>(&v)[c];
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < SUB; ++j)
+#pragma unroll
+                        for (int c = 0; c < VEC; ++c) {
+                            const unsigned long long i = base + s0 + (unsigned long long)(j * 32 + lane) * VEC + c;
+                            e[j * VEC + c] = i < N ? __ldcs(succ + i) : SuccT(0);
+                        }
+                }
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) {
+                    // ruler hash along the lane's VEC consecutive ids: h advances by PHI per id
+                    // (is_ruler's (h >> (32 - kbits)) == 0 is h < 2^(32 - kbits); node 0 is added below)
+                    uint32_t h = ((uint32_t)base + s0 + (uint32_t)(j * 32 + lane) * VEC) * PHI + salt;
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c, h += PHI) {
+                        const uint32_t l = s0 + (j * 32 + lane) * VEC + c;
+                        if (full || base + l < N) {
+                            const unsigned long long x64 = as_index<SuccT>(e[j * VEC + c]);
+                            const uint32_t i = (uint32_t)base + l, x = (uint32_t)x64;
+                            const bool oor = kNarrow ? x >= (uint32_t)N : x64 >= N;
+                            const bool self = !oor && x == i;
+                            if (oor | self) note_succ(st, i, x64, N);
+                            packed += (h < rT ? 0x10000u : 0u) + ((oor | self | ((x ^ i) >= TILE)) ? 1u : 0u);
+                        }
                     }
                 }
             }
@@ -2425,13 +2465,16 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         unsigned long long* wk = k == 0 ? b.word0 : b.word[k];
         uint32_t* tk = k == 0 ? b.tiles : b.tiles_up;
         if (k == 0) {
-            const uint32_t cw = (nt + TILE_THREADS / 32 - 1) / (TILE_THREADS / 32);  // one warp per tile
-            const uint32_t cg = cw < sm_count() * 8 ? cw : sm_count() * 8;
-            rec.begin(K_RS_COUNT, 0, cg, TILE_THREADS, capN);
             const bool narrow = sizeof(SuccT) == 4 && n <= 0x80000000ull;
             const bool vec = ((uintptr_t)succ & 15) == 0;
             auto kc = vec ? (narrow ? k_rs_count0<SuccT, true, true> : k_rs_count0<SuccT, true, false>)
                           : (narrow ? k_rs_count0<SuccT, false, true> : k_rs_count0<SuccT, false, false>);
+            // persistent warps stride over the tiles by the grid's warp count, so
+            // the grid is what stays resident (48 registers: 5 CTAs per SM, not 8)
+            const uint32_t cw = (nt + TILE_THREADS / 32 - 1) / (TILE_THREADS / 32);  // one warp per tile
+            const uint32_t cmax = sm_count() * resident_ctas(kc, TILE_THREADS);
+            const uint32_t cg = cw < cmax ? cw : cmax;
+            rec.begin(K_RS_COUNT, 0, cg, TILE_THREADS, capN);
             kc<<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0], p.salt[0]);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);

@@ -166,6 +166,28 @@ int sm_count() {
     return v;
 }
 
+int resident_ctas(const void* kernel, int threads) {
+    struct Entry {
+        const void* k;
+        int threads, dev, nb;
+    };
+    static std::mutex mu;
+    static Entry cache[64];
+    static int used = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < used; ++i)
+        if (cache[i].k == kernel && cache[i].threads == threads && cache[i].dev == dev) return cache[i].nb;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0) != cudaSuccess || nb <= 0) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    if (used < 64) cache[used++] = Entry{kernel, threads, dev, nb};
+    return nb;
+}
+
 static uint32_t env_u32(const char* name, uint32_t dflt, uint32_t lo, uint32_t hi) {
     const char* s = getenv(name);
     if (!s || !*s) return dflt;

@@ -216,6 +216,33 @@ def test_invalid_large_lists_detected(cuda):
         g.rs_rank(g.SuccessorList(s), 64)
 
 
+def test_census_full_tile_violations(cuda):
+    """Violations inside full 4096-node tiles: the census's branch-free path
+    flags the tile and its exact re-scan reports the reference's first
+    violation, for host int64 (narrowed to u32 ids) and device int32 input."""
+    n = 100_000
+    base = g.gen_list(n, seed=5).succ
+    cases = []
+    s = base.copy()
+    s[50_000] = 50_000          # two self-loops in different full tiles
+    s[7_000] = 7_000
+    cases.append(s)
+    s = base.copy()
+    s[9_001] = n                # out of range right at n
+    s[60_000] = 60_000
+    cases.append(s)
+    s = base.copy()
+    s[4_096 * 3 + 5] = -2       # negative id
+    cases.append(s)
+    for s in cases:
+        want = g.validate_list(g.SuccessorList(s))
+        assert want is not None
+        for arg in (s, torch.from_numpy(s.astype(np.int32)).cuda()):
+            with pytest.raises(g.InvalidListError) as ei:
+                g.rs_rank(g.SuccessorList(arg), 64)
+            assert str(ei.value) == str(want)
+
+
 def test_rs_reuse_succ_buffer(cuda, orc):
     sl = g.gen_list(1500, seed=17)
     rank, stats = g.rs_rank(sl, p=32, reuse_succ=True, accounting="counts")

@@ -1,0 +1,16 @@
+#!/bin/bash
+# census fast path: GPU list tests + sanitizer on the list paths + lr28/lr28o bench
+TAG=${TAG:-r02bg}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
+timeout 900 python -m pytest tests/test_listrank_gpu.py tests/test_boundary_gpu.py -q -x > $O/pytest.log 2>&1
+timeout 600 compute-sanitizer --tool memcheck --kernel-name kns=sg:: python tools/sanitize_driver.py list > $O/memcheck_list.txt 2>&1
+timeout 600 compute-sanitizer --tool racecheck --racecheck-report all --kernel-name kns=sg:: python tools/sanitize_driver.py list > $O/racecheck_list.txt 2>&1
+for wl in lr28 lr28o lr26; do
+  timeout 300 python bench.py --workload $wl --steps 20 --warmup 5 --no-e2e --no-cpu --blocks none > $O/$wl.json 2>$O/$wl.err
+done
+tail -n 2 $O/pytest.log; tail -n 2 $O/memcheck_list.txt $O/racecheck_list.txt
+for f in $O/*.json; do python -c "
+import json,sys
+d=json.loads(open('$f').read().strip().splitlines()[-1]); k=d['kernels_ms_per_step']; print('$f', d['ms_per_step'], d['step_ms_spread']['median'], k.get('rs1_validate'))"; done
