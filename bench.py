@@ -502,12 +502,19 @@ def e2e_run(a, ctx, kind, n, m, dev_input):
     outs = [step()[0] for _ in range(3)]  # warm: the pinned host-allocator cache fills on the first calls
     del outs
     steps = max(3, min(a.steps, 10))
+    gc.collect()
+    if os.environ.get("SG_BENCH_GC", "0") != "1":
+        gc.disable()  # as in the device-timed loop
     ctx.barrier()
     t0 = time.perf_counter()
+    marks = [t0]
     for _ in range(steps):
         out, _ = step()
+        marks.append(time.perf_counter())
     ctx.barrier()
     dt = ctx.max_over_ranks(time.perf_counter() - t0) / steps
+    gc.enable()
+    per = sorted((b - a_) * 1e3 for a_, b in zip(marks, marks[1:]))
     units = (n * world) if kind == "list" else m
     assert isinstance(out, np.ndarray) and out.shape == (n,)
     return {"value": round(units / dt / 1e6, 1), "unit": "M nodes/s" if kind == "list" else "M edges/s",
@@ -515,6 +522,8 @@ def e2e_run(a, ctx, kind, n, m, dev_input):
             "api": "rs_rank(SuccessorList(pinned int64)) -> numpy int64" if kind == "list"
             else "sv_components(EdgeGraph(pinned int64)) -> numpy int64",
             "host_threads": _xfer_threads(),
+            "step_ms_spread": {"min": round(per[0], 3), "median": round(per[len(per) // 2], 3),
+                               "max": round(per[-1], 3)},
             "timing": "host perf_counter around the API calls, max over ranks"}
 
 
