@@ -440,6 +440,8 @@ def measure(a, ctx, name, primary):
     if kind == "cc":
         res["cc"] = {"rounds": st.meta["rounds"], "edge_sweeps": st.meta["edge_sweeps"],
                      "vertex_sweeps": st.meta["vertex_sweeps"], "components": st.meta["roots_per_round"][-1]}
+        if world > 1:
+            res["cc"]["collectives"] = collective_bw(st.meta, step_kern, world)
     else:
         res["ruling_set"] = {"path": st.meta["path"], "levels": st.meta["levels"],
                              "level_size": st.meta["level_size"], "fallback": st.meta["fallback"]}
@@ -478,6 +480,24 @@ def measure(a, ctx, name, primary):
             cpu["labels_equal_ours"] = bool(np.array_equal(lab, ours.cpu().numpy()))
             res["cpu_baseline"] = cpu
     return res
+
+
+def collective_bw(meta, step_kern, world):
+    """SURVEY 8(d) multi-GPU figures for the sharded rounds: per step, bytes
+    and CUDA-event time of the min all-reduce and the all-gather(s), algbw =
+    bytes / time, busbw = algbw * 2(G-1)/G (all-reduce) or (G-1)/G
+    (all-gather; its span also holds the 8-B root-count all-reduce)."""
+    out = {}
+    for name, key, factor, bkey in (("allreduce_min", "nccl_allreduce_min", 2.0 * (world - 1) / world,
+                                     "allreduce_bytes"),
+                                    ("allgather", "nccl_allgather", (world - 1) / world, "allgather_bytes")):
+        ms = step_kern.get(key, 0.0) + (step_kern.get(key + "_changes", 0.0) if name == "allgather" else 0.0)
+        nbytes = int(meta.get(bkey, 0))
+        algbw = nbytes / (ms / 1e3) / 1e9 if ms > 0 else None
+        out[name] = {"bytes_per_step": nbytes, "ms_per_step": round(ms, 4),
+                     "algbw_gbs": round(algbw, 1) if algbw else None,
+                     "busbw_gbs": round(algbw * factor, 1) if algbw else None}
+    return out
 
 
 def e2e_run(a, ctx, kind, n, m, dev_input):
