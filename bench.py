@@ -71,8 +71,10 @@ def kernel_bytes(kernel, order, out):
         "rs3_walk": 96 if order == "random" else 20,   # RS3: packed write + succ[cur] + packed read (listrank.py:279-283)
         "rs5_refine": 8 + 8,                           # binned walk record in, {cur, rank} out (IS_1 gather: L2)
         "rs5_scatter": 8 + out,
-        "rs3_contract": 4 + 4,                         # succ in, {segment, distance} word out
-        "rs5_expand": 4 + out,                         # node word in, rank out
+        # contraction: succ in, {segment, distance} word out; the run tiles of an
+        # ordered list are settled from the census's flag (no per-node bytes)
+        "rs3_contract": 4 + 4 if order != "ordered" else None,
+        "rs5_expand": 4 + out if order != "ordered" else out,  # node word in (not for run tiles), rank out
         "rs1_validate": 4,
         "cc_hook_uf": CC_EDGE_SWEEP_BYTES,
         "cc_hook_sv": CC_EDGE_SWEEP_BYTES,

@@ -293,7 +293,8 @@ template <class SuccT, bool kVec, bool kNarrow>
 __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restrict__ succ,
                                                             uint32_t* __restrict__ tile_cnt,
                                                             uint32_t* __restrict__ tile_end, ListStatus* st,
-                                                            uint32_t kbits, uint32_t salt) {
+                                                            uint32_t kbits, uint32_t salt,
+                                                            uint32_t* __restrict__ tile_run) {
     // one warp per tile (persistent warps): no block barrier between tiles, so
     // a warp's next loads never wait on its neighbours' reductions
     constexpr int VEC = 16 / sizeof(SuccT);  // ids per 16-B load
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
         if (kFast && full) {
             const uint32_t Nn = (uint32_t)N, b32 = (uint32_t)base;
             uint32_t rul = 0, ends = 0;
-            bool err = false;
+            bool err = false, brk = false;  // brk: some successor is not the next id
 #pragma unroll 1
             for (uint32_t s0 = 0; s0 < (uint32_t)TILE; s0 += PER) {
                 V v[SUB];
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
                     for (int c = 0; c < VEC; ++c, h += PHI) {
                         const uint32_t x = (uint32_t)reinterpret_cast<const SuccT*>(&v[j])[c];
                         err |= (x >= Nn) | (x == i0 + c);
+                        brk |= x != i0 + c + 1;
                         rul += h < rT ? 1u : 0u;
                         ends += (x - b32) >= (uint32_t)TILE ? 1u : 0u;
                     }
@@ -346,6 +348,13 @@ __global__ void __launch_bounds__(TILE_THREADS) k_rs_count0(const SuccT* __restr
             }
             exact = __any_sync(0xffffffffu, err);
             packed = (rul << 16) + ends;
+            // a full tile whose every successor is the next id (its last node
+            // continues into the next tile): the contraction takes it without
+            // reading it again
+            const bool run = !exact && !__any_sync(0xffffffffu, brk);
+            if (lane == 0) tile_run[tile] = run ? 1u : 0u;
+        } else if (lane == 0) {
+            tile_run[tile] = 0u;
         }
         if (exact) {
             packed = 0;
@@ -1847,7 +1856,7 @@ template <class SuccT, bool kVec>
 __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
     const SuccT* __restrict__ succ, ListStatus* st, const uint32_t* __restrict__ tile_off,
     uint32_t* __restrict__ headsid, uint32_t* __restrict__ seg_head, uint32_t* __restrict__ seg_succ,
-    uint2* __restrict__ lvl1, uint32_t* __restrict__ node_word) {
+    uint2* __restrict__ lvl1, uint32_t* __restrict__ node_word, uint32_t* __restrict__ tile_run) {
     if (!layout_local(st)) return;
     constexpr int VEC = 4;  // ids per thread and vector access
     constexpr int NV = TILE_ITEMS / VEC;
@@ -1862,336 +1871,381 @@ __global__ void __launch_bounds__(TILE_THREADS, CT_CTAS_PER_SM) k_rs_contract(
     const uint32_t lane = lane_id();
     static_assert(TILE == TILE_THREADS * 16, "one uint4 of predecessor flags per thread");
     bool bad = false;
-    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const unsigned long long base = tile * TILE;
-        const uint32_t tn = (uint32_t)min((unsigned long long)TILE, N - base);
-        const bool full = kVec && tn == TILE;
-        // 1. successors -> in-tile links, predecessor flags (plain byte
-        //    stores: a node with two in-tile predecessors shows up as fewer
-        //    flags than links), run-break masks.  Thread t holds ids
-        //    4(j*256+t) .. +3.
-        SuccT v[TILE_ITEMS];
-        if (full) {
-#pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                const SuccT* p = succ + base + (size_t)(j * TILE_THREADS + t) * VEC;
-                if (sizeof(SuccT) == 4) {
-                    const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p));
-                    v[j * 4 + 0] = (SuccT)w.x, v[j * 4 + 1] = (SuccT)w.y, v[j * 4 + 2] = (SuccT)w.z, v[j * 4 + 3] = (SuccT)w.w;
+    // the CTA's tiles in batches of TILE_THREADS: thread k settles batch tile k
+    // if the census flagged it as a run (succ = id + 1 throughout, the last
+    // node continuing into the next tile: one segment, written without
+    // reading the tile again); the CTA then contracts the others together
+    __shared__ uint32_t s_run[TILE_THREADS];
+    const unsigned long long bstep = (unsigned long long)TILE_THREADS * gridDim.x;
+    for (unsigned long long tb = blockIdx.x; tb < ntiles; tb += bstep) {
+        {
+            const unsigned long long mt = tb + (unsigned long long)t * gridDim.x;
+            const uint32_t r = mt < ntiles ? __ldg(tile_run + mt) : 1u;
+            if (mt < ntiles && r) {
+                const unsigned long long sid = tile_off[mt];
+                const uint32_t segs = mt + 1 < ntiles ? tile_off[mt + 1] - tile_off[mt] : (uint32_t)(R1 - tile_off[mt]);
+                if (segs != 1u) {
+                    bad = true;
                 } else {
-                    const ulonglong2 w0 = __ldcs(reinterpret_cast<const ulonglong2*>(p));
-                    const ulonglong2 w1 = __ldcs(reinterpret_cast<const ulonglong2*>(p) + 1);
-                    v[j * 4 + 0] = (SuccT)w0.x, v[j * 4 + 1] = (SuccT)w0.y, v[j * 4 + 2] = (SuccT)w1.x, v[j * 4 + 3] = (SuccT)w1.y;
+                    const unsigned long long mb = mt * TILE;
+                    seg_head[sid] = (uint32_t)mb;
+                    headsid[mb] = (uint32_t)sid;
+                    lvl1[sid] = make_uint2(0u, (uint32_t)TILE);
+                    seg_succ[sid] = (uint32_t)(mb + TILE);
                 }
             }
-        } else {
-#pragma unroll
-            for (int j = 0; j < NV; ++j)
-#pragma unroll
-                for (int c = 0; c < VEC; ++c) {
-                    const uint32_t l = (j * TILE_THREADS + t) * VEC + c;
-                    v[j * 4 + c] = l < tn ? succ[base + l] : SuccT(0);
-                }
+            s_run[t] = r;
+            __syncthreads();
         }
-        // Single-run tile (every id's successor is the next id, the last one
-        // leaves the tile or is the tail), decided from the registers: one
-        // segment, distance to its end = tn - 1 - l, written in closed form
-        // without the shared-memory ranking.
-        {
-            bool run = true;
-            const uint32_t last = tn - 1;
-#pragma unroll
-            for (int j = 0; j < NV; ++j)
-#pragma unroll
-                for (int c = 0; c < VEC; ++c) {
-                    const uint32_t l = (j * TILE_THREADS + t) * VEC + c;
-                    const unsigned long long x = as_index<SuccT>(v[j * 4 + c]);
-                    if (l < last)
-                        run &= x == base + l + 1;
-                    else if (l == last)
-                        run &= (x - base >= tn) || x == base + l;
-                }
-            if (__syncthreads_and(run)) {
-                const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
-                                                        : (uint32_t)(R1 - tile_off[tile]);
-                if (segs != 1u) bad = true;
-                if (t == 0 && segs == 1u) {
-                    const unsigned long long sid = tile_off[tile];
-                    seg_head[sid] = (uint32_t)base;
-                    headsid[base] = (uint32_t)sid;
-                    lvl1[sid] = make_uint2(0u, tn);
-                    const unsigned long long x = as_index<SuccT>(succ[base + last]);
-                    seg_succ[sid] = (x >= N || x == base + last) ? NIL : (uint32_t)x;
-                }
+        for (uint32_t k = 0; k < (uint32_t)TILE_THREADS; ++k) {
+            if (s_run[k]) continue;  // a run (settled above) or past the end
+            const unsigned long long tile = tb + (unsigned long long)k * gridDim.x;
+            const unsigned long long base = tile * TILE;
+            const uint32_t tn = (uint32_t)min((unsigned long long)TILE, N - base);
+            const bool full = kVec && tn == TILE;
+            // 1. successors -> in-tile links, predecessor flags (plain byte
+            //    stores: a node with two in-tile predecessors shows up as fewer
+            //    flags than links), run-break masks.  Thread t holds ids
+            //    4(j*256+t) .. +3.
+            SuccT v[TILE_ITEMS];
+            if (full) {
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
-                    const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
-                    if (full) {
-                        *reinterpret_cast<uint4*>(node_word + base + l0) =
-                            make_uint4(last - l0, last - l0 - 1, last - l0 - 2, last - l0 - 3);
+                    const SuccT* p = succ + base + (size_t)(j * TILE_THREADS + t) * VEC;
+                    if (sizeof(SuccT) == 4) {
+                        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p));
+                        v[j * 4 + 0] = (SuccT)w.x, v[j * 4 + 1] = (SuccT)w.y, v[j * 4 + 2] = (SuccT)w.z, v[j * 4 + 3] = (SuccT)w.w;
                     } else {
-#pragma unroll
-                        for (int c = 0; c < VEC; ++c)
-                            if (l0 + c < tn) node_word[base + l0 + c] = last - (l0 + c);
+                        const ulonglong2 w0 = __ldcs(reinterpret_cast<const ulonglong2*>(p));
+                        const ulonglong2 w1 = __ldcs(reinterpret_cast<const ulonglong2*>(p) + 1);
+                        v[j * 4 + 0] = (SuccT)w0.x, v[j * 4 + 1] = (SuccT)w0.y, v[j * 4 + 2] = (SuccT)w1.x, v[j * 4 + 3] = (SuccT)w1.y;
                     }
                 }
-                continue;  // no shared memory was touched
-            }
-        }
-        reinterpret_cast<uint4*>(S.pred)[t] = make_uint4(0u, 0u, 0u, 0u);  // 4096 flags
-        __syncthreads();
-        uint32_t links = 0;
+            } else {
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
-            uint16_t nx[VEC];
-            uint32_t nib = 0;  // run breaks: nx[l] != l + 1
+                for (int j = 0; j < NV; ++j)
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-                const uint32_t l = l0 + c;
-                nx[c] = CT_END;
-                if (l < tn) {
-                    const unsigned long long dx = as_index<SuccT>(v[j * 4 + c]) - base;
-                    if (dx < tn && dx != l) {
-                        nx[c] = (uint16_t)dx;
-                        S.pred[dx] = 1;
-                        ++links;
+                    for (int c = 0; c < VEC; ++c) {
+                        const uint32_t l = (j * TILE_THREADS + t) * VEC + c;
+                        v[j * 4 + c] = l < tn ? succ[base + l] : SuccT(0);
                     }
+            }
+            // Single-run tile (every id's successor is the next id, the last one
+            // leaves the tile or is the tail), decided from the registers: one
+            // segment, distance to its end = tn - 1 - l, written in closed form
+            // without the shared-memory ranking.
+            {
+                bool run = true;
+                const uint32_t last = tn - 1;
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c) {
+                        const uint32_t l = (j * TILE_THREADS + t) * VEC + c;
+                        const unsigned long long x = as_index<SuccT>(v[j * 4 + c]);
+                        if (l < last)
+                            run &= x == base + l + 1;
+                        else if (l == last)
+                            run &= (x - base >= tn) || x == base + l;
+                    }
+                if (__syncthreads_and(run)) {
+                    const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
+                                                            : (uint32_t)(R1 - tile_off[tile]);
+                    if (segs != 1u) bad = true;
+                    if (t == 0 && segs == 1u) {
+                        const unsigned long long sid = tile_off[tile];
+                        seg_head[sid] = (uint32_t)base;
+                        headsid[base] = (uint32_t)sid;
+                        lvl1[sid] = make_uint2(0u, tn);
+                        const unsigned long long x = as_index<SuccT>(succ[base + last]);
+                        seg_succ[sid] = (x >= N || x == base + last) ? NIL : (uint32_t)x;
+                    }
+                    // the node words of a run are tn - 1 - l (segment 0): the
+                    // expand recomputes them from this flag instead of a 4-B
+                    // write and read per node
+                    if (t == 0) tile_run[tile] = 1u;
+                    continue;  // no shared memory was touched
                 }
-                if (nx[c] != l + 1) nib |= 1u << c;
             }
-            *reinterpret_cast<ushort4*>(&S.nx[sw16(l0)]) = make_ushort4(nx[0], nx[1], nx[2], nx[3]);
-            *reinterpret_cast<uint4*>(&S.own[sw32(l0) & ~3u]) = make_uint4(~0u, ~0u, ~0u, ~0u);
-            // the 4 nibbles of a 16-id block sit in 4 consecutive lanes
-            uint32_t m16 = nib << (4 * (lane & 3));
-            m16 |= __shfl_xor_sync(0xffffffffu, m16, 1);
-            m16 |= __shfl_xor_sync(0xffffffffu, m16, 2);
-            if ((lane & 3) == 0) S.brk[l0 >> 4] = (uint16_t)m16;
-        }
-        __syncthreads();
-        if (tile == 0 && S.pred[0]) bad = true;  // node 0 must start the list
-        // 2. local rulers (blocked: thread t owns nodes 16t .. 16t+15): heads
-        //    and every CT_STRIDE-th node; numbered in index order
-        uint32_t rflags = 0, hflags = 0;
-        const uint4 pf = reinterpret_cast<const uint4*>(S.pred)[t];
-        const uint32_t pw[4] = {pf.x, pf.y, pf.z, pf.w};
+            if (t == 0) tile_run[tile] = 0u;
+            reinterpret_cast<uint4*>(S.pred)[t] = make_uint4(0u, 0u, 0u, 0u);  // 4096 flags
+            __syncthreads();
+            uint32_t links = 0;
 #pragma unroll
-        for (int q = 0; q < TILE_ITEMS; ++q) {
-            const uint32_t l = t * TILE_ITEMS + q;
-            if (l < tn) {
-                const bool head = ((pw[q >> 2] >> (8 * (q & 3))) & 0xFFu) == 0u;
-                if (head) hflags |= 1u << q;
-                if (head || (l % CT_STRIDE) == 0) rflags |= 1u << q;
-            }
-        }
-        // one scan: rulers (bits 32..), heads (16..31), in-tile links (0..15)
-        unsigned long long packed = ((unsigned long long)__popc(rflags) << 32) |
-                                    ((unsigned long long)__popc(hflags) << 16) | links, pre, tot;
-        BS(scan_tmp).ExclusiveSum(packed, pre, tot);
-        const uint32_t rpre = (uint32_t)(pre >> 32), hpre = (uint32_t)(pre >> 16) & 0xFFFFu;
-        const uint32_t K = (uint32_t)(tot >> 32), H = (uint32_t)(tot >> 16) & 0xFFFFu;
-        if (H + (uint32_t)(tot & 0xFFFFu) != tn) bad = true;  // two in-tile predecessors
+            for (int j = 0; j < NV; ++j) {
+                const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
+                uint16_t nx[VEC];
+                uint32_t nib = 0;  // run breaks: nx[l] != l + 1
 #pragma unroll
-        for (int g = 0; g < TILE_ITEMS / 4; ++g) {
-            uint16_t r[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int q = g * 4 + c;
-                r[c] = (rflags & (1u << q)) ? (uint16_t)(rpre + __popc(rflags & ((1u << q) - 1u))) : CT_END;
-            }
-            *reinterpret_cast<ushort4*>(&S.rid[sw16(t * TILE_ITEMS + g * 4)]) = make_ushort4(r[0], r[1], r[2], r[3]);
-        }
-        __syncthreads();
-        // 3. each thread walks from its own local rulers to the next local
-        //    ruler / the segment end.  A run of +1 successors inside a 16-id
-        //    block is crossed in one step (no ruler can sit inside it: its
-        //    nodes have in-tile predecessors and are not 16-aligned); the
-        //    block start after a full run is a ruler.
-        for (uint32_t rem = rflags; rem != 0; rem &= rem - 1) {
-            const uint32_t q = __ffs(rem) - 1;
-            const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
-            uint32_t l = t * TILE_ITEMS + q, off = 0;
-            for (;;) {
-                const uint32_t m = (uint32_t)S.brk[l >> 4] >> (l & 15u);
-                const uint32_t r = m ? (uint32_t)(__ffs(m) - 1) : 16u - (l & 15u);
-                if (r) {
-                    if (r == 16) {  // a whole block: four 16-B stores (sw32 permutes each group by XOR)
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            const uint32_t gp = sw32(l + 4 * g), xr = gp & 3u;
-                            const uint32_t b0 = (k << 16) | (off + 4 * g);
-                            *reinterpret_cast<uint4*>(&S.own[gp & ~3u]) =
-                                make_uint4(b0 + (0u ^ xr), b0 + (1u ^ xr), b0 + (2u ^ xr), b0 + (3u ^ xr));
+                for (int c = 0; c < VEC; ++c) {
+                    const uint32_t l = l0 + c;
+                    nx[c] = CT_END;
+                    if (l < tn) {
+                        const unsigned long long dx = as_index<SuccT>(v[j * 4 + c]) - base;
+                        if (dx < tn && dx != l) {
+                            nx[c] = (uint16_t)dx;
+                            S.pred[dx] = 1;
+                            ++links;
                         }
-                    } else {
-                        for (uint32_t j = 0; j < r; ++j) S.own[sw32(l + j)] = (k << 16) | (off + j);
                     }
-                    l += r;
-                    off += r;
-                    if (m == 0) {  // l: the next block's first id, a ruler
-                        S.link[k] = ((uint32_t)S.rid[sw16(l)] << 16) | off;
+                    if (nx[c] != l + 1) nib |= 1u << c;
+                }
+                *reinterpret_cast<ushort4*>(&S.nx[sw16(l0)]) = make_ushort4(nx[0], nx[1], nx[2], nx[3]);
+                *reinterpret_cast<uint4*>(&S.own[sw32(l0) & ~3u]) = make_uint4(~0u, ~0u, ~0u, ~0u);
+                // the 4 nibbles of a 16-id block sit in 4 consecutive lanes
+                uint32_t m16 = nib << (4 * (lane & 3));
+                m16 |= __shfl_xor_sync(0xffffffffu, m16, 1);
+                m16 |= __shfl_xor_sync(0xffffffffu, m16, 2);
+                if ((lane & 3) == 0) S.brk[l0 >> 4] = (uint16_t)m16;
+            }
+            __syncthreads();
+            if (tile == 0 && S.pred[0]) bad = true;  // node 0 must start the list
+            // 2. local rulers (blocked: thread t owns nodes 16t .. 16t+15): heads
+            //    and every CT_STRIDE-th node; numbered in index order
+            uint32_t rflags = 0, hflags = 0;
+            const uint4 pf = reinterpret_cast<const uint4*>(S.pred)[t];
+            const uint32_t pw[4] = {pf.x, pf.y, pf.z, pf.w};
+#pragma unroll
+            for (int q = 0; q < TILE_ITEMS; ++q) {
+                const uint32_t l = t * TILE_ITEMS + q;
+                if (l < tn) {
+                    const bool head = ((pw[q >> 2] >> (8 * (q & 3))) & 0xFFu) == 0u;
+                    if (head) hflags |= 1u << q;
+                    if (head || (l % CT_STRIDE) == 0) rflags |= 1u << q;
+                }
+            }
+            // one scan: rulers (bits 32..), heads (16..31), in-tile links (0..15)
+            unsigned long long packed = ((unsigned long long)__popc(rflags) << 32) |
+                                        ((unsigned long long)__popc(hflags) << 16) | links, pre, tot;
+            BS(scan_tmp).ExclusiveSum(packed, pre, tot);
+            const uint32_t rpre = (uint32_t)(pre >> 32), hpre = (uint32_t)(pre >> 16) & 0xFFFFu;
+            const uint32_t K = (uint32_t)(tot >> 32), H = (uint32_t)(tot >> 16) & 0xFFFFu;
+            if (H + (uint32_t)(tot & 0xFFFFu) != tn) bad = true;  // two in-tile predecessors
+#pragma unroll
+            for (int g = 0; g < TILE_ITEMS / 4; ++g) {
+                uint16_t r[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int q = g * 4 + c;
+                    r[c] = (rflags & (1u << q)) ? (uint16_t)(rpre + __popc(rflags & ((1u << q) - 1u))) : CT_END;
+                }
+                *reinterpret_cast<ushort4*>(&S.rid[sw16(t * TILE_ITEMS + g * 4)]) = make_ushort4(r[0], r[1], r[2], r[3]);
+            }
+            __syncthreads();
+            // 3. each thread walks from its own local rulers to the next local
+            //    ruler / the segment end.  A run of +1 successors inside a 16-id
+            //    block is crossed in one step (no ruler can sit inside it: its
+            //    nodes have in-tile predecessors and are not 16-aligned); the
+            //    block start after a full run is a ruler.
+            for (uint32_t rem = rflags; rem != 0; rem &= rem - 1) {
+                const uint32_t q = __ffs(rem) - 1;
+                const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
+                uint32_t l = t * TILE_ITEMS + q, off = 0;
+                for (;;) {
+                    const uint32_t m = (uint32_t)S.brk[l >> 4] >> (l & 15u);
+                    const uint32_t r = m ? (uint32_t)(__ffs(m) - 1) : 16u - (l & 15u);
+                    if (r) {
+                        if (r == 16) {  // a whole block: four 16-B stores (sw32 permutes each group by XOR)
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                const uint32_t gp = sw32(l + 4 * g), xr = gp & 3u;
+                                const uint32_t b0 = (k << 16) | (off + 4 * g);
+                                *reinterpret_cast<uint4*>(&S.own[gp & ~3u]) =
+                                    make_uint4(b0 + (0u ^ xr), b0 + (1u ^ xr), b0 + (2u ^ xr), b0 + (3u ^ xr));
+                            }
+                        } else {
+                            for (uint32_t j = 0; j < r; ++j) S.own[sw32(l + j)] = (k << 16) | (off + j);
+                        }
+                        l += r;
+                        off += r;
+                        if (m == 0) {  // l: the next block's first id, a ruler
+                            S.link[k] = ((uint32_t)S.rid[sw16(l)] << 16) | off;
+                            S.term[k] = CT_END;
+                            break;
+                        }
+                    }
+                    S.own[sw32(l)] = (k << 16) | off;
+                    const uint16_t nx = S.nx[sw16(l)];
+                    if (nx == CT_END) {
+                        S.link[k] = ((uint32_t)CT_END << 16) | off;
+                        S.term[k] = (uint16_t)l;
+                        break;
+                    }
+                    const uint16_t r2 = S.rid[sw16(nx)];
+                    if (r2 != CT_END || off + 1 >= TILE) {  // the cap only trips on invalid lists
+                        if (r2 == CT_END) bad = true;
+                        S.link[k] = ((uint32_t)(r2 == CT_END ? k : r2) << 16) | ((off + 1) & 0xFFFFu);
                         S.term[k] = CT_END;
                         break;
                     }
+                    l = nx;
+                    ++off;
                 }
-                S.own[sw32(l)] = (k << 16) | off;
-                const uint16_t nx = S.nx[sw16(l)];
-                if (nx == CT_END) {
-                    S.link[k] = ((uint32_t)CT_END << 16) | off;
-                    S.term[k] = (uint16_t)l;
-                    break;
-                }
-                const uint16_t r2 = S.rid[sw16(nx)];
-                if (r2 != CT_END || off + 1 >= TILE) {  // the cap only trips on invalid lists
-                    if (r2 == CT_END) bad = true;
-                    S.link[k] = ((uint32_t)(r2 == CT_END ? k : r2) << 16) | ((off + 1) & 0xFFFFu);
-                    S.term[k] = CT_END;
-                    break;
-                }
-                l = nx;
-                ++off;
             }
-        }
-        __syncthreads();
-        // 4. weighted pointer jumping over the local rulers, in place (one
-        //    32-bit {next, distance} word per ruler keeps every read
-        //    consistent), until each ruler points at the last ruler of its
-        //    segment -- whose word holds the distance to the end
-        for (int round = 0; round < 16; ++round) {
-            int active = 0;
-            for (uint32_t k = t; k < K; k += TILE_THREADS) {
+            __syncthreads();
+            // 4. weighted pointer jumping over the local rulers, in place (one
+            //    32-bit {next, distance} word per ruler keeps every read
+            //    consistent), until each ruler points at the last ruler of its
+            //    segment -- whose word holds the distance to the end
+            for (int round = 0; round < 16; ++round) {
+                int active = 0;
+                for (uint32_t k = t; k < K; k += TILE_THREADS) {
+                    const uint32_t a = S.link[k];
+                    const uint32_t p = a >> 16;
+                    if (p != CT_END) {
+                        const uint32_t b = S.link[p];
+                        if ((b >> 16) != CT_END) {
+                            S.link[k] = (b & 0xFFFF0000u) | ((a + b) & 0xFFFFu);
+                            active = 1;
+                        }
+                    }
+                }
+                if (!__syncthreads_or(active)) break;
+            }
+            // distance from ruler k to its segment end, and the end node
+            auto seg_end = [&](uint32_t k, uint32_t& d, uint16_t& e) {
                 const uint32_t a = S.link[k];
                 const uint32_t p = a >> 16;
-                if (p != CT_END) {
+                if (p == CT_END) {
+                    d = a & 0xFFFFu;
+                    e = S.term[k];
+                } else {
                     const uint32_t b = S.link[p];
-                    if ((b >> 16) != CT_END) {
-                        S.link[k] = (b & 0xFFFF0000u) | ((a + b) & 0xFFFFu);
-                        active = 1;
-                    }
+                    d = (a + b) & 0xFFFFu;
+                    e = (b >> 16) == CT_END ? S.term[p] : CT_END;
+                }
+            };
+            for (uint32_t k = t; k < K; k += TILE_THREADS) {
+                uint32_t d;
+                uint16_t e;
+                seg_end(k, d, e);
+                if (e == CT_END) bad = true;  // a cycle through local rulers
+            }
+            // 5. segments: numbered by head index; end node -> tile-local segment
+            const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
+                                                    : (uint32_t)(R1 - tile_off[tile]);
+            if (segs != H) bad = true;
+            __syncthreads();  // rid[] is rewritten below
+            for (uint32_t rem = hflags; rem != 0; rem &= rem - 1) {
+                const uint32_t q = __ffs(rem) - 1;
+                const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
+                const uint32_t h = hpre + __popc(hflags & ((1u << q) - 1u));
+                uint32_t d;
+                uint16_t e;
+                seg_end(k, d, e);
+                if (e != CT_END) S.rid[sw16(e)] = (uint16_t)h;
+                if (h < segs && e != CT_END) {
+                    const unsigned long long sid = (unsigned long long)tile_off[tile] + h;
+                    const uint32_t l = t * TILE_ITEMS + q;
+                    seg_head[sid] = (uint32_t)(base + l);
+                    headsid[base + l] = (uint32_t)sid;
+                    lvl1[sid] = make_uint2(0u, d + 1u);
+                    const unsigned long long x = as_index<SuccT>(succ[base + e]);
+                    seg_succ[sid] = (x >= N || x == base + e) ? NIL : (uint32_t)x;
                 }
             }
-            if (!__syncthreads_or(active)) break;
-        }
-        // distance from ruler k to its segment end, and the end node
-        auto seg_end = [&](uint32_t k, uint32_t& d, uint16_t& e) {
-            const uint32_t a = S.link[k];
-            const uint32_t p = a >> 16;
-            if (p == CT_END) {
-                d = a & 0xFFFFu;
-                e = S.term[k];
-            } else {
-                const uint32_t b = S.link[p];
-                d = (a + b) & 0xFFFFu;
-                e = (b >> 16) == CT_END ? S.term[p] : CT_END;
+            __syncthreads();
+            // per ruler: its segment (tile-local) and distance to the segment end;
+            // nx[] is dead after the walk and holds the segment from here on
+            for (uint32_t k = t; k < K; k += TILE_THREADS) {
+                uint32_t d;
+                uint16_t e;
+                seg_end(k, d, e);
+                S.nx[k] = e != CT_END ? S.rid[sw16(e)] : CT_END;
+                S.rd[k] = (uint16_t)d;
             }
-        };
-        for (uint32_t k = t; k < K; k += TILE_THREADS) {
-            uint32_t d;
-            uint16_t e;
-            seg_end(k, d, e);
-            if (e == CT_END) bad = true;  // a cycle through local rulers
-        }
-        // 5. segments: numbered by head index; end node -> tile-local segment
-        const uint32_t segs = tile + 1 < ntiles ? tile_off[tile + 1] - tile_off[tile]
-                                                : (uint32_t)(R1 - tile_off[tile]);
-        if (segs != H) bad = true;
-        __syncthreads();  // rid[] is rewritten below
-        for (uint32_t rem = hflags; rem != 0; rem &= rem - 1) {
-            const uint32_t q = __ffs(rem) - 1;
-            const uint32_t k = rpre + __popc(rflags & ((1u << q) - 1u));
-            const uint32_t h = hpre + __popc(hflags & ((1u << q) - 1u));
-            uint32_t d;
-            uint16_t e;
-            seg_end(k, d, e);
-            if (e != CT_END) S.rid[sw16(e)] = (uint16_t)h;
-            if (h < segs && e != CT_END) {
-                const unsigned long long sid = (unsigned long long)tile_off[tile] + h;
-                const uint32_t l = t * TILE_ITEMS + q;
-                seg_head[sid] = (uint32_t)(base + l);
-                headsid[base + l] = (uint32_t)sid;
-                lvl1[sid] = make_uint2(0u, d + 1u);
-                const unsigned long long x = as_index<SuccT>(succ[base + e]);
-                seg_succ[sid] = (x >= N || x == base + e) ? NIL : (uint32_t)x;
-            }
-        }
-        __syncthreads();
-        // per ruler: its segment (tile-local) and distance to the segment end;
-        // nx[] is dead after the walk and holds the segment from here on
-        for (uint32_t k = t; k < K; k += TILE_THREADS) {
-            uint32_t d;
-            uint16_t e;
-            seg_end(k, d, e);
-            S.nx[k] = e != CT_END ? S.rid[sw16(e)] : CT_END;
-            S.rd[k] = (uint16_t)d;
-        }
-        __syncthreads();
-        // 6. per node: {tile-local segment : 16 | distance to the segment end : 16}
+            __syncthreads();
+            // 6. per node: {tile-local segment : 16 | distance to the segment end : 16}
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
-            const uint32_t g = sw32(l0);
-            const uint4 ow4 = *reinterpret_cast<const uint4*>(&S.own[g & ~3u]);
-            const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
-            uint32_t wd[VEC];
+            for (int j = 0; j < NV; ++j) {
+                const uint32_t l0 = (j * TILE_THREADS + t) * VEC;
+                const uint32_t g = sw32(l0);
+                const uint4 ow4 = *reinterpret_cast<const uint4*>(&S.own[g & ~3u]);
+                const uint32_t ow[4] = {ow4.x, ow4.y, ow4.z, ow4.w};
+                uint32_t wd[VEC];
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) {
-                const uint32_t o = ow[c ^ (g & 3u)];
-                wd[c] = 0xFFFFFFFFu;
-                if (l0 + c < tn) {
-                    if (o == 0xFFFFFFFFu) {
-                        bad = true;  // a cycle without local rulers
-                    } else {
-                        const uint32_t k = o >> 16;
-                        wd[c] = ((uint32_t)S.nx[k] << 16) | (((uint32_t)S.rd[k] - (o & 0xFFFFu)) & 0xFFFFu);
+                for (int c = 0; c < VEC; ++c) {
+                    const uint32_t o = ow[c ^ (g & 3u)];
+                    wd[c] = 0xFFFFFFFFu;
+                    if (l0 + c < tn) {
+                        if (o == 0xFFFFFFFFu) {
+                            bad = true;  // a cycle without local rulers
+                        } else {
+                            const uint32_t k = o >> 16;
+                            wd[c] = ((uint32_t)S.nx[k] << 16) | (((uint32_t)S.rd[k] - (o & 0xFFFFu)) & 0xFFFFu);
+                        }
                     }
                 }
-            }
-            if (full) {
-                *reinterpret_cast<uint4*>(node_word + base + l0) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-            } else {
+                if (full) {
+                    *reinterpret_cast<uint4*>(node_word + base + l0) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                } else {
 #pragma unroll
-                for (int c = 0; c < VEC; ++c)
-                    if (l0 + c < tn) node_word[base + l0 + c] = wd[c];
+                    for (int c = 0; c < VEC; ++c)
+                        if (l0 + c < tn) node_word[base + l0 + c] = wd[c];
+                }
             }
+            __syncthreads();  // shared memory is reused by the next tile
         }
-        __syncthreads();  // shared memory is reused by the next tile
+        __syncthreads();  // s_run is rewritten by the next batch
     }
     if (bad) st->bad = 1;
 }
 
 // expand the contraction: rank = (IS1[segment] - length) + distance to the
-// segment end; two streaming 4-B accesses per node plus L1-resident gathers
+// segment end.  One warp per tile: the tile's flag and first segment are
+// loaded once, then the lanes stream the tile -- a run tile (k_rs_count0 /
+// k_rs_contract flag) is one segment whose words are tn - 1 - l, so its ranks
+// are written without reading anything per node; other tiles read their node
+// words and gather their segments' bases (L1-resident).
 template <class OutT, bool kVec>
 __global__ void __launch_bounds__(256) k_rs_contract_expand(const uint32_t* __restrict__ node_word,
                                                             const uint32_t* __restrict__ tile_off,
                                                             const uint2* __restrict__ lvl1,
                                                             const uint32_t* __restrict__ IS1, OutT* __restrict__ rank,
-                                                            const ListStatus* st) {
+                                                            const ListStatus* st, const uint32_t* __restrict__ tile_run) {
     if (!layout_local(st) || ranks_invalid(st)) return;
     const unsigned long long N = st->R[0];
     const unsigned long long R1 = st->R[1];
-    auto rank_of = [&](unsigned long long i, uint32_t w) -> uint32_t {
-        const unsigned long long sid = (unsigned long long)__ldg(tile_off + (i / TILE)) + (w >> 16);
-        return sid < R1 ? __ldg(IS1 + sid) - __ldg(&lvl1[sid].y) + (w & 0xFFFFu) : 0u;
-    };
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    const unsigned long long nq = kVec ? N / 4 : 0;
-    for (unsigned long long qd = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; qd < nq; qd += stride) {
-        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(node_word) + qd);
-        const unsigned long long i = qd * 4;
-        const uint32_t r0 = rank_of(i, w.x), r1 = rank_of(i + 1, w.y), r2 = rank_of(i + 2, w.z),
-                       r3 = rank_of(i + 3, w.w);
+    const unsigned long long ntiles = (N + TILE - 1) / TILE;
+    const uint32_t lane = lane_id();
+    const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    auto put4 = [&](unsigned long long i, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
         if (sizeof(OutT) == 4) {
-            __stcs(reinterpret_cast<uint4*>(rank) + qd, make_uint4(r0, r1, r2, r3));
+            __stcs(reinterpret_cast<uint4*>(rank + i), make_uint4(r0, r1, r2, r3));
         } else {
-            ulonglong2* q = reinterpret_cast<ulonglong2*>(rank) + 2 * qd;
+            ulonglong2* q = reinterpret_cast<ulonglong2*>(rank + i);
             __stcs(q, make_ulonglong2(r0, r1));
             __stcs(q + 1, make_ulonglong2(r2, r3));
         }
+    };
+    for (unsigned long long tile = gw; tile < ntiles; tile += nw) {
+        const unsigned long long base = tile * TILE;
+        const uint32_t tn = (uint32_t)min((unsigned long long)TILE, N - base);
+        const unsigned long long off = __ldg(tile_off + tile);
+        if (__ldg(tile_run + tile)) {
+            // rank of id base + l = r - l (0 throughout for an out-of-range segment, as rank_of)
+            const uint32_t r = off < R1 ? __ldg(IS1 + off) - __ldg(&lvl1[off].y) + (tn - 1) : 0u;
+            const uint32_t dl = off < R1 ? 1u : 0u;
+            const uint32_t nq = kVec ? tn / 4 : 0;
+            for (uint32_t q = lane; q < nq; q += 32) {
+                const uint32_t x = r - 4 * q * dl;
+                put4(base + 4 * q, x, x - dl, x - 2 * dl, x - 3 * dl);
+            }
+            for (uint32_t l = nq * 4 + lane; l < tn; l += 32) rank[base + l] = (OutT)(r - l * dl);
+        } else {
+            auto rank_of = [&](uint32_t w) -> uint32_t {
+                const unsigned long long sid = off + (w >> 16);
+                return sid < R1 ? __ldg(IS1 + sid) - __ldg(&lvl1[sid].y) + (w & 0xFFFFu) : 0u;
+            };
+            const uint32_t nq = kVec ? tn / 4 : 0;
+            for (uint32_t q = lane; q < nq; q += 32) {
+                const uint4 w = __ldcs(reinterpret_cast<const uint4*>(node_word + base) + q);
+                put4(base + 4 * q, rank_of(w.x), rank_of(w.y), rank_of(w.z), rank_of(w.w));
+            }
+            for (uint32_t l = nq * 4 + lane; l < tn; l += 32) rank[base + l] = (OutT)rank_of(node_word[base + l]);
+        }
     }
-    for (unsigned long long i = nq * 4 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < N;
-         i += stride)
-        rank[i] = (OutT)rank_of(i, node_word[i]);
 }
 
 // contracted list links: segment s -> the segment whose head is succ(end(s))
@@ -2328,6 +2382,7 @@ struct RsBufs {
     uint32_t* toff = nullptr;              // rs5_refine tile layout: fine-bin offsets per refine tile
     uint32_t* tiles = nullptr;
     uint32_t* tiles_end = nullptr;
+    uint32_t* tiles_run = nullptr;  // per tile: 1 = a run of consecutive ids (census, contraction -> expand)
     uint32_t* tiles_up = nullptr;   // levels >= 1 (level 0's offsets stay for the contraction expand)
     uint32_t* spl[SG_MAX_LEVELS] = {};
     uint2* lvl[SG_MAX_LEVELS + 1] = {};
@@ -2354,6 +2409,7 @@ static bool carve_rs(Carver& c, uint64_t n, const RsPlan& p, RsBufs& b) {
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     b.tiles = c.take<uint32_t>(ntiles + 1);
     b.tiles_end = c.take<uint32_t>(ntiles + 1);
+    b.tiles_run = c.take<uint32_t>(ntiles + 1);
     b.tiles_up = c.take<uint32_t>((p.levels > 0 ? (p.cap[1] + TILE - 1) / TILE : 0) + 1);
     for (int k = 0; k < p.levels; ++k) {
         const unsigned long long cap = p.cap[k + 1];
@@ -2421,12 +2477,12 @@ static int wyllie_run(const SuccT* succ, OutT* rank, uint64_t n, int variant, Li
 template <class SuccT>
 static int launch_contract(uint32_t grid, cudaStream_t s, const SuccT* succ, ListStatus* st, const uint32_t* tile_off,
                            uint32_t* headsid, uint32_t* seg_head, uint32_t* seg_succ, uint2* lvl1,
-                           uint32_t* node_word) {
+                           uint32_t* node_word, uint32_t* tile_run) {
     const bool vec = ((uintptr_t)succ & 15) == 0;
     auto k = vec ? k_rs_contract<SuccT, true> : k_rs_contract<SuccT, false>;
     SG_CUDA(set_smem_max(k, sizeof(ContractSmem)));
     k<<<grid, TILE_THREADS, sizeof(ContractSmem), s>>>(succ, st, tile_off, headsid, seg_head, seg_succ, lvl1,
-                                                       node_word);
+                                                       node_word, tile_run);
     return SG_OK;
 }
 
@@ -2475,7 +2531,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             const uint32_t cmax = sm_count() * resident_ctas(kc, TILE_THREADS);
             const uint32_t cg = cw < cmax ? cw : cmax;
             rec.begin(K_RS_COUNT, 0, cg, TILE_THREADS, capN);
-            kc<<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0], p.salt[0]);
+            kc<<<cg, TILE_THREADS, 0, s>>>(succ, b.tiles, b.tiles_end, b.st, p.kbits[0], p.salt[0], b.tiles_run);
         } else {
             rec.begin(K_RS4_COUNT, k, nt, TILE_THREADS, capN);
             k_rs_count<uint32_t, false><<<nt, TILE_THREADS, 0, s>>>(nullptr, tk, b.st, k, p.kbits[k], p.salt[k], 1);
@@ -2531,7 +2587,7 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
             const uint32_t cg = nt < sm_count() * CT_CTAS_PER_SM ? nt : sm_count() * CT_CTAS_PER_SM;
             rec.begin(K_RS_CONTRACT, 0, cg, TILE_THREADS, capN);
             const int rc = launch_contract<SuccT>(cg, s, succ, b.st, b.tiles, b.rid, b.spl[0], b.IS[1], b.lvl[1],
-                                                  reinterpret_cast<uint32_t*>(b.word0));
+                                                  reinterpret_cast<uint32_t*>(b.word0), b.tiles_run);
             if (rc != SG_OK) return rc;
             rec.end();
             SG_LAUNCH_CHECK();
@@ -2622,10 +2678,10 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
         rec.begin(K_RS5_EXPAND, 0, eg, 256, n);
         if (((uintptr_t)rank & 15) == 0)
             k_rs_contract_expand<OutT, true><<<eg, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(b.word0), b.tiles,
-                                                                b.lvl[1], b.IS[1], rank, b.st);
+                                                                b.lvl[1], b.IS[1], rank, b.st, b.tiles_run);
         else
             k_rs_contract_expand<OutT, false><<<eg, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(b.word0), b.tiles,
-                                                                 b.lvl[1], b.IS[1], rank, b.st);
+                                                                 b.lvl[1], b.IS[1], rank, b.st, b.tiles_run);
         rec.end();
         SG_LAUNCH_CHECK();
     }

@@ -416,6 +416,46 @@ def test_full_size_properties_2_26(cuda, kind):
     assert torch.equal(w, rank)
 
 
+def _list_from_order(order):
+    succ = np.empty(order.size, dtype=np.int64)
+    succ[order[:-1]] = order[1:]
+    succ[order[-1]] = order[-1]
+    return succ
+
+
+def test_contraction_run_tiles(cuda, orc):
+    """Ordered tiles the census flags as runs (the contraction skips them)
+    next to locally shuffled and partial tiles, and defects next to runs."""
+    T = 4096
+    n = 10 * T + 123
+    rng = np.random.default_rng(11)
+    order = np.arange(n)
+    order[3 * T:4 * T] = 3 * T + rng.permutation(T)       # tile 3 shuffled inside
+    order[6 * T + 7:6 * T + 40] = order[6 * T + 7:6 * T + 40][::-1]  # a reversed stretch in tile 6
+    succ = _list_from_order(order)
+    want = orc.seq_rank(succ)
+    for arg in (succ, torch.from_numpy(succ.astype(np.int32)).cuda()):
+        rank, stats = g.rs_rank(g.SuccessorList(arg), 64)
+        assert stats.meta["path"] == "contract"
+        rank = rank.cpu().numpy() if isinstance(rank, torch.Tensor) else rank
+        assert np.array_equal(rank, want)
+    # defects beside run tiles: a back edge (in-degree 2 + cycle), a jump
+    # skipping a node, a tile whose successor leaves to a non-head
+    ordered = np.arange(1, n + 1, dtype=np.int64)
+    ordered[-1] = n - 1
+    bad = []
+    s = ordered.copy(); s[5 * T + 10] = 5 * T; bad.append(s)
+    s = ordered.copy(); s[7 * T - 1] = 7 * T + 1; bad.append(s)
+    s = ordered.copy(); s[2 * T + 5] = 8 * T + 3; bad.append(s)
+    for s in bad:
+        want = g.validate_list(g.SuccessorList(s))
+        assert want is not None
+        for arg in (s, torch.from_numpy(s.astype(np.int32)).cuda()):
+            with pytest.raises(g.InvalidListError) as ei:
+                g.rs_rank(g.SuccessorList(arg), 64)
+            assert str(ei.value) == str(want)
+
+
 def test_walk_cap_fallback(cuda, orc, sg_env):
     """A walk that exceeds the hop cap falls back to pointer jumping."""
     sg_env(SG_RS_WALK_CAP="4")
