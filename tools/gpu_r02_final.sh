@@ -27,6 +27,11 @@ for spec in lr28:'k_rs_count0|k_rs_select|k_rs_walk_bin|k_rs_refine_atom|k_rs_re
   IFS=: read -r wl kern name cnt <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kern" -c $cnt -o $O/prof_$name \
       python tools/prof_target.py $wl > $O/ncu_$name.log 2>&1
+  # summarise on the box (the reports together exceed gpurun's 64 MiB return limit)
+  python tools/ncu_summary.py $O/prof_$name.ncu-rep $wl r02_ncu_$name >> $O/ncu_$name.log 2>&1
+  cp profiles/r02_ncu_$name.txt $O/
+  case $name in cc*) rm -f $O/prof_$name.ncu-rep ;; esac
 done
+cp profiles/traffic.json $O/traffic.json
 fi
 ls -la $O
