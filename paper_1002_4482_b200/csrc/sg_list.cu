@@ -1507,6 +1507,55 @@ __global__ void __launch_bounds__(RA_THREADS, RA_CTAS_PER_SM) k_rs_refine_atom(
     if (over) st->bad = 1;
 }
 
+// rs5_refine + rs5_scatter in one pass (SG_RS_REFINE=7, experiment): every
+// record's rank (IS_1[sid] - local - 1, listrank.py:375-379) is stored
+// straight to rank[cur].  The records arrive binned by coarse window and the
+// blocks run roughly in index order, so the stores of the ~1-2 coarse windows
+// in flight (4-8 MiB of output) land in L2 and their sectors are complete
+// before eviction: no pairs buffer, no sort, no second pass -- at the price of
+// one L2 sector write per node next to the IS_1 gather.
+constexpr int RD_THREADS = 256;
+constexpr int RD_IT = 8;  // records per thread (four 16-B loads)
+template <class OutT>
+__global__ void __launch_bounds__(RD_THREADS) k_rs_refine_direct(const unsigned long long* __restrict__ in,
+                                                                 OutT* __restrict__ rank, const ListStatus* st,
+                                                                 unsigned long long n, uint32_t cshift,
+                                                                 const uint32_t* __restrict__ IS1, uint32_t sb,
+                                                                 uint32_t lb) {
+    if (layout_local(st) || ranks_invalid(st)) return;
+    const uint32_t R1 = (uint32_t)min(st->R[1], (unsigned long long)0xFFFFFFFFu);
+    const unsigned long long pol_last = l2_evict_last();
+    const uint32_t lmask = (1u << lb) - 1u;
+    const uint32_t smask = (uint32_t)((1ull << (sb - lb)) - 1);
+    const unsigned long long e0 = (unsigned long long)blockIdx.x * (RD_THREADS * RD_IT);
+    unsigned long long r[RD_IT];
+    uint32_t g[RD_IT];
+#pragma unroll
+    for (int j = 0; j < RD_IT / 2; ++j) {
+        const unsigned long long e = e0 + (unsigned long long)(j * RD_THREADS + threadIdx.x) * 2;
+        if (e + 1 < n) {
+            const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(in + e));
+            r[2 * j] = v.x;
+            r[2 * j + 1] = v.y;
+        } else {
+            r[2 * j] = e < n ? __ldcs(in + e) : ~0ull;
+            r[2 * j + 1] = ~0ull;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < RD_IT; ++j) {
+        const uint32_t sid = (uint32_t)(r[j] >> lb) & smask;
+        g[j] = ld_hint(IS1 + (sid < R1 ? sid : 0u), pol_last);
+    }
+#pragma unroll
+    for (int j = 0; j < RD_IT; ++j) {
+        const unsigned long long e = e0 + (unsigned long long)((j >> 1) * RD_THREADS + threadIdx.x) * 2 + (j & 1);
+        const unsigned long long cur = r[j] >> sb;
+        // padding / dropped slots hold ids outside the record's own coarse window
+        if (e < n && (cur >> cshift) == (e >> cshift)) rank[cur] = (OutT)(g[j] - ((uint32_t)r[j] & lmask) - 1u);
+    }
+}
+
 // rs5_scatter over the tile layout of k_rs_refine_lean<.., true>: one CTA
 // per fine window f (bin d of coarse window c) collects bin d's run from
 // each of the coarse window's tiles -- lane l of a warp reads the run bounds
@@ -2705,6 +2754,17 @@ static int rs_run(const SuccT* succ, OutT* rank, uint64_t n, const RsPlan& p, Rs
     // the lean refine keeps local (< walk cap) in 20 bits next to the 8-bit warp rank
     const bool lean_ok = p.fused && fbits_r <= 6 && p.rec_lb < 32 && p.walk_cap < (1u << 20);
     bool tiled = false;
+    if (p.fused && tu_r.rs_refine == 7) {  // one pass: ranks stored straight from the records
+        const unsigned long long per = (unsigned long long)RD_THREADS * RD_IT;
+        const uint32_t g = (uint32_t)((n + per - 1) / per);
+        rec.begin(K_RS5_REFINE, 0, g, RD_THREADS, n);
+        k_rs_refine_direct<OutT><<<g, RD_THREADS, 0, s>>>(b.pairs, rank, b.st, n, p.cshift, b.IS[1], p.rec_sb,
+                                                           p.rec_lb);
+        rec.end();
+        SG_LAUNCH_CHECK();
+        if (stats) stats->levels = (uint32_t)L;
+        return SG_OK;
+    }
     if (lean_ok && tu_r.rs_refine == 0 && ((1ull << p.cshift) % RA_TILE) == 0) {
         const size_t sma = ra_smem_bytes();  // (k_rs_refine_atom: staging + one sorted tile)
         SG_CUDA(set_smem_max(k_rs_refine_atom, sma));

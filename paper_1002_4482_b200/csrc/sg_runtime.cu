@@ -213,7 +213,7 @@ static Tuning read_tuning(uint32_t generation) {
     v.rs_topn = env_u32("SG_RS_TOPN", 1u << 20, 0, 1u << 30);
     v.rs_packed = env_u32("SG_RS_PACKED", 1, 0, 1);
     v.rs_fused = env_u32("SG_RS_FUSED", 1, 0, 1);
-    v.rs_refine = env_u32("SG_RS_REFINE", 0, 0, 6);  // rs5_refine variant (sg_list.cu)
+    v.rs_refine = env_u32("SG_RS_REFINE", 0, 0, 7);  // rs5_refine variant (sg_list.cu)
     v.cc_wbits = env_u32("SG_CC_WBITS", 0, 0, 31);
     const char* part = getenv("SG_CC_PART");
     v.cc_part_count = part && strcmp(part, "count") == 0;  // count + scatter instead of chunk lists

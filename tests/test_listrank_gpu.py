@@ -541,12 +541,12 @@ def test_plan_boundaries(cuda, orc, n):
     assert np.array_equal(out.cpu().numpy().astype(np.int64), want)
 
 
-@pytest.mark.parametrize("refine", ["0", "1", "2", "3", "4", "5", "6"])
+@pytest.mark.parametrize("refine", ["0", "1", "2", "3", "4", "5", "6", "7"])
 def test_refine_variants(cuda, orc, sg_env, refine):
     """rs5_refine variants (SG_RS_REFINE: 0 shared-atomic ranking, the
     default; 1 the block multisplit refine; 2 lean + match.any; 3 lean,
     alternating; 4 lean in the tile layout; 5 lean + shared atomics; 6 lean +
-    ballots) on
+    ballots; 7 ranks stored straight from the records, no rs5_scatter) on
     windows shrunk to 8 KiB (SG_RS_WIN_KB=8) so 2^20 nodes already split
     every coarse window into 8 fine bins and 2^25 nodes into 64 (the C3
     fan-out): exact against the oracle, and the size-independent rank
