@@ -23,7 +23,7 @@ tail -3 $O/pytest_gpu.log; tail -1 $O/smoke.log
 else
 for spec in lr28:'k_rs_count0|k_rs_select|k_rs_walk_bin|k_rs_refine_atom|k_rs_rec_scatter':lr28:7 \
             cc26:'k_cc_part_chunks|k_cc_hook_uf|k_cc_compress':cc26:10 \
-            lr28o:'k_rs_count0|k_rs_contract|k_rs_contract_expand':lr28o:3 cc22:'k_cc_hook_uf':cc22:1; do
+            lr28o:'k_rs_count0|k_rs_contract|k_rs_contract_expand':lr28o:4 cc22:'k_cc_hook_uf':cc22:1; do
   IFS=: read -r wl kern name cnt <<< "$spec"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$kern" -c $cnt -o $O/prof_$name \
       python tools/prof_target.py $wl > $O/ncu_$name.log 2>&1
