@@ -314,3 +314,35 @@ def test_c4_matches_reference_counts(cuda):
     counts = torch.bincount(labels.to(torch.int64), minlength=n)
     assert int((counts > 0).sum()) == 1_437
     assert int(counts.max()) == 4_192_867
+
+
+@pytest.mark.parametrize("split", ["0", "1", "3", "5", "3+1"])
+def test_uf_split_hook(cuda, orc, sg_env, split):
+    """Unpartitioned UF with a full shortcut sweep after the first m / 2^f rows
+    (SG_CC_SPLIT=f; 3 is the default, 0 one hook launch): labels exact on
+    random, tree, path and int64 / device-resident edge lists (the second hook
+    starts m1 rows in, so 16-B rows are offset correctly), the invalid row
+    reported by its global index from either half, and one more vertex sweep
+    counted per sweep when the split applies (m >= 2^16); "3+1" adds the
+    second sweep after m / 2 rows (SG_CC_SPLIT2)."""
+    f, _, f2 = split.partition("+")
+    sg_env(SG_CC_SPLIT=f, SG_CC_SPLIT2=f2 or "0")
+    cases = [g.gen_random_graph(1 << 16, 4.0 / (1 << 16), seed=11), g.gen_tree_graph(90_000, 3, seed=4),
+             g.list_to_graph(g.gen_list(70_001, seed=8)), g.gen_random_graph(5_000, 1e-3, seed=2)]
+    base = None
+    for gr in cases:
+        labels, stats = g.sv_components(gr, p=64, variant="uf")
+        assert np.array_equal(labels, orc.seq_components(gr.n, gr.edges)), (gr.n, gr.m, split)
+        if gr is cases[0]:
+            base = stats.meta["vertex_sweeps"]
+        d = torch.from_numpy(gr.edges.astype(np.int64)).to(cuda)  # int64 rows on the device
+        dl, _ = g.sv_components(g.EdgeGraph(gr.n, d), p=64, variant="uf")
+        assert np.array_equal(dl.cpu().numpy(), orc.seq_components(gr.n, gr.edges))
+    assert base == 2 + (f != "0") + (f2 != "")
+    e = cases[0].edges.copy()
+    m = len(e)
+    for row in (m // 64, m - 3):  # before and after the split point
+        bad = e.copy()
+        bad[row] = [5, 5]
+        with pytest.raises(g.InvalidGraphError, match=f"self-loop at edge {row}"):
+            g.sv_components(g.EdgeGraph(cases[0].n, bad), p=8, variant="uf")
