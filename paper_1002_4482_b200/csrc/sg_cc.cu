@@ -242,6 +242,67 @@ __global__ void __launch_bounds__(COMP_THREADS) k_cc_compress(uint32_t* D, unsig
     if (lane_id() == 0 && nroots && roots != nullptr) atomicAdd(roots, (unsigned long long)nroots);
 }
 
+// the same over four consecutive vertices per thread (16-B loads and stores
+// of D, four root chases in flight per thread); [lo, hi) starts 16-B aligned.
+// C5: 0.161 -> 0.089 ms (SG_CC_COMP4=1, default; pass x8)
+template <class OutT>
+__global__ void __launch_bounds__(COMP_THREADS) k_cc_compress4(uint32_t* D, unsigned long long lo,
+                                                               unsigned long long hi, unsigned long long* roots,
+                                                               OutT* out) {
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long nq = (hi - lo) >> 2;
+    uint4* D4 = reinterpret_cast<uint4*>(D + lo);
+    uint32_t nroots = 0;
+    for (unsigned long long q = t0; q < nq; q += stride) {
+        const uint4 p = D4[q];
+        const uint32_t i0 = (uint32_t)(lo + 4 * q);
+        uint32_t r[4] = {p.x, p.y, p.z, p.w};
+        bool live[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            live[j] = r[j] != i0 + (uint32_t)j;
+            nroots += live[j] ? 0u : 1u;
+        }
+        for (;;) {  // roots do not move during the shortcut
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (live[j]) {
+                    const uint32_t pp = ld_parent(D + r[j]);
+                    if (pp == r[j])
+                        live[j] = false;
+                    else
+                        r[j] = pp;
+                }
+                any |= live[j];
+            }
+            if (!any) break;
+        }
+        if (r[0] != p.x || r[1] != p.y || r[2] != p.z || r[3] != p.w) __stcg(D4 + q, make_uint4(r[0], r[1], r[2], r[3]));
+        if (out != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) out[lo + 4 * q + j] = (OutT)r[j];
+        }
+    }
+    for (unsigned long long i = lo + 4 * nq + t0; i < hi; i += stride) {  // the < 4 trailing vertices
+        uint32_t r = ld_parent(D + i);
+        if (r == (uint32_t)i) {
+            ++nroots;
+        } else {
+            for (;;) {
+                const uint32_t pp = ld_parent(D + r);
+                if (pp == r) break;
+                r = pp;
+            }
+            __stcg(D + i, r);
+        }
+        if (out != nullptr) out[i] = (OutT)r;
+    }
+    for (int o = 16; o > 0; o >>= 1) nroots += __shfl_xor_sync(0xffffffffu, nroots, o);
+    if (lane_id() == 0 && nroots && roots != nullptr) atomicAdd(roots, (unsigned long long)nroots);
+}
+
 template <class OutT>
 __global__ void __launch_bounds__(COMP_THREADS) k_cc_labels(const uint32_t* __restrict__ D, unsigned long long n,
                                                             OutT* __restrict__ out) {
@@ -960,6 +1021,18 @@ static int compress_dispatch(uint32_t* D, unsigned long long lo, unsigned long l
                              void* out, int odt, cudaStream_t s) {
     if (hi <= lo) return SG_OK;
     const uint32_t g = vtx_grid(hi - lo);
+    if (tuning().cc_comp4 && ((uintptr_t)(D + lo) & 15) == 0) {  // four vertices per thread
+        const uint32_t g4 = vtx_grid((hi - lo + 3) / 4);
+        if (out == nullptr || odt == SG_U32 || odt == SG_I32)
+            k_cc_compress4<uint32_t><<<g4, COMP_THREADS, 0, s>>>(D, lo, hi, roots,
+                                                                 out == (void*)D ? nullptr : (uint32_t*)out);
+        else if (odt == SG_I64)
+            k_cc_compress4<int64_t><<<g4, COMP_THREADS, 0, s>>>(D, lo, hi, roots, (int64_t*)out);
+        else
+            return SG_ERR_VALUE;
+        SG_LAUNCH_CHECK();
+        return SG_OK;
+    }
     if (out == nullptr || odt == SG_U32 || odt == SG_I32) {
         // u32 / i32 labels share D's bit pattern (ids < 2^31 for i32)
         k_cc_compress<uint32_t><<<g, COMP_THREADS, 0, s>>>(D, lo, hi, roots,

@@ -43,7 +43,7 @@ struct Tuning {
     uint32_t rs_win_kb, rs_kb0, rs_kb1, rs_fin, rs_walk_cap, rs_load_mode, rs_contract, rs_coop, rs_topn,
         rs_packed, rs_fused, rs_refine;
     // components (sg_cc.cu): window bits (0 = default), one-pass tile partition
-    uint32_t cc_wbits, cc_part_count, cc_rank_ballot, cc_split, cc_split2, cc_splitw;
+    uint32_t cc_wbits, cc_part_count, cc_rank_ballot, cc_split, cc_split2, cc_splitw, cc_comp4;
     // block multisplit peer ranking (sg_msplit.cuh): 0 match.any, 1 ballots, 2 alternate
     uint32_t ms_peers;
     uint32_t generation;  // bumped by every reload

@@ -217,6 +217,7 @@ static Tuning read_tuning(uint32_t generation) {
     v.cc_wbits = env_u32("SG_CC_WBITS", 0, 0, 31);
     v.cc_split = env_u32("SG_CC_SPLIT", 3, 0, 31);   // UF, unpartitioned: shortcut after m / 2^f rows (0: off)
     v.cc_split2 = env_u32("SG_CC_SPLIT2", 0, 0, 31);  // UF, unpartitioned: a second shortcut (experiment)
+    v.cc_comp4 = env_u32("SG_CC_COMP4", 1, 0, 1);  // cc_shortcut: four vertices per thread (0: one)
     v.cc_splitw = env_u32("SG_CC_SPLITW", 0, 0, 64);  // UF, partitioned: shortcut after k windows (experiment)
     const char* part = getenv("SG_CC_PART");
     v.cc_part_count = part && strcmp(part, "count") == 0;  // count + scatter instead of chunk lists

@@ -346,3 +346,22 @@ def test_uf_split_hook(cuda, orc, sg_env, split):
         bad[row] = [5, 5]
         with pytest.raises(g.InvalidGraphError, match=f"self-loop at edge {row}"):
             g.sv_components(g.EdgeGraph(cases[0].n, bad), p=8, variant="uf")
+
+
+@pytest.mark.parametrize("comp4", ["0", "1"])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_shortcut_widths(cuda, orc, sg_env, comp4, variant):
+    """cc_shortcut with one or four vertices per thread (SG_CC_COMP4): n not
+    a multiple of four (the trailing vertices), int64 labels from host input
+    (separate label buffer) and u32 labels in place on the device, the root
+    count in roots_per_round."""
+    sg_env(SG_CC_COMP4=comp4)
+    for gr in (g.gen_random_graph(100_003, 3e-5, seed=21), g.gen_tree_graph(50_001, 4, seed=3),
+               g.list_to_graph(g.gen_list(9_999, seed=5)), g.EdgeGraph(7, [[1, 2], [5, 6]])):
+        want = orc.seq_components(gr.n, gr.edges)
+        labels, st = g.sv_components(gr, p=min(64, gr.n), variant=variant)
+        assert np.array_equal(labels, want)
+        assert st.meta["roots_per_round"][-1] == int(np.count_nonzero(want == np.arange(gr.n)))
+        d = torch.from_numpy(gr.edges.astype(np.int32)).to(cuda)
+        dl, _ = g.sv_components(g.EdgeGraph(gr.n, d), p=min(64, gr.n), variant=variant)
+        assert np.array_equal(dl.cpu().numpy().astype(np.int64), want)
