@@ -3,7 +3,7 @@
 # line (lr28 + lr28o/lr26/cc22/cc26 blocks), the reference arm (lr28, cc26),
 # the ncu launch lists of lr28 and cc26 steps.  NCU=1: the ncu --set full
 # captures instead (summarise here with tools/ncu_summary.py).
-TAG=${TAG:-r02final6}
+TAG=${TAG:-r02final7}
 O=gpurun_out/$TAG
 mkdir -p $O
 python -c "import __graft_entry__ as e; e.build()" > $O/build.log 2>&1
