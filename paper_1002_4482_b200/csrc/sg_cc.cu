@@ -151,7 +151,10 @@ __global__ void __launch_bounds__(HOOK_THREADS) k_cc_hook_uf(E edges, unsigned l
     }
     // HU edges per iteration: 2*HU independent parent loads in flight (2 beats 4 and 8:
     // fewer unions racing for the same roots, measured)
-    constexpr int HU = 2;
+#ifndef CC_HOOK_HU
+#define CC_HOOK_HU 2
+#endif
+    constexpr int HU = CC_HOOK_HU;
     for (; i + (HU - 1) * stride < m; i += HU * stride) {
         unsigned long long u[HU], v[HU];
         bool ok[HU];
