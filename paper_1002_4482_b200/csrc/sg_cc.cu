@@ -544,7 +544,13 @@ __global__ void __launch_bounds__(MS_THREADS, PART2_CTAS_PER_SM) k_cc_part_scatt
 constexpr int CC_CHUNK_BITS = 10;
 constexpr uint32_t CC_CHUNK = 1u << CC_CHUNK_BITS;
 constexpr int PD_THREADS = 256;
-constexpr int PD_CTAS_PER_SM = 5;
+#ifndef CC_PD_CTAS
+#define CC_PD_CTAS 5
+#endif
+#ifndef CC_PD_G16
+#define CC_PD_G16 4
+#endif
+constexpr int PD_CTAS_PER_SM = CC_PD_CTAS;
 constexpr uint32_t PD_RING = 16;  // chunk ids of the last PD_RING chunks per window, in shared memory
 // 64-row groups per warp iteration: 4 rows per lane in flight (8 rows with 4
 // CTAs per SM measured slower: 1.60 vs 1.09 ms at C5)
@@ -676,7 +682,7 @@ __global__ void __launch_bounds__(PD_THREADS, PD_CTAS_PER_SM) k_cc_part_chunks(
     // kV16 (8-B rows, 16-B aligned): a lane loads rows 2l, 2l + 1 of a group
     // with one 16-B load, so four groups (eight rows, 64 B per lane) are in
     // flight for the registers the 8-B path spends on two
-    constexpr int G = kV16 ? 4 : PD_GROUPS;
+    constexpr int G = kV16 ? CC_PD_G16 : PD_GROUPS;
     constexpr int RL = 2 * G;
     const unsigned long long nw = (unsigned long long)gridDim.x * (PD_THREADS / 32);
     const unsigned long long ng = (m + 63) / 64;
